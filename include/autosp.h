@@ -1,0 +1,139 @@
+/*
+ * autosp.h — C ABI of libautosp.so, the B200 (sm_100a) hot path of AutoSP's
+ * Ulysses sequence parallelism.
+ *
+ * Plain pointers, sizes and an opaque `void* stream` (a cudaStream_t); no torch
+ * types.  Every call is stream-ordered on `stream`, never allocates, never
+ * synchronises the host, and returns an autosp_status.  The text of the last
+ * error on the calling thread is available from autosp_last_error().
+ *
+ * Each entry point replaces one reference interface (paths relative to
+ * /root/reference/pkg/src/seqcomp):
+ *
+ *   autosp_a2a            all_to_all_shards          executor.py:203-230
+ *                         DeviceGroup.submit/take     executor.py:244-275
+ *                         (the AllToAll node inserted by transform_sp, sp_pass.py:172-195,
+ *                          and its gradient, autodiff.py:252-262)
+ *   autosp_a2a_wait       DeviceGroup.ready           executor.py:267-268
+ *   autosp_symm_*         DeviceGroup(P) rendezvous   executor.py:233-242
+ *   autosp_attn_fwd       _eval_attention_core        executor.py:132-142
+ *                         (lowered recipe lowering.py:82-122)
+ *   autosp_attn_bwd       attention backward recipes  autodiff.py:156-162,190-195,213-214,
+ *                                                     executor.py:89-91
+ *   status codes          errors.py:4-29 (ValidationError/CollectiveError -> 2)
+ */
+#ifndef AUTOSP_H_
+#define AUTOSP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AUTOSP_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define AUTOSP_API __attribute__((visibility("default")))
+#else
+#define AUTOSP_API
+#endif
+
+typedef enum autosp_status {
+  AUTOSP_OK = 0,
+  AUTOSP_ERR_INTERNAL = 1,   /* SeqcompError (errors.py:4-5)                       */
+  AUTOSP_ERR_VALIDATION = 2, /* ValidationError / CollectiveError (errors.py:8-29)  */
+  AUTOSP_ERR_UNSUPPORTED = 3,/* shape outside what the sm_100a kernels implement     */
+  AUTOSP_ERR_CUDA = 5        /* CUDA runtime / driver failure                        */
+} autosp_status;
+
+typedef enum autosp_direction {
+  AUTOSP_SEQ_TO_HEAD = 0, /* "seq_to_head" (sp_pass.py:175-180) */
+  AUTOSP_HEAD_TO_SEQ = 1  /* "head_to_seq" (sp_pass.py:187-192) */
+} autosp_direction;
+
+AUTOSP_API int autosp_abi_version(void);
+AUTOSP_API const char* autosp_last_error(void);
+/* number of SMs / compute capability of the current device, -1 if no device */
+AUTOSP_API int autosp_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ------------------------------------------------------------------ symmetric memory
+ * One allocation per rank, identical size on every rank, mapped into every peer of the
+ * SP group once at dist.init (CUDA IPC over NVLink/NVSwitch).  The handle is an opaque
+ * 64-byte blob exchanged by the host (torch.distributed all_gather_object).           */
+#define AUTOSP_IPC_HANDLE_BYTES 64
+AUTOSP_API int autosp_symm_alloc(size_t bytes, void** dev_ptr, void* ipc_handle_out);
+AUTOSP_API int autosp_symm_open(const void* ipc_handle, void** dev_ptr);
+AUTOSP_API int autosp_symm_close(void* peer_ptr);
+AUTOSP_API int autosp_symm_free(void* dev_ptr);
+AUTOSP_API int autosp_memset_async(void* dev_ptr, int value, size_t bytes, void* stream);
+
+/* ------------------------------------------------------------------ all-to-all reshard
+ * One logical [b, s, h, d] tensor (head_dim d contiguous).  Strides are in ELEMENTS.
+ *   seq_to_head: the source is this rank's sequence shard [b, s/P, h, d]; rank j receives
+ *                heads [j*h/P, (j+1)*h/P) of every token, written at sequence offset
+ *                rank*s/P of its destination [b, s, h/P, d].
+ *   head_to_seq: the source is this rank's head block [b, s, h, d] (h = local heads);
+ *                rank j receives tokens [j*s/P, (j+1)*s/P) written at head offset rank*h
+ *                of its destination [b, s/P, h*P, d].
+ * `dst_offset` is the byte offset of the destination tensor inside every rank's symmetric
+ * receive region (identical on all ranks); dst strides describe that destination, so
+ * the QKV-projection and O-projection layout transposes fold into the copy.          */
+typedef struct autosp_a2a_tensor {
+  const void* src;
+  int64_t src_stride_b, src_stride_s, src_stride_h;
+  int64_t dst_offset;
+  int64_t dst_stride_b, dst_stride_s, dst_stride_h;
+  int32_t heads; /* h of the SOURCE logical tensor */
+  int32_t _pad;
+} autosp_a2a_tensor;
+
+#define AUTOSP_A2A_MAX_TENSORS 4
+#define AUTOSP_MAX_WORLD 8
+#define AUTOSP_FLAG_WORDS 64 /* uint32 words of one rank's flag block */
+
+/* Push this rank's slabs of up to 4 tensors straight into every peer's receive region
+ * (16-byte vector stores over NVLink; the local slab is a local copy), then publish
+ * `epoch` in every peer's flag block.  peer_base[j] / peer_flags[j] are rank j's
+ * receive region / flag block as mapped in THIS process (peer_flags[rank] is local).
+ * Before writing into rank j the kernel waits until rank j has itself reached `epoch`
+ * (its previous readers of the region are stream-ordered before that point).
+ * epoch must increase by one per call, identically on every rank.                   */
+AUTOSP_API int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n_tensors, int b,
+               int s_global, int d, int elem_bytes, int world, int rank,
+               void* const* peer_base, uint32_t* const* peer_flags, uint32_t epoch,
+               void* stream);
+/* Stream-ordered wait until every peer has published `epoch` into this rank's flag
+ * block (the receive region then holds the complete a2a output).                    */
+AUTOSP_API int autosp_a2a_wait(uint32_t* local_flags, int world, int rank, uint32_t epoch, void* stream);
+/* Single-process loopback used by tests / benchmarks on one GPU: marks `epoch` as reached
+ * for all `world` virtual ranks whose flag blocks are given.                           */
+AUTOSP_API int autosp_a2a_mark_ready(uint32_t* const* flags, int world, uint32_t epoch, void* stream);
+
+/* ------------------------------------------------------------------ causal attention
+ * q [b, hq, s, d], k/v [b, hkv, s, d] as strided views (d contiguous, element strides in
+ * (b, h, s) order; 16-byte aligned), bf16.  GQA: q head i reads kv head i / (hq/hkv).
+ * o is written in the same convention; lse [b, hq, s] fp32 (natural log of the row sum
+ * of exp(scale * q.k) over unmasked keys).  d in {32, 64, 128}.                      */
+typedef struct autosp_attn_tensor {
+  const void* ptr;
+  int64_t stride_b, stride_h, stride_s;
+} autosp_attn_tensor;
+
+AUTOSP_API int autosp_attn_fwd(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
+                    autosp_attn_tensor o, float* lse, int b, int hq, int hkv, int s, int d,
+                    float scale, int causal, void* stream);
+
+/* fp32 workspace the backward needs: dq accumulator [b, hq, s, d] + delta [b, hq, s] */
+AUTOSP_API size_t autosp_attn_bwd_workspace_bytes(int b, int hq, int s, int d);
+AUTOSP_API int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
+                    autosp_attn_tensor o, autosp_attn_tensor d_o, const float* lse,
+                    autosp_attn_tensor dq, autosp_attn_tensor dk, autosp_attn_tensor dv,
+                    void* workspace, int b, int hq, int hkv, int s, int d, float scale,
+                    int causal, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AUTOSP_H_ */

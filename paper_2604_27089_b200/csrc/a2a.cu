@@ -1,0 +1,311 @@
+// K1 / K2: the Ulysses all-to-all reshard as ONE push kernel over NVLink/NVSwitch peer
+// memory.  Semantics = all_to_all_shards (reference executor.py:203-230): a pure index
+// permutation, so the result is bit-exact.
+//
+// Design (B200):
+//  * every rank PUSHES its slabs straight into each peer's symmetric receive region
+//    (mapped once via CUDA IPC) with 16-byte vector stores; no staging, no NCCL;
+//  * source/destination are arbitrary (b, s, h) strided views with head_dim contiguous,
+//    so the QKV-projection output [b, s/P, (hq+2hkv)*d] is read in place and written as
+//    the head-major [b, h/P, s, d] attention operand (the transpose is folded in), and
+//    the attention output is written back as the token-major O-projection input;
+//  * a warp owns (tensor, batch, head, 16-token tile): source rows are 128B-line
+//    coalesced, destination rows of consecutive tokens are contiguous, loads are issued
+//    in a batch before the stores (latency of remote HBM is hidden by MLP);
+//  * cross-GPU ordering with two epoch flags per rank and no host synchronisation:
+//    "ready" (I have reached call e: my readers of older data are stream-ordered
+//    before me) and "arrive[src]" (src finished writing call e into me).  All spins are
+//    bounded by %globaltimer and trap instead of hanging the GPU.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/autosp.h"
+#include "ptx.cuh"
+
+namespace autosp {
+
+constexpr int kReadyWord = 0;
+constexpr int kArriveWord = 16;   // + src rank
+constexpr int kCounterWord = 48;  // CTA completion counter (local use only)
+constexpr int kTileTokens = 16;
+constexpr int kA2AThreads = 256;
+
+struct A2ATensorDev {
+  const char* src;
+  int64_t ss_b, ss_s, ss_h;  // element strides
+  int64_t dst_off;           // bytes
+  int64_t ds_b, ds_s, ds_h;  // element strides
+  int heads;
+  int tiles;                 // token tiles of the source
+  int64_t items;             // b * heads * tiles
+};
+
+struct A2AParams {
+  A2ATensorDev t[AUTOSP_A2A_MAX_TENSORS];
+  int n;
+  int dir;
+  int b, s_loc, s_glob, d, eb;
+  int P, rank;
+  char* peer_base[AUTOSP_MAX_WORLD];
+  uint32_t* peer_flags[AUTOSP_MAX_WORLD];
+  uint32_t epoch;
+  int64_t total_items;
+};
+
+AUTOSP_DEV bool epoch_reached(uint32_t v, uint32_t e) { return (int32_t)(v - e) >= 0; }
+
+AUTOSP_DEV void spin_until_epoch(const uint32_t* p, uint32_t e) {
+  if (epoch_reached(ld_acquire_sys(p), e)) return;
+  uint64_t t0 = globaltimer();
+  while (!epoch_reached(ld_acquire_sys(p), e)) {
+    if (globaltimer() - t0 > 10000000000ull) asm volatile("trap;");
+    __nanosleep(64);
+  }
+}
+
+// G = bytes moved per lane per row-chunk (16, 8, 4 or 2).
+template <typename V>
+__global__ void __launch_bounds__(kA2AThreads) a2a_push_kernel(const __grid_constant__ A2AParams p) {
+  constexpr int G = sizeof(V);
+  const int tid = threadIdx.x;
+  // 0) publish "I reached epoch" and wait for every peer to have reached it too
+  if (tid == 0) st_release_sys(p.peer_flags[p.rank] + kReadyWord, p.epoch);
+  if (tid < p.P && tid != p.rank) spin_until_epoch(p.peer_flags[tid] + kReadyWord, p.epoch);
+  __syncthreads();
+
+  const int vpr = p.d * p.eb / G;  // vectors per row (1..32)
+  const int rows_per_pass = min(32 / vpr, kTileTokens);
+  const int lane = tid & 31;
+  const int r_in_pass = lane / vpr;
+  const int v_in_row = lane % vpr;
+  const bool lane_active = r_in_pass < rows_per_pass;
+  const int warps_total = gridDim.x * (kA2AThreads / 32);
+  const int64_t gw = (int64_t)blockIdx.x * (kA2AThreads / 32) + (tid >> 5);
+
+  for (int64_t item = gw; item < p.total_items; item += warps_total) {
+    int ti = 0;
+    int64_t it = item;
+    while (ti < p.n - 1 && it >= p.t[ti].items) { it -= p.t[ti].items; ++ti; }
+    const A2ATensorDev& T = p.t[ti];
+    const int tile = (int)(it % T.tiles);
+    const int64_t bh = it / T.tiles;
+    const int hh = (int)(bh % T.heads);
+    const int bi = (int)(bh / T.heads);
+    const int s_src = (p.dir == AUTOSP_SEQ_TO_HEAD) ? p.s_loc : p.s_glob;
+    const int t0 = tile * kTileTokens;
+    const int hl = T.heads / p.P;  // seq_to_head: heads per destination rank
+
+    constexpr int kMaxPass = kTileTokens;  // vpr==32 -> 1 row per pass
+    V vals[kMaxPass];
+    const int passes = (kTileTokens + rows_per_pass - 1) / rows_per_pass;
+#pragma unroll
+    for (int ps = 0; ps < kMaxPass; ++ps) {
+      if (ps < passes) {
+        const int t = t0 + ps * rows_per_pass + r_in_pass;
+        if (lane_active && t < s_src) {
+          const char* src = T.src + ((int64_t)bi * T.ss_b + (int64_t)t * T.ss_s +
+                                     (int64_t)hh * T.ss_h) * p.eb;
+          vals[ps] = __ldg(reinterpret_cast<const V*>(src) + v_in_row);
+        }
+      }
+    }
+#pragma unroll
+    for (int ps = 0; ps < kMaxPass; ++ps) {
+      if (ps < passes) {
+        const int t = t0 + ps * rows_per_pass + r_in_pass;
+        if (lane_active && t < s_src) {
+          int j, dt, dh;
+          if (p.dir == AUTOSP_SEQ_TO_HEAD) {
+            j = hh / hl; dt = p.rank * p.s_loc + t; dh = hh - j * hl;
+          } else {
+            j = t / p.s_loc; dt = t - j * p.s_loc; dh = p.rank * T.heads + hh;
+          }
+          char* dst = p.peer_base[j] + T.dst_off +
+                      ((int64_t)bi * T.ds_b + (int64_t)dt * T.ds_s + (int64_t)dh * T.ds_h) * p.eb;
+          reinterpret_cast<V*>(dst)[v_in_row] = vals[ps];
+        }
+      }
+    }
+  }
+
+  // 1) completion: make this thread's (remote) stores visible system-wide, then the
+  //    last CTA publishes arrive[rank] = epoch in every peer's flag block.
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t* ctr = p.peer_flags[p.rank] + kCounterWord;
+    const uint32_t old = atom_add_acqrel_gpu(ctr, 1u);
+    if (old == gridDim.x - 1) {
+      *ctr = 0u;
+      __threadfence_system();
+      for (int j = 0; j < p.P; ++j)
+        if (j != p.rank) st_release_sys(p.peer_flags[j] + kArriveWord + p.rank, p.epoch);
+    }
+  }
+}
+
+__global__ void a2a_wait_kernel(uint32_t* flags, int P, int rank, uint32_t epoch) {
+  const int j = threadIdx.x;
+  if (j < P && j != rank) spin_until_epoch(flags + kArriveWord + j, epoch);
+  __syncthreads();
+}
+
+struct MarkParams {
+  uint32_t* flags[AUTOSP_MAX_WORLD];
+  int P;
+  uint32_t epoch;
+};
+__global__ void a2a_mark_ready_kernel(const __grid_constant__ MarkParams m) {
+  const int j = threadIdx.x;
+  if (j < m.P) st_release_sys(m.flags[j] + kReadyWord, m.epoch);
+}
+
+}  // namespace autosp
+
+// ---------------------------------------------------------------------------- C ABI
+extern "C" void autosp_set_error(const char* fmt, ...);
+
+extern "C" int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n_tensors, int b,
+                          int s_global, int d, int elem_bytes, int world, int rank,
+                          void* const* peer_base, uint32_t* const* peer_flags, uint32_t epoch,
+                          void* stream) {
+  using namespace autosp;
+  if (direction != AUTOSP_SEQ_TO_HEAD && direction != AUTOSP_HEAD_TO_SEQ) {
+    autosp_set_error("unknown all-to-all direction %d", direction);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (world < 1 || world > AUTOSP_MAX_WORLD || rank < 0 || rank >= world) {
+    autosp_set_error("world %d / rank %d out of range (max world %d)", world, rank,
+                     AUTOSP_MAX_WORLD);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (n_tensors < 1 || n_tensors > AUTOSP_A2A_MAX_TENSORS || !tensors) {
+    autosp_set_error("n_tensors %d out of range", n_tensors);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (b < 1 || s_global < 1 || d < 1 || (elem_bytes != 2 && elem_bytes != 4 && elem_bytes != 8)) {
+    autosp_set_error("bad shape b=%d s=%d d=%d elem_bytes=%d", b, s_global, d, elem_bytes);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (s_global % world) {
+    autosp_set_error("sequence %d not divisible by world size %d", s_global, world);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (!peer_base || !peer_flags) {
+    autosp_set_error("peer_base / peer_flags must be non-null");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  A2AParams p{};
+  p.n = n_tensors;
+  p.dir = direction;
+  p.b = b;
+  p.s_glob = s_global;
+  p.s_loc = s_global / world;
+  p.d = d;
+  p.eb = elem_bytes;
+  p.P = world;
+  p.rank = rank;
+  p.epoch = epoch;
+  for (int j = 0; j < world; ++j) {
+    p.peer_base[j] = static_cast<char*>(peer_base[j]);
+    p.peer_flags[j] = peer_flags[j];
+    if (!p.peer_base[j] || !p.peer_flags[j]) {
+      autosp_set_error("peer %d base/flags pointer is null", j);
+      return AUTOSP_ERR_VALIDATION;
+    }
+  }
+  // widest vector that divides every row / stride / pointer
+  uint64_t align = (uint64_t)d * elem_bytes;
+  auto fold = [&](uint64_t v) { while (align > 1 && (v % align)) align >>= 1; };
+  for (int j = 0; j < world; ++j) fold((uint64_t)(uintptr_t)p.peer_base[j]);
+  const int s_src = direction == AUTOSP_SEQ_TO_HEAD ? p.s_loc : s_global;
+  p.total_items = 0;
+  for (int i = 0; i < n_tensors; ++i) {
+    const autosp_a2a_tensor& T = tensors[i];
+    if (T.heads < 1 || !T.src) {
+      autosp_set_error("tensor %d: heads must be positive and src non-null", i);
+      return AUTOSP_ERR_VALIDATION;
+    }
+    if (direction == AUTOSP_SEQ_TO_HEAD && T.heads % world) {
+      autosp_set_error("heads %d not divisible by world size %d", T.heads, world);
+      return AUTOSP_ERR_VALIDATION;
+    }
+    A2ATensorDev& D = p.t[i];
+    D.src = static_cast<const char*>(T.src);
+    D.ss_b = T.src_stride_b; D.ss_s = T.src_stride_s; D.ss_h = T.src_stride_h;
+    D.dst_off = T.dst_offset;
+    D.ds_b = T.dst_stride_b; D.ds_s = T.dst_stride_s; D.ds_h = T.dst_stride_h;
+    D.heads = T.heads;
+    D.tiles = (s_src + kTileTokens - 1) / kTileTokens;
+    D.items = (int64_t)b * T.heads * D.tiles;
+    p.total_items += D.items;
+    fold((uint64_t)(uintptr_t)T.src);
+    fold((uint64_t)T.dst_offset);
+    for (int64_t st : {T.src_stride_b, T.src_stride_s, T.src_stride_h, T.dst_stride_b,
+                       T.dst_stride_s, T.dst_stride_h})
+      fold((uint64_t)(st < 0 ? -st : st) * elem_bytes);
+  }
+  if (align > 16) align = 16;
+  const uint64_t row = (uint64_t)d * elem_bytes;
+  if (row / align > 32) {
+    autosp_set_error("row of %llu bytes needs >32 lanes at %llu-byte granularity (unsupported)",
+                     (unsigned long long)row, (unsigned long long)align);
+    return AUTOSP_ERR_UNSUPPORTED;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t warps_needed = p.total_items;
+  int64_t blocks = (warps_needed + (kA2AThreads / 32) - 1) / (kA2AThreads / 32);
+  const int64_t max_blocks = (int64_t)sms * 4;
+  if (blocks > max_blocks) blocks = max_blocks;
+  if (blocks < 1) blocks = 1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (align) {
+    case 16: a2a_push_kernel<uint4><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
+    case 8: a2a_push_kernel<uint2><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
+    case 4: a2a_push_kernel<uint32_t><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
+    default: a2a_push_kernel<uint16_t><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    autosp_set_error("a2a launch failed: %s", cudaGetErrorString(e));
+    return AUTOSP_ERR_CUDA;
+  }
+  return AUTOSP_OK;
+}
+
+extern "C" int autosp_a2a_wait(uint32_t* local_flags, int world, int rank, uint32_t epoch,
+                               void* stream) {
+  if (!local_flags || world < 1 || world > AUTOSP_MAX_WORLD || rank < 0 || rank >= world) {
+    autosp_set_error("bad a2a_wait arguments (world %d rank %d)", world, rank);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (world == 1) return AUTOSP_OK;
+  autosp::a2a_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(local_flags, world,
+                                                                          rank, epoch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    autosp_set_error("a2a_wait launch failed: %s", cudaGetErrorString(e));
+    return AUTOSP_ERR_CUDA;
+  }
+  return AUTOSP_OK;
+}
+
+extern "C" int autosp_a2a_mark_ready(uint32_t* const* flags, int world, uint32_t epoch,
+                                     void* stream) {
+  if (!flags || world < 1 || world > AUTOSP_MAX_WORLD) {
+    autosp_set_error("bad mark_ready arguments");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  autosp::MarkParams m{};
+  for (int j = 0; j < world; ++j) m.flags[j] = flags[j];
+  m.P = world;
+  m.epoch = epoch;
+  autosp::a2a_mark_ready_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(m);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    autosp_set_error("mark_ready launch failed: %s", cudaGetErrorString(e));
+    return AUTOSP_ERR_CUDA;
+  }
+  return AUTOSP_OK;
+}

@@ -1,0 +1,423 @@
+// K3: causal flash-attention forward on the local head block over the FULL gathered
+// sequence (the AttentionCore after the seq->head all-to-all; reference semantics
+// executor.py:132-142 / lowering.py:82-122: softmax(q k^T / sqrt(d) + M) v with M the
+// strictly-upper-triangular mask), written for sm_100a:
+//
+//  * one CTA = one (batch, q head, 256-query block) processed as two 128-row Q tiles that
+//    ping-pong on the tensor core (while softmax works on tile 0, the MMA runs tile 1);
+//  * warp 0: TMA producer (Q once, then a K/V ring of kStages 128-key tiles, 128B swizzle);
+//  * warp 1: single-thread tcgen05.mma issuer: S_i = Q_i K^T (SS, M=128,N=128) into TMEM,
+//    O_i += P_i V (TS: P read straight from TMEM, V MN-major from smem);
+//  * warps 4-7 / 8-11: softmax warpgroups, one query row per thread (TMEM lane), online
+//    softmax in the log2 domain with lazy O rescaling (only when the row max grows by
+//    more than 2^8), P written back to TMEM as bf16 aliasing S;
+//  * causal: KV tiles above the diagonal are never loaded; only the diagonal tile masks;
+//  * outputs O (bf16) and the natural-log LSE per row (what sp_ac saves instead of the
+//    O(s^2) probabilities, SURVEY §0 finding 3).
+#include <cmath>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/autosp.h"
+#include "ptx.cuh"
+#include "tma.cuh"
+
+extern "C" void autosp_set_error(const char* fmt, ...);
+
+namespace autosp {
+namespace fwd {
+
+constexpr int BM = 128;  // query rows per tile
+constexpr int BN = 128;  // keys per tile
+constexpr int kThreads = 384;
+constexpr int kSoftmaxWarp0 = 4;
+
+template <int D>
+struct Cfg {
+  static constexpr int SW = (D * 2 >= 128) ? 128 : D * 2;  // swizzle bytes
+  static constexpr int CE = SW / 2;                         // elements per swizzle chunk
+  static constexpr int NCH = D / CE;                        // chunks per row
+  static constexpr int TILE_BYTES = BM * D * 2;             // 128 x D bf16
+  static constexpr int kStages = D == 128 ? 2 : (D == 64 ? 3 : 4);
+  static constexpr int LAYOUT = SW == 128 ? 2 : (SW == 64 ? 4 : 6);
+  static constexpr int SBO = 8 * SW;  // 8-row swizzle atom
+  // smem: Q[2] | K[kStages] | V[kStages] | barriers
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = 2 * TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + kStages * TILE_BYTES;
+  static constexpr int BAR_OFF = V_OFF + kStages * TILE_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;  // + alignment slack
+  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr uint32_t S_COL = 0;      // S_i at i*128
+  static constexpr uint32_t O_COL = 256;    // O_i at 256 + i*D
+};
+
+struct Params {
+  CUtensorMap tm_q, tm_k, tm_v;
+  __nv_bfloat16* o;
+  int64_t o_sb, o_sh, o_ss;
+  float* lse;
+  int B, Hq, Hkv, S;
+  float scale_log2;
+  int causal;
+  int n_qblk;
+};
+
+// K-major operand tile [128 rows x D] stored as NCH swizzled chunks of [128 x SW bytes].
+template <int D>
+AUTOSP_DEV uint64_t desc_kmajor(uint32_t tile_saddr, int kk) {
+  using C = Cfg<D>;
+  const int e = kk * 16;  // element offset along K
+  const uint32_t addr = tile_saddr + (e / C::CE) * (BM * C::SW) + (e % C::CE) * 2;
+  return make_smem_desc(addr, 16, C::SBO, C::LAYOUT);
+}
+// MN-major B operand V [128 keys x D] (N = D contiguous), K-step kk covers 16 keys.
+template <int D>
+AUTOSP_DEV uint64_t desc_v(uint32_t tile_saddr, int kk) {
+  using C = Cfg<D>;
+  const uint32_t addr = tile_saddr + kk * 16 * C::SW;
+  return make_smem_desc(addr, BN * C::SW /*LBO: next D chunk*/, C::SBO, C::LAYOUT);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ Params p) {
+  using C = Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + C::kStages;
+  uint64_t* v_full = k_empty + C::kStages;
+  uint64_t* v_empty = v_full + C::kStages;
+  uint64_t* s_full = v_empty + C::kStages;  // [2]
+  uint64_t* p_full = s_full + 2;            // [2]
+  uint64_t* o_done = p_full + 2;            // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int qblk = p.n_qblk - 1 - blockIdx.x;  // heaviest causal blocks first
+  const int head = blockIdx.y;
+  const int batch = blockIdx.z;
+  const int kvhead = head / (p.Hq / p.Hkv);
+  const int q0 = qblk * 2 * BM;
+  const int n_kv_total = (p.S + BN - 1) / BN;
+  int n_tiles[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int last_row = min(q0 + (i + 1) * BM, p.S) - 1;
+    n_tiles[i] = p.causal ? min(last_row / BN + 1, n_kv_total) : n_kv_total;
+    if (q0 + i * BM >= p.S) n_tiles[i] = 0;
+  }
+  const int n_max = max(n_tiles[0], n_tiles[1]);
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(p_full + i, 128);
+      mbar_init(o_done + i, 1);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&p.tm_q);
+    tma_prefetch_desc(&p.tm_k);
+    tma_prefetch_desc(&p.tm_v);
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const uint32_t sq = smem_u32(smem + C::Q_OFF);
+  const uint32_t sk = smem_u32(smem + C::K_OFF);
+  const uint32_t sv = smem_u32(smem + C::V_OFF);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && n_max > 0) {
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_last();
+      mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
+      for (int i = 0; i < 2; ++i)
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_4d(smem + C::Q_OFF + i * C::TILE_BYTES + c * BM * C::SW, &p.tm_q, q_full,
+                      c * C::CE, q0 + i * BM, head, batch, pol_q);
+      for (int j = 0; j < n_max; ++j) {
+        const int st = j % C::kStages;
+        const uint32_t ph = (j / C::kStages) & 1;
+        mbar_wait(k_empty + st, ph ^ 1);
+        mbar_arrive_expect_tx(k_full + st, C::TILE_BYTES);
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_4d(smem + C::K_OFF + st * C::TILE_BYTES + c * BN * C::SW, &p.tm_k,
+                      k_full + st, c * C::CE, j * BN, kvhead, batch, pol_kv);
+        mbar_wait(v_empty + st, ph ^ 1);
+        mbar_arrive_expect_tx(v_full + st, C::TILE_BYTES);
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_4d(smem + C::V_OFF + st * C::TILE_BYTES + c * BN * C::SW, &p.tm_v,
+                      v_full + st, c * C::CE, j * BN, kvhead, batch, pol_kv);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && n_max > 0) {
+      constexpr uint32_t idesc_qk = make_idesc_bf16(BM, BN, 0, 0);
+      constexpr uint32_t idesc_pv = make_idesc_bf16(BM, D, 0, 1);
+      auto issue_qk = [&](int i, int j) {
+        const int st = j % C::kStages;
+        const uint32_t qa = sq + i * C::TILE_BYTES;
+        const uint32_t kb = sk + st * C::TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_ss(tmem + C::S_COL + i * BN, desc_kmajor<D>(qa, kk), desc_kmajor<D>(kb, kk),
+                 idesc_qk, kk > 0);
+        tc_commit(s_full + i);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(k_full + 0, 0);
+      tc_fence_after();
+      for (int i = 0; i < 2; ++i)
+        if (n_tiles[i] > 0) issue_qk(i, 0);
+      tc_commit(k_empty + 0);
+      for (int j = 0; j < n_max; ++j) {
+        const int st = j % C::kStages;
+        const uint32_t ph = (j / C::kStages) & 1;
+        const bool next = j + 1 < n_max;
+        const int st1 = (j + 1) % C::kStages;
+        const uint32_t ph1 = ((j + 1) / C::kStages) & 1;
+        mbar_wait(v_full + st, ph);
+        bool k_next_ready = false;
+        for (int i = 0; i < 2; ++i) {
+          if (j >= n_tiles[i]) continue;
+          mbar_wait(p_full + i, j & 1);
+          tc_fence_after();
+          const uint32_t vb = sv + st * C::TILE_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            mma_ts(tmem + C::O_COL + i * D, tmem + C::S_COL + i * BN + kk * 8, desc_v<D>(vb, kk),
+                   idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(o_done + i);
+          if (j + 1 < n_tiles[i]) {
+            if (!k_next_ready) {
+              mbar_wait(k_full + st1, ph1);
+              tc_fence_after();
+              k_next_ready = true;
+            }
+            issue_qk(i, j + 1);
+          }
+        }
+        tc_commit(v_empty + st);
+        if (next) {
+          if (!k_next_ready) {  // K_{j+1} loaded but unused by either tile: still release it
+            mbar_wait(k_full + st1, ph1);
+          }
+          tc_commit(k_empty + st1);
+        }
+      }
+    }
+  } else if (warp >= kSoftmaxWarp0) {
+    // ------------------------------------------------------------ softmax warpgroups
+    const int i = (warp - kSoftmaxWarp0) / 4;  // Q tile
+    const int quarter = warp & 3;              // TMEM lane quarter
+    const int row = quarter * 32 + lane;
+    const int qi = q0 + i * BM + row;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t s_addr = tmem + lane_base + C::S_COL + i * BN;
+    const uint32_t o_addr = tmem + lane_base + C::O_COL + i * D;
+    const int n = n_tiles[i];
+    float m = -INFINITY;  // running max in log2 units
+    float l = 0.f;
+    for (int j = 0; j < n; ++j) {
+      mbar_wait(s_full + i, j & 1);
+      tc_fence_after();
+      uint32_t sr[BN];
+      tmem_ld32(s_addr + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tmem_ld32(s_addr + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
+      tmem_ld32(s_addr + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
+      tmem_wait_ld();
+      float* s = reinterpret_cast<float*>(sr);
+      const int k0 = j * BN;
+      const bool need_mask = (p.causal && k0 + BN - 1 > q0 + i * BM) || (k0 + BN > p.S);
+      if (need_mask) {
+        const int lim = p.causal ? min(qi + 1, p.S) : p.S;  // keys < lim are valid
+#pragma unroll
+        for (int c = 0; c < BN; ++c)
+          if (k0 + c >= lim) s[c] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int c = 1; c < BN; ++c) mx = fmaxf(mx, s[c]);
+      const float m_cand = mx * p.scale_log2;
+      float alpha = 1.f;
+      bool rescale = false;
+      if (m_cand > m + 8.f) {  // lazy rescale (also taken on the first tile)
+        alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - m_cand);
+        rescale = (j > 0);
+        m = m_cand;
+      }
+      const float moff = (m == -INFINITY) ? 0.f : m;
+      float rs = 0.f;
+#pragma unroll
+      for (int c4 = 0; c4 < BN / 32; ++c4) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const float a = fast_exp2(fmaf(s[c4 * 32 + 2 * c], p.scale_log2, -moff));
+          const float b = fast_exp2(fmaf(s[c4 * 32 + 2 * c + 1], p.scale_log2, -moff));
+          rs += a + b;
+          pk[c] = pack_bf16(a, b);
+        }
+        tmem_st16(s_addr + c4 * 16, pk);
+      }
+      if (__any_sync(0xffffffffu, rescale)) {
+        // O holds tiles < j: wait for the PV of tile j-1 before touching it
+        mbar_wait(o_done + i, (j - 1) & 1);
+        tc_fence_after();
+        if (rescale) {
+#pragma unroll
+          for (int c = 0; c < D; c += 32) {
+            uint32_t orr[32];
+            tmem_ld32(o_addr + c, orr);
+            tmem_wait_ld();
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+              orr[t] = __float_as_uint(__uint_as_float(orr[t]) * alpha);
+            tmem_st32(o_addr + c, orr);
+          }
+        }
+      }
+      l = l * alpha + rs;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full + i);
+    }
+    // ---- epilogue: O / l -> bf16, LSE
+    if (n > 0) {
+      mbar_wait(o_done + i, (n - 1) & 1);
+      tc_fence_after();
+      const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
+      __nv_bfloat16* orow = p.o + (int64_t)batch * p.o_sb + (int64_t)head * p.o_sh +
+                            (int64_t)qi * p.o_ss;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t orr[32];
+        tmem_ld32(o_addr + c, orr);
+        tmem_wait_ld();
+        if (qi < p.S) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(orr[8 * t + 0]) * inv_l,
+                            __uint_as_float(orr[8 * t + 1]) * inv_l);
+            v.y = pack_bf16(__uint_as_float(orr[8 * t + 2]) * inv_l,
+                            __uint_as_float(orr[8 * t + 3]) * inv_l);
+            v.z = pack_bf16(__uint_as_float(orr[8 * t + 4]) * inv_l,
+                            __uint_as_float(orr[8 * t + 5]) * inv_l);
+            v.w = pack_bf16(__uint_as_float(orr[8 * t + 6]) * inv_l,
+                            __uint_as_float(orr[8 * t + 7]) * inv_l);
+            dst[t] = v;
+          }
+        }
+      }
+      if (qi < p.S)
+        p.lse[((int64_t)batch * p.Hq + head) * p.S + qi] =
+            (m + __log2f(l)) * 0.69314718055994531f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+template <int D>
+int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autosp_attn_tensor& v,
+           const autosp_attn_tensor& o, float* lse, int B, int Hq, int Hkv, int S, float scale,
+           int causal, cudaStream_t stream) {
+  using C = Cfg<D>;
+  Params p{};
+  if (!make_map_bhsd(&p.tm_q, q.ptr, B, Hq, S, D, q.stride_b, q.stride_h, q.stride_s, C::CE, BM,
+                     C::SW) ||
+      !make_map_bhsd(&p.tm_k, k.ptr, B, Hkv, S, D, k.stride_b, k.stride_h, k.stride_s, C::CE, BN,
+                     C::SW) ||
+      !make_map_bhsd(&p.tm_v, v.ptr, B, Hkv, S, D, v.stride_b, v.stride_h, v.stride_s, C::CE, BN,
+                     C::SW)) {
+    autosp_set_error("attn_fwd: cuTensorMapEncodeTiled failed (alignment/strides?)");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  p.o = static_cast<__nv_bfloat16*>(const_cast<void*>(o.ptr));
+  p.o_sb = o.stride_b;
+  p.o_sh = o.stride_h;
+  p.o_ss = o.stride_s;
+  p.lse = lse;
+  p.B = B;
+  p.Hq = Hq;
+  p.Hkv = Hkv;
+  p.S = S;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.causal = causal;
+  p.n_qblk = (S + 2 * BM - 1) / (2 * BM);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr_set = true;
+  }
+  dim3 grid(p.n_qblk, Hq, B);
+  attn_fwd_kernel<D><<<grid, kThreads, C::SMEM, stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    autosp_set_error("attn_fwd launch failed: %s", cudaGetErrorString(e));
+    return AUTOSP_ERR_CUDA;
+  }
+  return AUTOSP_OK;
+}
+
+}  // namespace fwd
+}  // namespace autosp
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int autosp_check_attn_tensor(const autosp_attn_tensor& t, const char* name) {
+  if (!t.ptr || !aligned16(t.ptr) || (t.stride_b * 2) % 16 || (t.stride_h * 2) % 16 ||
+      (t.stride_s * 2) % 16) {
+    autosp_set_error("attention tensor %s must be non-null, 16-byte aligned with strides that "
+                     "are multiples of 8 elements",
+                     name);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  return AUTOSP_OK;
+}
+
+extern "C" int autosp_attn_fwd(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
+                               autosp_attn_tensor o, float* lse, int b, int hq, int hkv, int s,
+                               int d, float scale, int causal, void* stream) {
+  if (b < 1 || hq < 1 || hkv < 1 || s < 1 || hq % hkv) {
+    autosp_set_error("attn_fwd: bad shape b=%d hq=%d hkv=%d s=%d", b, hq, hkv, s);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  int rc;
+  if ((rc = autosp_check_attn_tensor(q, "q")) || (rc = autosp_check_attn_tensor(k, "k")) ||
+      (rc = autosp_check_attn_tensor(v, "v")) || (rc = autosp_check_attn_tensor(o, "o")))
+    return rc;
+  if (!lse) {
+    autosp_set_error("attn_fwd: lse must be non-null");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (d) {
+    case 32: return autosp::fwd::launch<32>(q, k, v, o, lse, b, hq, hkv, s, scale, causal, st);
+    case 64: return autosp::fwd::launch<64>(q, k, v, o, lse, b, hq, hkv, s, scale, causal, st);
+    case 128: return autosp::fwd::launch<128>(q, k, v, o, lse, b, hq, hkv, s, scale, causal, st);
+    default:
+      autosp_set_error("attn_fwd: head_dim %d unsupported (32, 64, 128)", d);
+      return AUTOSP_ERR_UNSUPPORTED;
+  }
+}

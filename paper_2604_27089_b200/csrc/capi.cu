@@ -1,0 +1,87 @@
+// C ABI plumbing of libautosp.so: error text, device info, symmetric (IPC-mapped)
+// memory.  The compute entry points live next to their kernels (a2a.cu, attn_*.cu).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cuda_runtime.h>
+
+#include "../../include/autosp.h"
+
+static thread_local char g_err[512] = "";
+
+extern "C" void autosp_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  autosp_set_error("%s: %s", what, cudaGetErrorString(e));
+  return AUTOSP_ERR_CUDA;
+}
+
+extern "C" int autosp_abi_version(void) { return AUTOSP_ABI_VERSION; }
+extern "C" const char* autosp_last_error(void) { return g_err; }
+
+extern "C" int autosp_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return -1; }
+  int sms = 0, ma = 0, mi = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&ma, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&mi, cudaDevAttrComputeCapabilityMinor, dev);
+  if (sm_count) *sm_count = sms;
+  if (cc_major) *cc_major = ma;
+  if (cc_minor) *cc_minor = mi;
+  return 0;
+}
+
+extern "C" int autosp_symm_alloc(size_t bytes, void** dev_ptr, void* ipc_handle_out) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == AUTOSP_IPC_HANDLE_BYTES, "ipc handle size");
+  if (!dev_ptr || bytes == 0) {
+    autosp_set_error("symm_alloc: bad arguments");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  cudaError_t e = cudaMalloc(dev_ptr, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "symm_alloc cudaMalloc");
+  e = cudaMemset(*dev_ptr, 0, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "symm_alloc cudaMemset");
+  if (ipc_handle_out) {
+    cudaIpcMemHandle_t h;
+    e = cudaIpcGetMemHandle(&h, *dev_ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    memcpy(ipc_handle_out, &h, sizeof(h));
+  }
+  return AUTOSP_OK;
+}
+
+extern "C" int autosp_symm_open(const void* ipc_handle, void** dev_ptr) {
+  if (!ipc_handle || !dev_ptr) {
+    autosp_set_error("symm_open: bad arguments");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  return AUTOSP_OK;
+}
+
+extern "C" int autosp_symm_close(void* peer_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(peer_ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  return AUTOSP_OK;
+}
+
+extern "C" int autosp_symm_free(void* dev_ptr) {
+  cudaError_t e = cudaFree(dev_ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "symm_free cudaFree");
+  return AUTOSP_OK;
+}
+
+extern "C" int autosp_memset_async(void* dev_ptr, int value, size_t bytes, void* stream) {
+  cudaError_t e = cudaMemsetAsync(dev_ptr, value, bytes, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "memset_async");
+  return AUTOSP_OK;
+}

@@ -1,0 +1,140 @@
+"""Torch-facing launchers of the sm_100a kernels in libautosp.so.
+
+Tensors are passed as raw device pointers + strides through the C ABI (the library
+never sees torch types).  All launches go on torch's current CUDA stream.  Nothing
+here falls back to a PyTorch implementation: a missing library or a non-CUDA tensor
+is an error."""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import _lib
+from .errors import ValidationError
+
+SUPPORTED_HEAD_DIMS = (32, 64, 128)
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _attn_tensor(t: torch.Tensor, name: str) -> _lib.AttnTensor:
+    """[b, h, s, d] view, d contiguous."""
+    if not t.is_cuda or t.dtype != torch.bfloat16:
+        raise ValidationError(f"{name}: expected a CUDA bf16 tensor, got {t.device}/{t.dtype}")
+    if t.dim() != 4 or t.stride(3) != 1:
+        raise ValidationError(f"{name}: expected [b, h, s, d] with contiguous head_dim")
+    sb, sh, ss, _ = t.stride()
+    return _lib.AttnTensor(t.data_ptr(), sb, sh, ss)
+
+
+def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool = True,
+             scale: float | None = None, out: torch.Tensor | None = None):
+    """Causal flash attention forward.  q [b, hq, s, d], k/v [b, hkv, s, d] (bf16 views).
+    Returns (o [b, hq, s, d] bf16, lse [b, hq, s] fp32)."""
+    lib = _lib.load()
+    b, hq, s, d = q.shape
+    hkv = k.shape[1]
+    if k.shape != (b, hkv, s, d) or v.shape != k.shape:
+        raise ValidationError(f"attn_fwd: q {tuple(q.shape)} k {tuple(k.shape)} v {tuple(v.shape)}")
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    o = torch.empty((b, hq, s, d), dtype=torch.bfloat16, device=q.device) if out is None else out
+    lse = torch.empty((b, hq, s), dtype=torch.float32, device=q.device)
+    rc = lib.autosp_attn_fwd(_attn_tensor(q, "q"), _attn_tensor(k, "k"), _attn_tensor(v, "v"),
+                             _attn_tensor(o, "o"), lse.data_ptr(), b, hq, hkv, s, d,
+                             float(scale), int(causal), _stream())
+    _lib.check(rc, "attn_fwd")
+    return o, lse
+
+
+def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = None,
+             dq=None, dk=None, dv=None):
+    """Flash attention backward recomputing P from the saved LSE.
+    Returns (dq, dk, dv) in bf16 ([b, h, s, d])."""
+    lib = _lib.load()
+    b, hq, s, d = q.shape
+    hkv = k.shape[1]
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    dev = q.device
+    dq = torch.empty((b, hq, s, d), dtype=torch.bfloat16, device=dev) if dq is None else dq
+    dk = torch.empty((b, hkv, s, d), dtype=torch.bfloat16, device=dev) if dk is None else dk
+    dv = torch.empty((b, hkv, s, d), dtype=torch.bfloat16, device=dev) if dv is None else dv
+    ws = torch.empty(lib.autosp_attn_bwd_workspace_bytes(b, hq, s, d), dtype=torch.uint8,
+                     device=dev)
+    if not lse.is_contiguous() or lse.dtype != torch.float32:
+        raise ValidationError("attn_bwd: lse must be contiguous fp32 [b, hq, s]")
+    rc = lib.autosp_attn_bwd(_attn_tensor(q, "q"), _attn_tensor(k, "k"), _attn_tensor(v, "v"),
+                             _attn_tensor(o, "o"), _attn_tensor(do, "do"), lse.data_ptr(),
+                             _attn_tensor(dq, "dq"), _attn_tensor(dk, "dk"),
+                             _attn_tensor(dv, "dv"), ws.data_ptr(), b, hq, hkv, s, d,
+                             float(scale), int(causal), _stream())
+    _lib.check(rc, "attn_bwd")
+    return dq, dk, dv
+
+
+# ----------------------------------------------------------------------------- all-to-all
+def a2a_tensor_desc(src: torch.Tensor, heads: int, dst_offset: int,
+                    dst_strides: tuple[int, int, int]) -> _lib.A2ATensor:
+    """src is a logical [b, s, h, d] view with d contiguous."""
+    if src.dim() != 4 or src.stride(3) != 1:
+        raise ValidationError("a2a source must be a [b, s, h, d] view with contiguous head_dim")
+    sb, ss, sh, _ = src.stride()
+    db, ds, dh = dst_strides
+    return _lib.A2ATensor(src.data_ptr(), sb, ss, sh, dst_offset, db, ds, dh, heads, 0)
+
+
+def a2a_launch(direction: int, descs: list, b: int, s_global: int, d: int, elem_bytes: int,
+               world: int, rank: int, peer_base: list[int], peer_flags: list[int],
+               epoch: int) -> None:
+    lib = _lib.load()
+    arr = (_lib.A2ATensor * len(descs))(*descs)
+    pb = (C.c_void_p * world)(*peer_base)
+    pf = (C.c_void_p * world)(*peer_flags)
+    rc = lib.autosp_a2a(direction, arr, len(descs), b, s_global, d, elem_bytes, world, rank,
+                        pb, pf, epoch & 0xFFFFFFFF, _stream())
+    _lib.check(rc, "a2a")
+
+
+def a2a_wait(local_flags: int, world: int, rank: int, epoch: int) -> None:
+    rc = _lib.load().autosp_a2a_wait(local_flags, world, rank, epoch & 0xFFFFFFFF, _stream())
+    _lib.check(rc, "a2a_wait")
+
+
+def a2a_mark_ready(flags: list[int], epoch: int) -> None:
+    pf = (C.c_void_p * len(flags))(*flags)
+    rc = _lib.load().autosp_a2a_mark_ready(pf, len(flags), epoch & 0xFFFFFFFF, _stream())
+    _lib.check(rc, "a2a_mark_ready")
+
+
+def a2a_loopback(direction: str, shards: list[torch.Tensor]) -> list[torch.Tensor]:
+    """Run the push kernel for P VIRTUAL ranks on one GPU (each rank's receive region and
+    flag block is a local allocation).  Same semantics as the reference's
+    all_to_all_shards (executor.py:203-230); used by tests and the single-GPU bench."""
+    P = len(shards)
+    b, s_src, h_src, d = shards[0].shape
+    dev, dt = shards[0].device, shards[0].dtype
+    eb = shards[0].element_size()
+    if direction == "seq_to_head":
+        out_shape = (b, s_src * P, h_src // P, d)
+        dirn, s_glob = _lib.SEQ_TO_HEAD, s_src * P
+    elif direction == "head_to_seq":
+        out_shape = (b, s_src // P, h_src * P, d)
+        dirn, s_glob = _lib.HEAD_TO_SEQ, s_src
+    else:
+        raise ValidationError(f"unknown all-to-all direction {direction!r}")
+    outs = [torch.empty(out_shape, dtype=dt, device=dev) for _ in range(P)]
+    flags = torch.zeros((P, _lib.FLAG_WORDS), dtype=torch.int32, device=dev)
+    fptr = [flags[j].data_ptr() for j in range(P)]
+    optr = [o.data_ptr() for o in outs]
+    ostr = outs[0].stride()
+    a2a_mark_ready(fptr, 1)
+    for r in range(P):
+        desc = a2a_tensor_desc(shards[r], h_src, 0, (ostr[0], ostr[1], ostr[2]))
+        a2a_launch(dirn, [desc], b, s_glob, d, eb, P, r, optr, fptr, 1)
+    for r in range(P):
+        a2a_wait(fptr[r], P, r, 1)
+    return outs
