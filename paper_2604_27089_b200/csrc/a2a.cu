@@ -215,8 +215,9 @@ extern "C" int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n
     }
   }
   // widest vector that divides every row / stride / pointer
-  uint64_t align = (uint64_t)d * elem_bytes;
+  uint64_t align = 16;  // power of two dividing every row / stride / pointer
   auto fold = [&](uint64_t v) { while (align > 1 && (v % align)) align >>= 1; };
+  fold((uint64_t)d * elem_bytes);
   for (int j = 0; j < world; ++j) fold((uint64_t)(uintptr_t)p.peer_base[j]);
   const int s_src = direction == AUTOSP_SEQ_TO_HEAD ? p.s_loc : s_global;
   p.total_items = 0;
@@ -245,7 +246,6 @@ extern "C" int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n
                        T.dst_stride_s, T.dst_stride_h})
       fold((uint64_t)(st < 0 ? -st : st) * elem_bytes);
   }
-  if (align > 16) align = 16;
   const uint64_t row = (uint64_t)d * elem_bytes;
   if (row / align > 32) {
     autosp_set_error("row of %llu bytes needs >32 lanes at %llu-byte granularity (unsupported)",

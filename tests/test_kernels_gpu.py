@@ -159,3 +159,32 @@ def test_attn_fwd_reference_fixture_qkv_shared(golden_dir):
     torch.cuda.synchronize()
     o = o.float().cpu().permute(0, 2, 1, 3).numpy()
     assert orc.norm_rel_err(o, z["c2_out"]) < O_TOL
+
+
+BWD_CASES = [
+    (1, 2, 2, 256, 64, True),
+    (1, 2, 2, 128, 128, True),
+    (2, 4, 2, 300, 128, True),
+    (1, 8, 8, 1024, 32, True),
+    (1, 4, 1, 512, 64, True),
+    (1, 2, 2, 200, 64, False),
+    (1, 3, 3, 777, 128, True),
+]
+
+
+@pytest.mark.parametrize("b,hq,hkv,s,d,causal", BWD_CASES)
+def test_attn_bwd_matches_oracle(b, hq, hkv, s, d, causal):
+    q, k, v = _rand_qkv(b, hq, hkv, s, d, seed=7 * s + d)
+    g = torch.Generator().manual_seed(s)
+    do = torch.randn(b, s, hq, d, generator=g)
+    qb, kb, vb, dob = (x.bfloat16().double().numpy() for x in (q, k, v, do))
+    dq_ref, dk_ref, dv_ref = orc.attention_bwd(qb, kb, vb, dob, causal=causal)
+    K = _k()
+    qd, kd, vd, dod = (_to_dev(x, "bhsd") for x in (q, k, v, do))
+    o, lse = K.attn_fwd(qd, kd, vd, causal=causal)
+    dq, dk, dv = K.attn_bwd(qd, kd, vd, o, dod, lse, causal=causal)
+    torch.cuda.synchronize()
+    for name, got, ref in (("dq", dq, dq_ref), ("dk", dk, dk_ref), ("dv", dv, dv_ref)):
+        got = got.float().cpu().permute(0, 2, 1, 3).numpy()
+        err = orc.norm_rel_err(got, ref)
+        assert err < GRAD_TOL, (name, err)
