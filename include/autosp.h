@@ -105,8 +105,11 @@ AUTOSP_API int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n
                void* const* peer_base, uint32_t* const* peer_flags, uint32_t epoch,
                void* stream);
 /* Stream-ordered wait until every peer has published `epoch` into this rank's flag
- * block (the receive region then holds the complete a2a output).                    */
-AUTOSP_API int autosp_a2a_wait(uint32_t* local_flags, int world, int rank, uint32_t epoch, void* stream);
+ * block (the receive region then holds the complete a2a output).  `first_dst_offset` is
+ * this rank's dst_offset of tensor 0 for the call: every sender records its own view of
+ * it and the wait traps on disagreement (symmetric-allocation invariant).           */
+AUTOSP_API int autosp_a2a_wait(uint32_t* local_flags, int world, int rank, uint32_t epoch,
+                               int64_t first_dst_offset, void* stream);
 /* Single-process loopback used by tests / benchmarks on one GPU: marks `epoch` as reached
  * for all `world` virtual ranks whose flag blocks are given.                           */
 AUTOSP_API int autosp_a2a_mark_ready(uint32_t* const* flags, int world, uint32_t epoch, void* stream);

@@ -50,7 +50,8 @@ EXPORTS = {
     "autosp_a2a": (C.c_int, [C.c_int, C.POINTER(A2ATensor), C.c_int, C.c_int, C.c_int, C.c_int,
                              C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p),
                              C.POINTER(C.c_void_p), C.c_uint32, C.c_void_p]),
-    "autosp_a2a_wait": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_uint32, C.c_void_p]),
+    "autosp_a2a_wait": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_uint32, C.c_int64,
+                                  C.c_void_p]),
     "autosp_a2a_mark_ready": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_uint32,
                                         C.c_void_p]),
     "autosp_attn_fwd": (C.c_int, [AttnTensor] * 4 + [C.c_void_p] + [C.c_int] * 5 +

@@ -1,0 +1,163 @@
+"""``auto_sp`` — the Ulysses sequence-parallel rewrite on the Dynamo (Torch-IR) graph.
+
+Reference: ``transform_sp`` (``sp_pass.py:133-220``).  Differences that follow from
+running inside ``torch.compile`` instead of on a global desk-scale IR:
+
+* the traced graph already sees each rank's sequence shard (the user feeds
+  ``batch[:, sp_slice]``, paper Listing 1; reference ``shard_inputs``
+  ``executor.py:324-341``), so RESIZE_BUFS need no rewrite — every shape outside
+  attention is already ``s/P``;
+* ATTN_OPS: every ``scaled_dot_product_attention`` call becomes
+  a2a(seq->head) of (q, k, v) in one launch -> causal sm_100a attention over the full
+  sequence on ``h/P`` heads -> a2a(head->seq)  (``sp_pass.py:172-195``);
+* INDEX_OPS: position indices (``autosp.positions`` or integer ``torch.arange`` of the
+  local sequence length) gain the rank offset ``rank * s/P`` (``sp_pass.py:160-163``,
+  ``executor.py:68-70``); the causal mask stays implicit and full-sequence inside the
+  kernel (``sp_pass.py:164-166``);
+* errors mirror the reference: indivisible heads -> ValidationError
+  (``sp_pass.py:145-148``), pass applied twice -> ValidationError (``sp_pass.py:134-135``).
+
+At P = 1 the collectives are omitted (``sp_pass.py:138-144``) but attention is still
+lowered to the sm_100a kernel.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from enum import Enum
+
+import torch
+import torch.fx as fx
+import torch.nn.functional as F
+
+from . import ops
+from .dist import SPState
+from .errors import ValidationError
+
+
+class RewriteReason(str, Enum):  # sp_pass.py:34-37
+    RESIZED_BUFFER = "ResizedBuffer"
+    RECOMPUTED_INDEX = "RecomputedIndex"
+    INSERTED_COLLECTIVE = "InsertedCollective"
+
+
+ATTN_OPS = (torch._C._nn.scaled_dot_product_attention, F.scaled_dot_product_attention)
+
+
+def positions(n: int, device=None) -> torch.Tensor:
+    """Explicit position-index op (reference OpKind.POSITION_INDEX): auto_sp offsets it by
+    rank * s/P.  Equivalent to torch.arange(n) when run without the pass."""
+    return torch.arange(n, device=device)
+
+
+INDEX_OPS = (positions, torch.arange)
+_LOWERED = (ops.ulysses_attention, ops.sdpa)
+
+
+@dataclass
+class SPDims:  # reference infer_dims (sp_pass.py:102-123), on the local shard
+    b: int
+    s_local: int
+    h: int
+    d: int
+    layers: int
+
+
+@dataclass
+class SPGraphInfo:
+    world_size: int
+    dims: SPDims
+    provenance: dict[str, RewriteReason] = field(default_factory=dict)
+
+
+def _val(n):
+    v = n.meta.get("example_value", n.meta.get("val")) if isinstance(n, fx.Node) else n
+    return v
+
+
+def infer_dims(gm: fx.GraphModule, example_inputs) -> SPDims:
+    attn = [n for n in gm.graph.nodes if n.op == "call_function" and n.target in ATTN_OPS]
+    if not attn:
+        raise ValidationError("graph has no attention node")
+    qv = _val(attn[0].args[0])
+    if qv is None or qv.dim() != 4:
+        raise ValidationError("cannot read [b, h, s, d] from the first attention's query")
+    b, h, s, d = qv.shape
+    return SPDims(b=int(b), s_local=int(s), h=int(h), d=int(d), layers=len(attn))
+
+
+def _is_int_arange_of(node: fx.Node, length: int) -> tuple[bool, int, int, int]:
+    args = list(node.args)
+    if not all(isinstance(a, int) for a in args):
+        return False, 0, 0, 0
+    dt = node.kwargs.get("dtype")
+    if dt is not None and dt.is_floating_point:
+        return False, 0, 0, 0
+    if len(args) == 1:
+        start, end, step = 0, args[0], 1
+    elif len(args) == 2:
+        start, end, step = args[0], args[1], 1
+    elif len(args) == 3:
+        start, end, step = args
+    else:
+        return False, 0, 0, 0
+    n = max(0, (end - start + step - 1) // step) if step > 0 else 0
+    return n == length and step == 1, start, end, step
+
+
+def auto_sp(gm: fx.GraphModule, example_inputs, st: SPState) -> tuple[fx.GraphModule, SPGraphInfo]:
+    g = gm.graph
+    if any(n.op == "call_function" and n.target in _LOWERED for n in g.nodes):
+        raise ValidationError("graph already lowered by auto_sp (pass already applied)")
+    dims = infer_dims(gm, example_inputs)
+    P = st.world
+    info = SPGraphInfo(world_size=P, dims=dims)
+    for n in list(g.nodes):
+        if n.op != "call_function":
+            continue
+        if n.target in ATTN_OPS:
+            q, k, v = n.args[:3]
+            kw = dict(n.kwargs)
+            extra = list(n.args[3:])
+            mask = kw.get("attn_mask", extra[0] if len(extra) > 0 else None)
+            dropout = kw.get("dropout_p", extra[1] if len(extra) > 1 else 0.0)
+            causal = kw.get("is_causal", extra[2] if len(extra) > 2 else False)
+            scale = kw.get("scale", None)
+            if mask is not None or not causal:
+                raise ValidationError("auto_sp lowers causal attention only (mask must be implicit, "
+                                      "reference executor.py:62-65)")
+            if dropout:
+                raise ValidationError("attention dropout is not supported")
+            hq, hkv = _val(q).shape[1], _val(k).shape[1]
+            if hq % P or hkv % P:
+                raise ValidationError(f"head count {hq}/{hkv} not divisible by world size {P}")
+            with g.inserting_before(n):
+                if P > 1:
+                    new = g.call_function(ops.ulysses_attention, (q, k, v),
+                                          {"group": st.name, "is_causal": True, "scale": scale})
+                    info.provenance[new.name] = RewriteReason.INSERTED_COLLECTIVE
+                else:
+                    new = g.call_function(ops.sdpa, (q, k, v), {"is_causal": True, "scale": scale})
+                    info.provenance[new.name] = RewriteReason.RESIZED_BUFFER
+            new.meta.update(n.meta)
+            n.replace_all_uses_with(new)
+            g.erase_node(n)
+        elif n.target in INDEX_OPS and P > 1:
+            if n.target is positions:
+                length = n.args[0]
+                ok, start, end = isinstance(length, int), 0, length
+            else:
+                ok, start, end, _ = _is_int_arange_of(n, dims.s_local)
+            if not ok or (end - start) != dims.s_local:
+                continue
+            off = st.rank * dims.s_local
+            kwargs = {k: v for k, v in n.kwargs.items() if k in ("device", "dtype")}
+            with g.inserting_before(n):
+                new = g.call_function(torch.arange, (start + off, end + off), kwargs)
+            new.meta.update(n.meta)
+            n.replace_all_uses_with(new)
+            g.erase_node(n)
+            info.provenance[new.name] = RewriteReason.RECOMPUTED_INDEX
+    g.lint()
+    gm.recompile()
+    return gm, info

@@ -1,0 +1,69 @@
+"""``reg_passes([...])`` and ``compile(model)`` — the paper's user API (Listing 1,
+PAPER.md:62-72) over torch.compile used as a graph-capture front end only:
+
+  Dynamo FX graph --auto_sp--> Torch IR with autosp ops --AOTAutograd--> joint graph
+  --sp_ac partitioner--> forward / backward graphs executed eagerly (boxed), whose hot
+  ops are the sm_100a kernels in libautosp.so; everything else is plain ATen/cuBLAS.
+
+No Inductor, no Triton: the compiled graphs run their ATen ops and our custom ops
+directly.  Reference equivalents: SPConfig + transform_sp (sp_pass.py:57-68,133-220),
+AcMode + plan_checkpoints (ac_pass.py:26-29,181-184)."""
+
+from __future__ import annotations
+
+import torch
+
+from . import dist as sp_dist
+from .auto_sp import auto_sp
+from .errors import ValidationError
+from .sp_ac import AcMode, make_partition_fn
+
+KNOWN_PASSES = ("auto_sp", "sp_ac")
+_PASSES: list[str] = []
+_AC_MODE = AcMode.SEQ_AWARE_NON_ATTENTION
+LAST_INFO: dict = {}
+
+
+def reg_passes(passes: list[str], ac_mode: str | AcMode = AcMode.SEQ_AWARE_NON_ATTENTION) -> None:
+    global _AC_MODE
+    unknown = [p for p in passes if p not in KNOWN_PASSES]
+    if unknown:
+        raise ValidationError(f"unknown passes {unknown}; known: {list(KNOWN_PASSES)}")
+    if "sp_ac" in passes and "auto_sp" not in passes:
+        raise ValidationError("sp_ac requires auto_sp")
+    _PASSES[:] = list(passes)
+    _AC_MODE = AcMode(ac_mode)
+
+
+def registered_passes() -> list[str]:
+    return list(_PASSES)
+
+
+def backend(passes: list[str] | None = None, ac_mode: AcMode | None = None):
+    """A torch.compile backend applying the registered passes."""
+    from functorch.compile import make_boxed_func
+    from torch._dynamo.backends.common import aot_autograd
+    from torch._functorch.partitioners import default_partition
+
+    passes = list(_PASSES if passes is None else passes)
+    mode = _AC_MODE if ac_mode is None else AcMode(ac_mode)
+
+    def _compiler(gm, example_inputs):
+        return make_boxed_func(gm.forward)
+
+    def _backend(gm: torch.fx.GraphModule, example_inputs):
+        st = sp_dist.state()
+        if "auto_sp" in passes:
+            gm, info = auto_sp(gm, example_inputs, st)
+            LAST_INFO["auto_sp"] = info
+        part = make_partition_fn(mode) if "sp_ac" in passes else default_partition
+        return aot_autograd(fw_compiler=_compiler, bw_compiler=_compiler,
+                            partition_fn=part)(gm, example_inputs)
+
+    return _backend
+
+
+def compile(model: torch.nn.Module, passes: list[str] | None = None,
+            ac_mode: AcMode | None = None) -> torch.nn.Module:
+    """``model.compile()`` with the AutoSP backend (static shapes)."""
+    return torch.compile(model, backend=backend(passes, ac_mode), dynamic=False, fullgraph=False)

@@ -26,6 +26,7 @@ namespace autosp {
 
 constexpr int kReadyWord = 0;
 constexpr int kArriveWord = 16;   // + src rank
+constexpr int kCheckWord = 32;    // + src rank: sender's view of the destination offset
 constexpr int kCounterWord = 48;  // CTA completion counter (local use only)
 constexpr int kTileTokens = 16;
 constexpr int kA2AThreads = 256;
@@ -49,6 +50,7 @@ struct A2AParams {
   char* peer_base[AUTOSP_MAX_WORLD];
   uint32_t* peer_flags[AUTOSP_MAX_WORLD];
   uint32_t epoch;
+  uint32_t check;
   int64_t total_items;
 };
 
@@ -139,14 +141,23 @@ __global__ void __launch_bounds__(kA2AThreads) a2a_push_kernel(const __grid_cons
       *ctr = 0u;
       __threadfence_system();
       for (int j = 0; j < p.P; ++j)
-        if (j != p.rank) st_release_sys(p.peer_flags[j] + kArriveWord + p.rank, p.epoch);
+        if (j != p.rank) {
+          p.peer_flags[j][kCheckWord + p.rank] = p.check;
+          st_release_sys(p.peer_flags[j] + kArriveWord + p.rank, p.epoch);
+        }
     }
   }
 }
 
-__global__ void a2a_wait_kernel(uint32_t* flags, int P, int rank, uint32_t epoch) {
+__global__ void a2a_wait_kernel(uint32_t* flags, int P, int rank, uint32_t epoch,
+                                uint32_t check) {
   const int j = threadIdx.x;
-  if (j < P && j != rank) spin_until_epoch(flags + kArriveWord + j, epoch);
+  if (j < P && j != rank) {
+    spin_until_epoch(flags + kArriveWord + j, epoch);
+    // every sender must have written where this rank expects the data (symmetric
+    // allocation invariant); a divergence is a bug -> fail loudly, never corrupt silently
+    if (*(volatile uint32_t*)(flags + kCheckWord + j) != check) asm volatile("trap;");
+  }
   __syncthreads();
 }
 
@@ -206,6 +217,7 @@ extern "C" int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n
   p.P = world;
   p.rank = rank;
   p.epoch = epoch;
+  p.check = (uint32_t)((uint64_t)tensors[0].dst_offset >> 4);
   for (int j = 0; j < world; ++j) {
     p.peer_base[j] = static_cast<char*>(peer_base[j]);
     p.peer_flags[j] = peer_flags[j];
@@ -275,14 +287,14 @@ extern "C" int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n
 }
 
 extern "C" int autosp_a2a_wait(uint32_t* local_flags, int world, int rank, uint32_t epoch,
-                               void* stream) {
+                               int64_t first_dst_offset, void* stream) {
   if (!local_flags || world < 1 || world > AUTOSP_MAX_WORLD || rank < 0 || rank >= world) {
     autosp_set_error("bad a2a_wait arguments (world %d rank %d)", world, rank);
     return AUTOSP_ERR_VALIDATION;
   }
   if (world == 1) return AUTOSP_OK;
-  autosp::a2a_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(local_flags, world,
-                                                                          rank, epoch);
+  autosp::a2a_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      local_flags, world, rank, epoch, (uint32_t)((uint64_t)first_dst_offset >> 4));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     autosp_set_error("a2a_wait launch failed: %s", cudaGetErrorString(e));

@@ -1,0 +1,230 @@
+"""``dist.init(SP_GROUP_SIZE)`` — the Ulysses process-group plumbing (paper Listing 1;
+reference equivalent ``DeviceGroup(P)``, ``executor.py:233-275``).
+
+One process per GPU.  The world is split into data-parallel replicas of
+``sp_group_size`` consecutive ranks.  Inside an SP group every rank owns one
+*symmetric* allocation (identical size on all ranks) holding
+
+    [ flag block (256 B) | receive region ]
+
+mapped once into every peer through CUDA IPC, so the all-to-all kernels write straight
+into peers' HBM over NVLink 5 / NVSwitch (no NCCL on the reshard path).  NCCL (or gloo
+on CPU test runs) carries only the host-side rendezvous and the per-step gradient
+reduction.
+
+Receive-region allocation is deterministic on every rank: a first-fit allocator whose
+slots are released when the storage of the tensor handed out is no longer referenced
+(C++ refcount, identical on all ranks running the same program).  The kernels verify
+at run time that sender and receiver agree on every offset (a mismatch traps)."""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as tdist
+
+from . import _lib
+from .errors import ValidationError
+
+FLAG_BYTES = 4096  # flag block (256 B used) padded to keep the receive region aligned
+DEFAULT_POOL_BYTES = int(os.environ.get("AUTOSP_POOL_BYTES", str(8 << 30)))
+
+
+class _CAI:
+    """Minimal __cuda_array_interface__ wrapper: a zero-copy torch view of raw memory."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
+def _raw_tensor(ptr: int, nbytes: int, device) -> torch.Tensor:
+    return torch.as_tensor(_CAI(ptr, nbytes), device=device)
+
+
+@dataclass
+class _Slot:
+    offset: int
+    nbytes: int
+    base: torch.Tensor  # uint8 view owned by the pool; busy while its storage is shared
+
+
+class SymmetricPool:
+    """Receive region + flag block of one rank, with the peers' mappings."""
+
+    ALIGN = 1024
+
+    def __init__(self, nbytes: int, world: int, rank: int, device, group=None,
+                 peers: list[tuple[int, int]] | None = None):
+        lib = _lib.load()
+        self.world, self.rank, self.device = world, rank, device
+        self.capacity = nbytes
+        self._owned: list[int] = []
+        self._opened: list[int] = []
+        if peers is None:
+            ptr = C.c_void_p()
+            handle = (C.c_char * _lib.IPC_HANDLE_BYTES)()
+            _lib.check(lib.autosp_symm_alloc(FLAG_BYTES + nbytes, C.byref(ptr), handle),
+                       "symm_alloc")
+            self._owned.append(ptr.value)
+            handles = [None] * world
+            if world > 1:
+                tdist.all_gather_object(handles, bytes(handle), group=group)
+            bases = []
+            for j in range(world):
+                if j == rank:
+                    bases.append(ptr.value)
+                else:
+                    pp = C.c_void_p()
+                    _lib.check(lib.autosp_symm_open(handles[j], C.byref(pp)), "symm_open")
+                    self._opened.append(pp.value)
+                    bases.append(pp.value)
+            self.flag_ptrs = bases
+            self.region_ptrs = [b + FLAG_BYTES for b in bases]
+        else:  # explicit (flag_ptr, region_ptr) per rank: single-process loopback
+            self.flag_ptrs = [f for f, _ in peers]
+            self.region_ptrs = [r for _, r in peers]
+        self.slots: list[_Slot] = []
+        self.epoch = 0
+        self.high_water = 0
+
+    # ------------------------------------------------------------------ allocation
+    @staticmethod
+    def _busy(slot: _Slot) -> bool:
+        return torch._C._storage_Use_Count(slot.base.untyped_storage()._cdata) > 2
+
+    def alloc(self, nbytes: int) -> tuple[int, torch.Tensor]:
+        """First-fit slot of the receive region; returns (offset, uint8 view)."""
+        self.slots = [s for s in self.slots if self._busy(s)]
+        self.slots.sort(key=lambda s: s.offset)
+        need = (nbytes + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+        off = 0
+        for s in self.slots:
+            if s.offset - off >= need:
+                break
+            off = max(off, s.offset + (s.nbytes + self.ALIGN - 1) // self.ALIGN * self.ALIGN)
+        if off + need > self.capacity:
+            raise ValidationError(
+                f"symmetric receive region exhausted ({off + need} > {self.capacity} bytes); "
+                "raise AUTOSP_POOL_BYTES / dist.init(pool_bytes=...)")
+        # a separate storage per slot so its C++ refcount tracks exactly this slot
+        base = _raw_tensor(self.region_ptrs[self.rank] + off, nbytes, self.device)
+        self.slots.append(_Slot(off, nbytes, base))
+        self.high_water = max(self.high_water, off + need)
+        return off, base
+
+    def next_epoch(self) -> int:
+        self.epoch += 1
+        return self.epoch
+
+    def close(self):
+        lib = _lib.load()
+        for p in self._opened:
+            lib.autosp_symm_close(p)
+        for p in self._owned:
+            lib.autosp_symm_free(p)
+        self._opened, self._owned = [], []
+
+
+@dataclass
+class SPState:
+    world: int = 1               # SP group size P
+    rank: int = 0                # rank inside the SP group
+    group: object = None         # torch ProcessGroup of the SP group (None when P == 1)
+    dp_group: object = None      # data-parallel group of this rank's SP position
+    device: torch.device = field(default_factory=lambda: torch.device("cpu"))
+    pool: SymmetricPool | None = None
+    name: str = "sp"
+
+
+_STATE: SPState | None = None
+_REGISTRY: dict[str, SPState] = {}
+
+
+def init(sp_group_size: int, pool_bytes: int | None = None, backend: str | None = None) -> SPState:
+    """Create the SP groups (consecutive ranks), map the symmetric receive regions."""
+    global _STATE
+    if sp_group_size < 1:
+        raise ValidationError("sp_group_size must be positive")
+    if not tdist.is_initialized():
+        if int(os.environ.get("WORLD_SIZE", "1")) > 1 or sp_group_size > 1:
+            be = backend or ("nccl" if torch.cuda.is_available() else "gloo")
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+            tdist.init_process_group(be)
+    world = tdist.get_world_size() if tdist.is_initialized() else 1
+    rank = tdist.get_rank() if tdist.is_initialized() else 0
+    if world % sp_group_size:
+        raise ValidationError(f"world size {world} not divisible by SP group size {sp_group_size}")
+    if torch.cuda.is_available():
+        local = int(os.environ.get("LOCAL_RANK", rank % max(torch.cuda.device_count(), 1)))
+        torch.cuda.set_device(local)
+        device = torch.device("cuda", local)
+    else:
+        device = torch.device("cpu")
+    st = SPState(world=sp_group_size, rank=rank % sp_group_size, device=device)
+    if tdist.is_initialized() and world > 1:
+        for g0 in range(0, world, sp_group_size):
+            ranks = list(range(g0, g0 + sp_group_size))
+            pg = tdist.new_group(ranks)
+            if rank in ranks:
+                st.group = pg
+        for r0 in range(sp_group_size):
+            ranks = list(range(r0, world, sp_group_size))
+            pg = tdist.new_group(ranks)
+            if rank in ranks:
+                st.dp_group = pg
+    if sp_group_size > 1 and device.type == "cuda":
+        st.pool = SymmetricPool(pool_bytes or DEFAULT_POOL_BYTES, sp_group_size, st.rank, device,
+                                group=st.group)
+    _STATE = st
+    _REGISTRY[st.name] = st
+    return st
+
+
+def state() -> SPState:
+    if _STATE is None:
+        return SPState()
+    return _STATE
+
+
+def lookup(name: str) -> SPState:
+    try:
+        return _REGISTRY[name]
+    except KeyError:
+        raise ValidationError(f"SP group {name!r} is not initialised (call dist.init)") from None
+
+
+def register_state(st: SPState) -> None:
+    """Used by single-process loopback harnesses (tests / bench) to install a state."""
+    global _STATE
+    _STATE = st
+    _REGISTRY[st.name] = st
+
+
+def reduce_gradients(params, st: SPState | None = None) -> None:
+    """Sum the per-rank partial parameter gradients over the SP group (SURVEY §0 finding 6:
+    the reference's tests sum them, test_acceptance.py:89-96) and average over DP."""
+    st = st or state()
+    if not tdist.is_initialized():
+        return
+    grads = [p.grad for p in params if p.grad is not None]
+    if not grads:
+        return
+    flat = torch.cat([g.reshape(-1) for g in grads])
+    if st.group is not None and st.world > 1:
+        tdist.all_reduce(flat, group=st.group)
+    if st.dp_group is not None and tdist.get_world_size(st.dp_group) > 1:
+        tdist.all_reduce(flat, group=st.dp_group)
+        flat /= tdist.get_world_size(st.dp_group)
+    off = 0
+    for g in grads:
+        n = g.numel()
+        g.copy_(flat[off:off + n].view_as(g))
+        off += n

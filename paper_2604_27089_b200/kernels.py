@@ -99,8 +99,9 @@ def a2a_launch(direction: int, descs: list, b: int, s_global: int, d: int, elem_
     _lib.check(rc, "a2a")
 
 
-def a2a_wait(local_flags: int, world: int, rank: int, epoch: int) -> None:
-    rc = _lib.load().autosp_a2a_wait(local_flags, world, rank, epoch & 0xFFFFFFFF, _stream())
+def a2a_wait(local_flags: int, world: int, rank: int, epoch: int, first_dst_offset: int = 0) -> None:
+    rc = _lib.load().autosp_a2a_wait(local_flags, world, rank, epoch & 0xFFFFFFFF,
+                                     first_dst_offset, _stream())
     _lib.check(rc, "a2a_wait")
 
 

@@ -1,0 +1,192 @@
+"""torch.library custom ops that the ``auto_sp`` pass lowers attention to.
+
+    autosp::attention(q, k, v, scale, causal) -> (o, lse)          K3 (attn_fwd.cu)
+    autosp::attention_backward(do, q, k, v, o, lse, ...) -> dq,dk,dv K4 (attn_bwd.cu)
+    autosp::all_to_all(xs, direction, group) -> ys                 K1/K2 (a2a.cu)
+
+All tensors use the SDPA logical layout ``[b, h, s, d]`` (head_dim contiguous, any
+other strides).  ``all_to_all`` is the reference's AllToAll node
+(``sp_pass.py:172-195``, ``executor.py:203-230``) over up to four tensors in ONE kernel
+launch; its gradient is the inverse-direction all-to-all (``autodiff.py:252-262``).
+
+The ops have CUDA kernels only.  There is no CPU kernel in the product: calling them on
+CPU tensors raises.  (``testing.enable_cpu_lowering()`` registers a test-only CPU/gloo
+lowering used by the multi-process CPU tests.)
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import dist as sp_dist
+from . import kernels
+from ._lib import HEAD_TO_SEQ, SEQ_TO_HEAD
+from .errors import ValidationError
+
+SEQ_TO_HEAD_DIR = SEQ_TO_HEAD
+HEAD_TO_SEQ_DIR = HEAD_TO_SEQ
+# The sm_100a attention computes in bf16 (fp32 accumulation); q/k/v of other dtypes are
+# cast before the all-to-all (half the NVLink bytes) and the output cast back.
+ATTN_DTYPE: torch.dtype | None = torch.bfloat16
+
+
+# ----------------------------------------------------------------------------- attention
+@torch.library.custom_op("autosp::attention", mutates_args=(), device_types="cuda")
+def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: float,
+              causal: bool) -> tuple[torch.Tensor, torch.Tensor]:
+    return kernels.attn_fwd(q, k, v, causal=causal, scale=scale)
+
+
+@attention.register_fake
+def _attention_fake(q, k, v, scale, causal):
+    b, h, s, d = q.shape
+    return q.new_empty((b, h, s, d)), q.new_empty((b, h, s), dtype=torch.float32)
+
+
+@torch.library.custom_op("autosp::attention_backward", mutates_args=(), device_types="cuda")
+def attention_backward(do: torch.Tensor, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                       o: torch.Tensor, lse: torch.Tensor, scale: float,
+                       causal: bool) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    if do.stride(-1) != 1:
+        do = do.contiguous()
+    return kernels.attn_bwd(q, k, v, o, do, lse, causal=causal, scale=scale)
+
+
+@attention_backward.register_fake
+def _attention_backward_fake(do, q, k, v, o, lse, scale, causal):
+    return (q.new_empty(q.shape), k.new_empty(k.shape), v.new_empty(v.shape))
+
+
+def _attn_setup(ctx, inputs, output):
+    q, k, v, scale, causal = inputs
+    o, lse = output
+    ctx.save_for_backward(q, k, v, o, lse)
+    ctx.scale, ctx.causal = scale, causal
+
+
+def _attn_bwd(ctx, do, dlse):
+    q, k, v, o, lse = ctx.saved_tensors
+    dq, dk, dv = attention_backward(do, q, k, v, o, lse, ctx.scale, ctx.causal)
+    return dq, dk, dv, None, None
+
+
+attention.register_autograd(_attn_bwd, setup_context=_attn_setup)
+
+
+def _cast_in(*ts):
+    if ATTN_DTYPE is None or ts[0].dtype == ATTN_DTYPE:
+        return ts, None
+    cast = {}
+    for t in ts:  # keep aliasing (q = k = v in the reference model)
+        if id(t) not in cast:
+            cast[id(t)] = t.to(ATTN_DTYPE)
+    return tuple(cast[id(t)] for t in ts), ts[0].dtype
+
+
+def _sdpa(q, k, v, is_causal, scale):
+    if not is_causal:
+        raise ValidationError("auto_sp attention is causal (reference mask, executor.py:62-65)")
+    scale = 1.0 / math.sqrt(q.shape[-1]) if scale is None else float(scale)
+    return attention(q, k, v, scale, True)[0]
+
+
+def sdpa(q, k, v, is_causal=True, scale=None):
+    """Drop-in for F.scaled_dot_product_attention(q, k, v, is_causal=True[, enable_gqa])."""
+    (q, k, v), dt = _cast_in(q, k, v)
+    o = _sdpa(q, k, v, is_causal, scale)
+    return o if dt is None else o.to(dt)
+
+
+# ----------------------------------------------------------------------------- all-to-all
+def _out_geometry(x: torch.Tensor, direction: int, P: int):
+    """Logical output shape/strides for one [b, h, s, d] input."""
+    b, h, s, d = x.shape
+    if direction == SEQ_TO_HEAD_DIR:
+        if h % P:
+            raise ValidationError(f"heads {h} not divisible by world size {P}")
+        hl, S = h // P, s * P
+        shape = (b, hl, S, d)
+        strides = (hl * S * d, S * d, d, 1)  # head-major: the attention operand layout
+    else:
+        if s % P:
+            raise ValidationError(f"sequence {s} not divisible by world size {P}")
+        H, sl = h * P, s // P
+        shape = (b, H, sl, d)
+        strides = (sl * H * d, d, H * d, 1)  # token-major: feeds the O projection directly
+    return shape, strides
+
+
+@torch.library.custom_op("autosp::all_to_all", mutates_args=(), device_types="cuda")
+def all_to_all(xs: list[torch.Tensor], direction: int, group: str) -> list[torch.Tensor]:
+    st = sp_dist.lookup(group)
+    P = st.world
+    if P == 1:
+        return [x.clone() for x in xs]  # executor.py:208-209 (P == 1 -> copy)
+    pool = st.pool
+    descs, outs, first_off = [], [], None
+    b, _, s, d = xs[0].shape
+    for x in xs:
+        if x.stride(-1) != 1:
+            x = x.contiguous()
+        shape, strides = _out_geometry(x, direction, P)
+        nbytes = math.prod(shape) * x.element_size()
+        off, base = pool.alloc(nbytes)
+        first_off = off if first_off is None else first_off
+        out = base.view(x.dtype).as_strided(shape, strides)
+        outs.append(out)
+        # kernel convention: logical [b, s, h, d] element strides of source and destination
+        src_bshd = x.permute(0, 2, 1, 3)
+        descs.append(kernels.a2a_tensor_desc(src_bshd, x.shape[1], off,
+                                             (strides[0], strides[2], strides[1])))
+    s_glob = s * P if direction == SEQ_TO_HEAD_DIR else s
+    epoch = pool.next_epoch()
+    kernels.a2a_launch(direction, descs, b, s_glob, d, xs[0].element_size(), P, st.rank,
+                       pool.region_ptrs, pool.flag_ptrs, epoch)
+    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, first_off)
+    return outs
+
+
+@all_to_all.register_fake
+def _all_to_all_fake(xs, direction, group):
+    P = sp_dist.lookup(group).world
+    outs = []
+    for x in xs:
+        shape, strides = _out_geometry(x, direction, P)
+        outs.append(x.new_empty_strided(shape, strides))
+    return outs
+
+
+def _a2a_setup(ctx, inputs, output):
+    _, direction, group = inputs
+    ctx.direction, ctx.group = direction, group
+
+
+def _a2a_bwd(ctx, grads):
+    inv = HEAD_TO_SEQ_DIR if ctx.direction == SEQ_TO_HEAD_DIR else SEQ_TO_HEAD_DIR
+    return all_to_all(list(grads), inv, ctx.group), None, None
+
+
+def _a2a_setup_shapes(ctx, inputs, output):
+    _a2a_setup(ctx, inputs, output)
+
+
+all_to_all.register_autograd(_a2a_bwd, setup_context=_a2a_setup)
+
+
+def ulysses_attention(q, k, v, group: str, is_causal=True, scale=None):
+    """The Ulysses attention block the auto_sp pass substitutes for SDPA
+    (sp_pass.py:172-195): a2a seq->head of (q, k, v) in one launch, causal attention over
+    the full sequence on the local heads, a2a head->seq of the output."""
+    (q, k, v), dt = _cast_in(q, k, v)
+    if k is v:  # reference model: q = k = v -> move the tensor once (transformer.py:3-6)
+        kk = [q] if q is k else [q, k]
+        moved = all_to_all(kk, SEQ_TO_HEAD_DIR, group)
+        qh, kh = moved[0], moved[-1]
+        vh = kh
+    else:
+        qh, kh, vh = all_to_all([q, k, v], SEQ_TO_HEAD_DIR, group)
+    oh = _sdpa(qh, kh, vh, is_causal, scale)
+    (o,) = all_to_all([oh], HEAD_TO_SEQ_DIR, group)
+    return o if dt is None else o.to(dt)

@@ -1,0 +1,181 @@
+"""``sp_ac`` — sequence-aware activation checkpointing as an AOTAutograd partitioner.
+
+Reference: ``ac_pass.py`` (``AcMode`` :26-29, ``guarded_nodes`` :103-114,
+``build_flow_network`` :117-139, ``min_cut`` :142-178).  The joint forward+backward
+graph is turned into a split-node flow network — node ``n`` becomes ``n_in -> n_out``
+with capacity = bytes of its output, data edges and source/sink wiring are infinite —
+and the minimum source/sink cut picks the cheapest set of forward values to keep; every
+other value the backward needs is recomputed in the backward graph.
+
+Modes differ only in which forward nodes get an infinite source edge (a *guard*: may
+not be recomputed):
+
+* ``conservative``  every matmul + the AutoSP ops  (≈ torch's default policy)
+* ``seq-aware``     only the attention region (default; the paper's sp_ac): projections
+                    and MLP matmuls may be recomputed, attention never is
+* ``seq-aware-all`` no matmul guards
+
+Deliberate divergence from the reference (SURVEY §0 findings 2/3, north star): in every
+mode the all-to-all outputs and the attention outputs (O, LSE) are guarded, so backward
+never re-issues communication and never re-runs the O(s^2) forward; the saved state of
+attention is O + LSE (flash-style), never the probabilities.
+"""
+
+from __future__ import annotations
+
+import operator
+from enum import Enum
+
+import torch
+import torch.fx as fx
+
+from .errors import InfeasibleError
+
+
+class AcMode(str, Enum):  # ac_pass.py:26-29
+    CONSERVATIVE = "conservative"
+    SEQ_AWARE_NON_ATTENTION = "seq-aware"
+    SEQ_AWARE_ALL = "seq-aware-all"
+
+
+RECOMPUTE_PENALTY = 0.05  # fraction of a node's bytes charged when it is recomputed
+MATMUL_PENALTY = 4.0      # matmuls cost more to recompute than elementwise ops
+_MATMULS = {"mm", "addmm", "bmm", "baddbmm", "matmul", "linear", "_scaled_mm"}
+
+
+def _opname(n: fx.Node) -> str:
+    t = n.target
+    if hasattr(t, "_schema"):
+        return t._schema.name  # e.g. "aten::mm", "autosp::all_to_all"
+    return getattr(t, "__name__", str(t))
+
+
+def is_autosp_collective(n: fx.Node) -> bool:
+    return n.op == "call_function" and _opname(n) == "autosp::all_to_all"
+
+
+def is_autosp_attention(n: fx.Node) -> bool:
+    return n.op == "call_function" and _opname(n) == "autosp::attention"
+
+
+def _is_matmul(n: fx.Node) -> bool:
+    name = _opname(n)
+    return name.startswith("aten::") and name[6:] in _MATMULS
+
+
+def _nbytes(n: fx.Node) -> int | None:
+    v = n.meta.get("val")
+    if isinstance(v, torch.Tensor):
+        return v.numel() * v.element_size()
+    if isinstance(v, (int, float, bool, torch.SymInt)) or v is None:
+        return 0 if not isinstance(v, torch.Tensor) and n.op == "placeholder" else None
+    return None  # tuples / lists: cannot be saved as a unit
+
+
+def guarded(n: fx.Node, mode: AcMode) -> bool:
+    """Forward nodes that must not be recomputed (ac_pass.py:103-114 + the AutoSP guard)."""
+    if is_autosp_collective(n) or is_autosp_attention(n):
+        return True
+    if n.op == "call_function" and n.target is operator.getitem:
+        src = n.args[0]
+        if isinstance(src, fx.Node) and (is_autosp_collective(src) or is_autosp_attention(src)):
+            return True
+    if mode is AcMode.CONSERVATIVE and _is_matmul(n):
+        return True
+    return False
+
+
+def plan(joint_module: fx.GraphModule, num_fwd_outputs: int, mode: AcMode):
+    """Return (saved_values, saved_sym_nodes, stats) for the joint graph."""
+    import networkx as nx
+    from torch._functorch.partitioners import classify_nodes
+
+    info = classify_nodes(joint_module, [], num_fwd_outputs)
+    # forward side = everything computable without the tangents (values only the backward
+    # consumes, e.g. the attention LSE, are still forward values: saved or recomputed)
+    fw = {n for n in joint_module.graph.nodes
+          if n.op != "output" and n not in info.tangents_closure}
+    G = nx.DiGraph()
+    INF = float("inf")
+
+    def add(u, v, cap=None):
+        if cap is None:
+            G.add_edge(u, v)  # no capacity attribute = infinite (networkx)
+        else:
+            G.add_edge(u, v, capacity=cap)
+
+    for n in joint_module.graph.nodes:
+        if n.op == "output":
+            continue
+        if n in fw:
+            if n.op == "placeholder":
+                add("source", n.name + "_in")
+            b = _nbytes(n)
+            sym = isinstance(n.meta.get("val"), torch.SymInt)
+            cap = None if (b is None and not sym) else (b or 1)
+            add(n.name + "_in", n.name + "_out", cap)
+            if guarded(n, mode):
+                add("source", n.name + "_in")
+            elif n.op != "placeholder" and b:
+                # recompute is not free: a node recomputed in backward (n_in on the sink
+                # side) pays a penalty, so long recompute chains lose to saving a small
+                # boundary value (the residual stream) -- keeps peak memory bounded
+                pen = RECOMPUTE_PENALTY * b * (MATMUL_PENALTY if _is_matmul(n) else 1.0)
+                add("source", n.name + "_in", max(1, int(pen)))
+            for u in n.users:
+                if u in fw:
+                    add(n.name + "_out", u.name + "_in")
+                elif u.op != "output":
+                    add(n.name + "_out", u.name + "_in")
+        else:
+            add(n.name + "_in", "sink")
+            for u in n.users:
+                if u.op != "output":
+                    add(n.name + "_in", u.name + "_in")
+    if "sink" not in G or "source" not in G:
+        return [], [], {"cut_bytes": 0}
+    try:
+        cut_value, (reach, _) = nx.minimum_cut(G, "source", "sink")
+    except nx.NetworkXUnbounded:
+        inf_only = nx.DiGraph([(u, v) for u, v, d in G.edges(data=True) if "capacity" not in d])
+        path = nx.shortest_path(inf_only, "source", "sink") if inf_only.has_node("sink") else []
+        raise InfeasibleError(f"sp_ac: forced-save path through {path}") from None
+    if cut_value == INF:
+        raise InfeasibleError(f"sp_ac plan infeasible under mode {mode.value}")
+    saved = [n for n in joint_module.graph.nodes
+             if n in fw and n.name + "_in" in reach and n.name + "_out" not in reach]
+    saved_sym = [n for n in saved if not isinstance(n.meta.get("val"), torch.Tensor)]
+    saved_vals = [n for n in saved if isinstance(n.meta.get("val"), torch.Tensor)]
+    recomputed = [n for n in fw if n.op != "placeholder" and n.name + "_out" not in reach]
+    stats = {"cut_bytes": int(cut_value), "saved": [n.name for n in saved_vals],
+             "recomputed_candidates": len(recomputed), "mode": mode.value}
+    return saved_vals, saved_sym, stats
+
+
+LAST_PLAN: dict = {}
+
+
+def make_partition_fn(mode: AcMode = AcMode.SEQ_AWARE_NON_ATTENTION):
+    from torch._functorch.partitioners import (_extract_fwd_bwd_modules,
+                                               reordering_to_mimic_autograd_engine)
+
+    def partition(joint_module: fx.GraphModule, _joint_inputs, *, num_fwd_outputs, **kwargs):
+        saved_vals, saved_sym, stats = plan(joint_module, num_fwd_outputs, mode)
+        fw_mod, bw_mod = _extract_fwd_bwd_modules(joint_module, saved_vals, saved_sym,
+                                                  num_fwd_outputs=num_fwd_outputs)
+        # recompute each value just before its first backward use (ref schedule.py:45-85)
+        bw_mod = reordering_to_mimic_autograd_engine(bw_mod)
+        stats["bw_recomputed_ops"] = sorted({_opname(n) for n in bw_mod.graph.nodes
+                                             if n.op == "call_function"})
+        # every forward a2a has exactly one gradient a2a in backward; more means a
+        # forward collective was recomputed (the reference's failure mode, SURVEY finding 2)
+        n_fw = sum(is_autosp_collective(n) for n in fw_mod.graph.nodes)
+        n_bw = sum(is_autosp_collective(n) for n in bw_mod.graph.nodes)
+        stats["fw_collectives"], stats["bw_collectives"] = n_fw, n_bw
+        stats["bw_recomputes_attention"] = any(is_autosp_attention(n)
+                                               for n in bw_mod.graph.nodes)
+        LAST_PLAN.clear()
+        LAST_PLAN.update(stats)
+        return fw_mod, bw_mod
+
+    return partition
