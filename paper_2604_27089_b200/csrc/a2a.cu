@@ -70,10 +70,7 @@ template <typename V>
 __global__ void __launch_bounds__(kA2AThreads) a2a_push_kernel(const __grid_constant__ A2AParams p) {
   constexpr int G = sizeof(V);
   const int tid = threadIdx.x;
-  // 0) publish "I reached epoch" and wait for every peer to have reached it too
-  if (tid == 0) st_release_sys(p.peer_flags[p.rank] + kReadyWord, p.epoch);
-  if (tid < p.P && tid != p.rank) spin_until_epoch(p.peer_flags[tid] + kReadyWord, p.epoch);
-  __syncthreads();
+  // (the ready handshake ran in a2a_handshake_kernel just before, stream-ordered)
 
   const int vpr = p.d * p.eb / G;  // vectors per row (1..32)
   const int rows_per_pass = min(32 / vpr, kTileTokens);
@@ -147,6 +144,15 @@ __global__ void __launch_bounds__(kA2AThreads) a2a_push_kernel(const __grid_cons
         }
     }
   }
+}
+
+// 0) publish "I reached epoch" and wait until every peer has reached it too.  One CTA:
+//    the only spinning work of a call is tiny, so it can never starve the push kernels of
+//    other ranks sharing the GPU (single-GPU loopback) and costs one short launch.
+__global__ void a2a_handshake_kernel(const __grid_constant__ A2AParams p) {
+  const int tid = threadIdx.x;
+  if (tid == 0) st_release_sys(p.peer_flags[p.rank] + kReadyWord, p.epoch);
+  if (tid < p.P && tid != p.rank) spin_until_epoch(p.peer_flags[tid] + kReadyWord, p.epoch);
 }
 
 __global__ void a2a_wait_kernel(uint32_t* flags, int P, int rank, uint32_t epoch,
@@ -272,6 +278,7 @@ extern "C" int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n
   if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (world > 1) a2a_handshake_kernel<<<1, 32, 0, st>>>(p);
   switch (align) {
     case 16: a2a_push_kernel<uint4><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
     case 8: a2a_push_kernel<uint2><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;

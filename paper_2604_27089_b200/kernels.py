@@ -18,6 +18,56 @@ from .errors import ValidationError
 SUPPORTED_HEAD_DIMS = (32, 64, 128)
 
 
+class LaunchLog:
+    """Counts the kernels this module launches and (optionally) times the attention
+    calls with CUDA events on the launching stream (used by bench.py for the live
+    roofline: algorithmic FLOPs per launch / measured launch duration)."""
+
+    def __init__(self):
+        self.enabled = False
+        self.timing = False
+        self.launches = 0
+        self.events: dict[str, list] = {}
+        self.flops: dict[str, float] = {}
+
+    def reset(self, timing: bool = False):
+        self.enabled, self.timing = True, timing
+        self.launches = 0
+        self.events, self.flops = {}, {}
+
+    def begin(self, name: str):
+        if not (self.enabled and self.timing):
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def end(self, name: str, start, n_kernels: int, flops: float = 0.0):
+        if self.enabled:
+            self.launches += n_kernels
+        if start is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.events.setdefault(name, []).append((start, e))
+            self.flops[name] = self.flops.get(name, 0.0) + flops
+
+    def summary(self) -> dict:
+        out = {}
+        for name, pairs in self.events.items():
+            ms = sum(a.elapsed_time(b) for a, b in pairs)
+            out[name] = {"calls": len(pairs), "ms": ms, "flops": self.flops.get(name, 0.0)}
+        return out
+
+
+LOG = LaunchLog()
+
+
+def causal_attn_flops(b: int, hq: int, s: int, d: int, causal: bool = True) -> float:
+    """Algorithmic forward FLOPs: 2 GEMMs (QK^T, PV) over the unmasked (lower) triangle."""
+    pairs = s * (s + 1) / 2 if causal else float(s) * s
+    return 4.0 * b * hq * d * pairs
+
+
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -44,10 +94,12 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool = T
     scale = 1.0 / math.sqrt(d) if scale is None else scale
     o = torch.empty((b, hq, s, d), dtype=torch.bfloat16, device=q.device) if out is None else out
     lse = torch.empty((b, hq, s), dtype=torch.float32, device=q.device)
+    ev = LOG.begin("attn_fwd")
     rc = lib.autosp_attn_fwd(_attn_tensor(q, "q"), _attn_tensor(k, "k"), _attn_tensor(v, "v"),
                              _attn_tensor(o, "o"), lse.data_ptr(), b, hq, hkv, s, d,
                              float(scale), int(causal), _stream())
     _lib.check(rc, "attn_fwd")
+    LOG.end("attn_fwd", ev, 1, causal_attn_flops(b, hq, s, d, causal))
     return o, lse
 
 
@@ -67,12 +119,14 @@ def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = Non
                      device=dev)
     if not lse.is_contiguous() or lse.dtype != torch.float32:
         raise ValidationError("attn_bwd: lse must be contiguous fp32 [b, hq, s]")
+    ev = LOG.begin("attn_bwd")
     rc = lib.autosp_attn_bwd(_attn_tensor(q, "q"), _attn_tensor(k, "k"), _attn_tensor(v, "v"),
                              _attn_tensor(o, "o"), _attn_tensor(do, "do"), lse.data_ptr(),
                              _attn_tensor(dq, "dq"), _attn_tensor(dk, "dk"),
                              _attn_tensor(dv, "dv"), ws.data_ptr(), b, hq, hkv, s, d,
                              float(scale), int(causal), _stream())
     _lib.check(rc, "attn_bwd")
+    LOG.end("attn_bwd", ev, 3, 2.5 * causal_attn_flops(b, hq, s, d, causal))
     return dq, dk, dv
 
 
@@ -94,15 +148,18 @@ def a2a_launch(direction: int, descs: list, b: int, s_global: int, d: int, elem_
     arr = (_lib.A2ATensor * len(descs))(*descs)
     pb = (C.c_void_p * world)(*peer_base)
     pf = (C.c_void_p * world)(*peer_flags)
+    ev = LOG.begin("a2a")
     rc = lib.autosp_a2a(direction, arr, len(descs), b, s_global, d, elem_bytes, world, rank,
                         pb, pf, epoch & 0xFFFFFFFF, _stream())
     _lib.check(rc, "a2a")
+    LOG.end("a2a", ev, 2 if world > 1 else 1)
 
 
 def a2a_wait(local_flags: int, world: int, rank: int, epoch: int, first_dst_offset: int = 0) -> None:
     rc = _lib.load().autosp_a2a_wait(local_flags, world, rank, epoch & 0xFFFFFFFF,
                                      first_dst_offset, _stream())
     _lib.check(rc, "a2a_wait")
+    LOG.end("a2a_wait", None, 1 if world > 1 else 0)
 
 
 def a2a_mark_ready(flags: list[int], epoch: int) -> None:

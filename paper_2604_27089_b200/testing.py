@@ -77,3 +77,22 @@ def enable_cpu_lowering() -> None:
         return outs
 
     _ENABLED = True
+
+
+def loopback_states(P: int, nbytes: int, device="cuda", prefix: str = "loop"):
+    """P virtual SP ranks on ONE GPU (test / single-GPU bench harness): every rank's
+    receive region and flag block is a local allocation and each rank's pool maps all of
+    them, so the real push kernels and epoch protocol run unchanged.  Returns the
+    SPStates (group names f"{prefix}{r}") and the backing buffers (keep them alive)."""
+    from . import dist as sp_dist
+    flags = torch.zeros((P, 1024), dtype=torch.int32, device=device)
+    regions = [torch.empty(nbytes, dtype=torch.uint8, device=device) for _ in range(P)]
+    peers = [(flags[j].data_ptr(), regions[j].data_ptr()) for j in range(P)]
+    states = []
+    for r in range(P):
+        pool = sp_dist.SymmetricPool(nbytes, P, r, torch.device(device), peers=peers)
+        st = sp_dist.SPState(world=P, rank=r, group=None, device=torch.device(device),
+                             pool=pool, name=f"{prefix}{r}")
+        sp_dist._REGISTRY[st.name] = st
+        states.append(st)
+    return states, (flags, regions)
