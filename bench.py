@@ -261,10 +261,12 @@ def main():
     kernels.LOG.reset(timing=True)
     barrier()
     with ClockSampler(dev.index or 0) as clk:
+        torch.cuda.nvtx.range_push("timed")
         e0.record()
         for _ in range(args.steps):
             loss = step(ids, labels)
         e1.record()
+        torch.cuda.nvtx.range_pop()
         barrier()
     launches = kernels.LOG.launches
     ksum = kernels.LOG.summary()

@@ -69,7 +69,7 @@ def _ulysses_rank(st, x_full, do_full, results, r, P, causal=True):
     torch.cuda.set_device(0)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        sl = x_full.shape[2] // P
+        sl = x_full[0].shape[2] // P
         q = x_full[0][:, :, r * sl:(r + 1) * sl].clone().requires_grad_(True)
         k = x_full[1][:, :, r * sl:(r + 1) * sl].clone().requires_grad_(True)
         v = x_full[2][:, :, r * sl:(r + 1) * sl].clone().requires_grad_(True)
