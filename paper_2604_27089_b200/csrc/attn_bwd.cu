@@ -58,20 +58,29 @@ struct Cfg {
   static constexpr int SBO = 8 * SW;
   static constexpr int TILE = 128 * D * 2;  // one [128 x D] bf16 tile
   static constexpr int kQStages = D == 128 ? 1 : 2;
+  // S^T buffers in TMEM: two (S(t+1) overlaps the softmax of t) when d <= 64
+  static constexpr int NSB = D == 128 ? 1 : 2;
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = TILE;
   static constexpr int Q_OFF = 2 * TILE;                       // Q[st]
   static constexpr int DO_OFF = Q_OFF + kQStages * TILE;       // dO[st]
   static constexpr int DS_OFF = DO_OFF + kQStages * TILE;      // dS^T [128 keys x 128 q] bf16
   static constexpr int DQ_OFF = DS_OFF + 128 * 128 * 2;        // 2 fp32 chunks [128 x 32]
-  static constexpr int LSE_OFF = DQ_OFF + 2 * 128 * 32 * 4;    // lse2[2][128], delta[2][128]
+  static constexpr int LSE_OFF = DQ_OFF + 2 * 128 * 32 * 4;    // lse[st][128], delta[st][128]
   static constexpr int BAR_OFF = LSE_OFF + 4 * 128 * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + D;
+  // TMEM columns.  d <= 64: S0 | S1 | dP (dS bf16 in cols 0..63, dQ fp32 in 64..64+D) | dV | dK
+  //                d = 128: S (dQ reuses it after dV consumed P) | dP | dV | dK
+  static constexpr uint32_t DP_COL = NSB * 128;
+  static constexpr uint32_t DV_COL = DP_COL + 128;
+  static constexpr uint32_t DK_COL = DV_COL + D;
+  static constexpr uint32_t DQ_COL = NSB == 2 ? DP_COL + 64 : 0;
+  static_assert(DK_COL + D <= 512, "TMEM budget");
 };
 
 struct Params {
-  CUtensorMap tm_q, tm_k, tm_v, tm_do, tm_dqacc;
+  CUtensorMap tm_q, tm_k, tm_v, tm_do, tm_dqacc, tm_lse, tm_dlt;
+  int lse_tma;         // lse/delta rows staged by TMA with Q/dO (needs S % 4 == 0)
   const float* lse;    // [B, Hq, S]
   const float* delta;  // [B, Hq, S]
   __nv_bfloat16* dk;
@@ -112,14 +121,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   uint64_t* kv_full = bars + 0;
   uint64_t* q_full = bars + 1;                  // [kQStages]
   uint64_t* q_empty = q_full + C::kQStages;     // [kQStages]
-  uint64_t* sdp_full = q_empty + C::kQStages;   // S^T and dP^T in TMEM
-  uint64_t* p_ready = sdp_full + 1;             // P^T, dS^T written (128 arrivals)
-  uint64_t* dq_full = p_ready + 1;              // dQ MMA complete (also: dS smem free)
+  uint64_t* s_full = q_empty + C::kQStages;     // [NSB] S^T(t) in TMEM
+  uint64_t* dp_full = s_full + 2;               // dP^T(t) in TMEM
+  uint64_t* p_ready = dp_full + 1;              // P^T written (128 arrivals)
+  uint64_t* ds_ready = p_ready + 1;             // dS^T written to TMEM + smem (128 arrivals)
+  uint64_t* dq_full = ds_ready + 1;             // dQ MMA complete
   uint64_t* dq_empty = dq_full + 1;             // dQ drained from TMEM (128 arrivals)
   uint64_t* acc_full = dq_empty + 1;            // final dK/dV complete
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_full + 1);
-  float* lse_s = reinterpret_cast<float*>(smem + C::LSE_OFF);  // [2][128]
-  float* dlt_s = lse_s + 256;                                   // [2][128]
+  float* lse_s = reinterpret_cast<float*>(smem + C::LSE_OFF);  // [kQStages][128]
+  float* dlt_s = lse_s + 256;                                   // [kQStages][128]
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -139,8 +150,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       mbar_init(q_full + s, 1);
       mbar_init(q_empty + s, 1);
     }
-    mbar_init(sdp_full, 1);
+    mbar_init(s_full + 0, 1);
+    mbar_init(s_full + 1, 1);
+    mbar_init(dp_full, 1);
     mbar_init(p_ready, 128);
+    mbar_init(ds_ready, 128);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 128);
     mbar_init(acc_full, 1);
@@ -150,6 +164,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     tma_prefetch_desc(&p.tm_v);
     tma_prefetch_desc(&p.tm_do);
     tma_prefetch_desc(&p.tm_dqacc);
+    if (p.lse_tma) {
+      tma_prefetch_desc(&p.tm_lse);
+      tma_prefetch_desc(&p.tm_dlt);
+    }
   }
   if (warp == 2) tmem_alloc<512>(tmem_holder);
   tc_fence_before();
@@ -179,7 +197,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         const int head = kvh * group + t / per_head;
         const int q0 = (m_first + t % per_head) * BQ;
         mbar_wait(q_empty + st, ph ^ 1);
-        mbar_arrive_expect_tx(q_full + st, 2 * C::TILE);
+        mbar_arrive_expect_tx(q_full + st, 2 * C::TILE + (p.lse_tma ? 2 * 128 * 4 : 0));
+        if (p.lse_tma) {  // the softmax warps need lse/delta of these 128 queries
+          tma_load_2d(lse_s + st * 128, &p.tm_lse, q_full + st, q0, batch * p.Hq + head);
+          tma_load_2d(dlt_s + st * 128, &p.tm_dlt, q_full + st, q0, batch * p.Hq + head);
+        }
         for (int c = 0; c < C::NCH; ++c) {
           tma_load_4d(smem + C::Q_OFF + st * C::TILE + c * 128 * C::SW, &p.tm_q, q_full + st,
                       c * C::CE, q0, head, batch, pol_last);
@@ -194,36 +216,52 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, 0, 0);   // K-major x K-major
       constexpr uint32_t idesc_g = make_idesc_bf16(128, D, 0, 1);     // TMEM A x MN-major B
       constexpr uint32_t idesc_q = make_idesc_bf16(128, D, 1, 1);     // MN-major A and B
-      mbar_wait(kv_full, 0);
-      for (int t = 0; t < T; ++t) {
-        const int st = t % C::kQStages;
-        const uint32_t ph = (t / C::kQStages) & 1;
-        const uint32_t qa = s_q + st * C::TILE;
-        const uint32_t da = s_do + st * C::TILE;
-        mbar_wait(q_full + st, ph);
+      auto issue_s = [&](int t) {  // S^T(t) = K Q(t)^T
+        const uint32_t qa = s_q + (t % C::kQStages) * C::TILE;
+        mbar_wait(q_full + (t % C::kQStages), (t / C::kQStages) & 1);
         tc_fence_after();
-        // S^T = K Q^T (S cols were last read by dV(t-1), issued earlier: in-order)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tmem + C::S_COL, desc_kmajor<D>(s_k, kk), desc_kmajor<D>(qa, kk), idesc_s,
-                 kk > 0);
-        // dP^T = V dO^T into the dP cols, which held dQ(t-1): wait for its drain
+          mma_ss(tmem + (t % C::NSB) * 128, desc_kmajor<D>(s_k, kk), desc_kmajor<D>(qa, kk),
+                 idesc_s, kk > 0);
+        tc_commit(s_full + (t % C::NSB));
+      };
+      mbar_wait(kv_full, 0);
+      if (C::NSB == 2) issue_s(0);
+      for (int t = 0; t < T; ++t) {
+        const int st = t % C::kQStages;
+        const uint32_t qa = s_q + st * C::TILE;
+        const uint32_t da = s_do + st * C::TILE;
+        const uint32_t s_col = (t % C::NSB) * 128;
+        // the dP region (and for d = 128 the S region) held dQ(t-1): wait for its drain
         if (t > 0) {
           mbar_wait(dq_empty, (t - 1) & 1);
           tc_fence_after();
         }
+        if (C::NSB == 1) issue_s(t);
+        else {
+          mbar_wait(q_full + st, (t / C::kQStages) & 1);
+          tc_fence_after();
+        }
+        // dP^T(t) = V dO(t)^T
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           mma_ss(tmem + C::DP_COL, desc_kmajor<D>(s_v, kk), desc_kmajor<D>(da, kk), idesc_s,
                  kk > 0);
-        tc_commit(sdp_full);
-        // gradients once the softmax warps have produced P^T and dS^T
+        tc_commit(dp_full);
+        // S^T(t+1) overlaps the softmax of tile t (its buffer held P(t-1): consumed by
+        // dV(t-1), issued earlier -> in-order)
+        if (C::NSB == 2 && t + 1 < T) issue_s(t + 1);
+        // dV += P^T dO once the exps of tile t are done
         mbar_wait(p_ready, t & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk)
-          mma_ts(tmem + C::DV_COL, tmem + C::S_COL + kk * 8, desc_mn<D>(da, kk), idesc_g,
+          mma_ts(tmem + C::DV_COL, tmem + s_col + kk * 8, desc_mn<D>(da, kk), idesc_g,
                  (t > 0 || kk > 0) ? 1u : 0u);
+        // dK += dS^T Q and dQ(t) = dS K once dS is in TMEM + smem
+        mbar_wait(ds_ready, t & 1);
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk)
           mma_ts(tmem + C::DK_COL, tmem + C::DP_COL + kk * 8, desc_mn<D>(qa, kk), idesc_g,
@@ -231,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         tc_commit(q_empty + st);
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk)
-          mma_ss(tmem + C::DP_COL, desc_ds(s_ds, kk), desc_mn<D>(s_k, kk), idesc_q, kk > 0);
+          mma_ss(tmem + C::DQ_COL, desc_ds(s_ds, kk), desc_mn<D>(s_k, kk), idesc_q, kk > 0);
         tc_commit(dq_full);
       }
       tc_commit(acc_full);
@@ -242,54 +280,79 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     const int row = quarter * 32 + lane;  // key row within the tile
     const int key = k0 + row;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t s_addr = tmem + lane_base + C::S_COL;
     const uint32_t dp_addr = tmem + lane_base + C::DP_COL;
     uint8_t* ds_row = smem + C::DS_OFF + row * 128;
     const float LOG2E = 1.4426950408889634f;
     for (int t = 0; t < T; ++t) {
       const int head = kvh * group + t / per_head;
       const int q0 = (m_first + t % per_head) * BQ;
-      float* lse_b = lse_s + (t & 1) * 128;
-      float* dlt_b = dlt_s + (t & 1) * 128;
-      {
+      const uint32_t s_addr = tmem + lane_base + (t % C::NSB) * 128;
+      const int st = t % C::kQStages;
+      float* lse_b = lse_s + st * 128;
+      float* dlt_b = dlt_s + st * 128;
+      if (!p.lse_tma) {  // S % 4 != 0: stage lse/delta through registers (slow path)
+        if (t >= C::kQStages) named_bar_sync(1, 128);  // everyone done with this slot
         const int q = q0 + row;
         const int64_t idx = ((int64_t)batch * p.Hq + head) * p.S + q;
-        lse_b[row] = q < p.S ? p.lse[idx] * LOG2E : INFINITY;
+        lse_b[row] = q < p.S ? p.lse[idx] : 0.f;
         dlt_b[row] = q < p.S ? p.delta[idx] : 0.f;
+        named_bar_sync(1, 128);
       }
-      named_bar_sync(1, 128);
       const bool diag = p.causal && (q0 < k0 + BK);
       const bool oob = (k0 + BK > p.S) || (q0 + BQ > p.S);
-      mbar_wait(sdp_full, t & 1);
+      // ---- part 1: P^T = exp2(S^T c - lse) -> bf16 into the S columns
+      mbar_wait(s_full + (t % C::NSB), (t / C::NSB) & 1);
       tc_fence_after();
-      if (t > 0) mbar_wait(dq_full, (t - 1) & 1);  // dQ(t-1) MMA done reading dS smem
 #pragma unroll
       for (int c4 = 0; c4 < BQ / 32; ++c4) {
-        uint32_t sr[32], dr[32];
+        uint32_t sr[32], pk[16];
         tmem_ld32(s_addr + c4 * 32, sr);
-        tmem_ld32(dp_addr + c4 * 32, dr);
         tmem_wait_ld();
-        uint32_t pk[16], dk[16];
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
-          float pv[2], dv[2];
+          float pv[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int col = c4 * 32 + 2 * c + e;
-            const float sv = __uint_as_float(sr[2 * c + e]);
-            float pp = fast_exp2(fmaf(sv, p.scale_log2, -lse_b[col]));
+            float pp = fast_exp2(fmaf(__uint_as_float(sr[2 * c + e]), p.scale_log2,
+                                      -lse_b[col] * LOG2E));
             if ((diag || oob) &&
                 ((p.causal && key > q0 + col) || key >= p.S || q0 + col >= p.S))
               pp = 0.f;
             pv[e] = pp;
-            dv[e] = pp * (__uint_as_float(dr[2 * c + e]) - dlt_b[col]);
           }
           pk[c] = pack_bf16(pv[0], pv[1]);
-          dk[c] = pack_bf16(dv[0], dv[1]);
         }
         tmem_st16(s_addr + c4 * 16, pk);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_ready);
+      // ---- part 2: dS^T = P^T (dP^T - delta) -> bf16 into the dP columns and smem
+      // (dp_full(t) also implies dQ(t-1) finished reading the smem dS tile)
+      mbar_wait(dp_full, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c4 = 0; c4 < BQ / 32; ++c4) {
+        uint32_t dr[32], pk[16];
+        tmem_ld32(dp_addr + c4 * 32, dr);
+        tmem_ld16(s_addr + c4 * 16, pk);  // P^T (bf16) written in part 1
+        tmem_wait_ld();
+        uint32_t dk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int col = c4 * 32 + 2 * c;
+          const float2 pf = __bfloat1622float2(
+              *reinterpret_cast<const __nv_bfloat162*>(&pk[c]));
+          float d0 = dlt_b[col], d1 = dlt_b[col + 1];
+          if (oob) {  // TMA zero-fills rows past S; keep 0 * (x - garbage) out of dS
+            d0 = (q0 + col < p.S) ? d0 : 0.f;
+            d1 = (q0 + col + 1 < p.S) ? d1 : 0.f;
+          }
+          dk[c] = pack_bf16(pf.x * (__uint_as_float(dr[2 * c]) - d0),
+                            pf.y * (__uint_as_float(dr[2 * c + 1]) - d1));
+        }
         tmem_st16(dp_addr + c4 * 16, dk);
-        // dS^T row -> smem (chunk = 64 queries = 128 B per key row, 128B swizzle)
         uint8_t* chunk = ds_row + (c4 >> 1) * (128 * 128);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -301,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(p_ready);
+      mbar_arrive(ds_ready);
     }
     // ---- epilogue: dV, dK (scaled) straight from TMEM
     if (T > 0) {
@@ -346,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;  // query row within the step
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t dq_addr = tmem + lane_base + C::DP_COL;
+    const uint32_t dq_addr = tmem + lane_base + C::DQ_COL;
     const bool leader = (warp == 8 && lane == 0);
     for (int t = 0; t < T; ++t) {
       const int head = kvh * group + t / per_head;
@@ -464,6 +527,20 @@ inline bool make_map_f32_3d(CUtensorMap* map, void* ptr, int BH, int S, int D) {
          CUDA_SUCCESS;
 }
 
+// [rows, S] fp32 (row stride S), box {128, 1}: one query tile of lse / delta
+inline bool make_map_rows_f32(CUtensorMap* map, const void* ptr, int rows, int S) {
+  PFN_encodeTiled enc = get_encode_tiled();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)S, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)S * 4};
+  cuuint32_t box[2] = {128, 1};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 template <int D>
 int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autosp_attn_tensor& v,
            const autosp_attn_tensor& o, const autosp_attn_tensor& d_o, const float* lse,
@@ -503,6 +580,8 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
             make_map_bhsd(&p.tm_v, v.ptr, B, Hkv, S, D, v.stride_b, v.stride_h, v.stride_s,
                           C::CE, 128, C::SW) &&
             make_map_f32_3d(&p.tm_dqacc, dqacc, B * Hq, S, D);
+  p.lse_tma = (S % 4 == 0) && make_map_rows_f32(&p.tm_lse, lse, B * Hq, S) &&
+              make_map_rows_f32(&p.tm_dlt, delta, B * Hq, S);
   if (!ok) {
     autosp_set_error("attn_bwd: cuTensorMapEncodeTiled failed (alignment/strides?)");
     return AUTOSP_ERR_VALIDATION;

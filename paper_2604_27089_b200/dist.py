@@ -25,6 +25,7 @@ from dataclasses import dataclass, field
 
 import torch
 import torch.distributed as tdist
+import torch.utils.dlpack
 
 from . import _lib
 from .errors import ValidationError
@@ -33,17 +34,53 @@ FLAG_BYTES = 4096  # flag block (256 B used) padded to keep the receive region a
 DEFAULT_POOL_BYTES = int(os.environ.get("AUTOSP_POOL_BYTES", str(8 << 30)))
 
 
-class _CAI:
-    """Minimal __cuda_array_interface__ wrapper: a zero-copy torch view of raw memory."""
+class _DLDevice(C.Structure):
+    _fields_ = [("device_type", C.c_int), ("device_id", C.c_int)]
 
-    def __init__(self, ptr: int, nbytes: int):
-        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
-                                         "data": (ptr, False), "version": 3,
-                                         "strides": None, "stream": None}
+
+class _DLDataType(C.Structure):
+    _fields_ = [("code", C.c_uint8), ("bits", C.c_uint8), ("lanes", C.c_uint16)]
+
+
+class _DLTensor(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("device", _DLDevice), ("ndim", C.c_int),
+                ("dtype", _DLDataType), ("shape", C.POINTER(C.c_int64)),
+                ("strides", C.POINTER(C.c_int64)), ("byte_offset", C.c_uint64)]
+
+
+class _DLManagedTensor(C.Structure):
+    pass
+
+
+_DLManagedTensor._fields_ = [("dl_tensor", _DLTensor), ("manager_ctx", C.c_void_p),
+                             ("deleter", C.CFUNCTYPE(None, C.POINTER(_DLManagedTensor)))]
+_PyCapsule_New = C.pythonapi.PyCapsule_New
+_PyCapsule_New.restype = C.py_object
+_PyCapsule_New.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+_KEEP: dict[int, tuple] = {}
+
+
+@C.CFUNCTYPE(None, C.POINTER(_DLManagedTensor))
+def _dl_deleter(ptr):
+    _KEEP.pop(C.addressof(ptr.contents), None)
 
 
 def _raw_tensor(ptr: int, nbytes: int, device) -> torch.Tensor:
-    return torch.as_tensor(_CAI(ptr, nbytes), device=device)
+    """Zero-copy uint8 tensor over raw device memory we own (its own StorageImpl, no
+    allocator involvement and -- unlike __cuda_array_interface__ -- no stream sync)."""
+    shape = (C.c_int64 * 1)(nbytes)
+    mt = _DLManagedTensor()
+    mt.dl_tensor.data = ptr
+    mt.dl_tensor.device = _DLDevice(2, device.index or 0)  # kDLCUDA
+    mt.dl_tensor.ndim = 1
+    mt.dl_tensor.dtype = _DLDataType(1, 8, 1)  # uint8
+    mt.dl_tensor.shape = shape
+    mt.dl_tensor.strides = None
+    mt.dl_tensor.byte_offset = 0
+    mt.deleter = _dl_deleter
+    _KEEP[C.addressof(mt)] = (mt, shape)
+    cap = _PyCapsule_New(C.addressof(mt), b"dltensor", None)
+    return torch.utils.dlpack.from_dlpack(cap)
 
 
 @dataclass
