@@ -55,6 +55,10 @@ typedef enum autosp_direction {
 
 AUTOSP_API int autosp_abi_version(void);
 AUTOSP_API const char* autosp_last_error(void);
+/* Load every kernel of the library into the current context now (instead of lazily at
+ * first launch: a lazy module load can implicitly synchronise the context, which must
+ * not happen while a peer's all-to-all is spinning on this GPU).                      */
+AUTOSP_API int autosp_preload_kernels(void);
 /* number of SMs / compute capability of the current device, -1 if no device */
 AUTOSP_API int autosp_device_info(int* sm_count, int* cc_major, int* cc_minor);
 
@@ -135,6 +139,9 @@ AUTOSP_API int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autos
                     autosp_attn_tensor dq, autosp_attn_tensor dk, autosp_attn_tensor dv,
                     void* workspace, int b, int hq, int hkv, int s, int d, float scale,
                     int causal, void* stream);
+
+/* debug only: per-step timeline of the backward's first CTA into dev_buf (16 x 64 int64) */
+AUTOSP_API int autosp_debug_set_bwd_trace(long long* dev_buf);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,7 @@ EXPORTS = {
     "autosp_abi_version": (C.c_int, []),
     "autosp_last_error": (C.c_char_p, []),
     "autosp_device_info": (C.c_int, [C.POINTER(C.c_int)] * 3),
+    "autosp_preload_kernels": (C.c_int, []),
     "autosp_symm_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p), C.c_void_p]),
     "autosp_symm_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "autosp_symm_close": (C.c_int, [C.c_void_p]),
@@ -56,6 +57,7 @@ EXPORTS = {
                                         C.c_void_p]),
     "autosp_attn_fwd": (C.c_int, [AttnTensor] * 4 + [C.c_void_p] + [C.c_int] * 5 +
                         [C.c_float, C.c_int, C.c_void_p]),
+    "autosp_debug_set_bwd_trace": (C.c_int, [C.c_void_p]),
     "autosp_attn_bwd_workspace_bytes": (C.c_size_t, [C.c_int] * 4),
     "autosp_attn_bwd": (C.c_int, [AttnTensor] * 5 + [C.c_void_p] + [AttnTensor] * 3 +
                         [C.c_void_p] + [C.c_int] * 5 + [C.c_float, C.c_int, C.c_void_p]),
@@ -82,6 +84,13 @@ def load():
         if lib.autosp_abi_version() != ABI_VERSION:
             raise ExtensionMissingError("libautosp.so ABI version mismatch; rebuild")
         _lib = lib
+        try:
+            import torch
+            if torch.cuda.is_available():
+                torch.cuda.init()
+                check(lib.autosp_preload_kernels(), "preload")
+        except ImportError:
+            pass
         return lib
 
 

@@ -328,3 +328,15 @@ extern "C" int autosp_a2a_mark_ready(uint32_t* const* flags, int world, uint32_t
   }
   return AUTOSP_OK;
 }
+
+int autosp_preload_a2a() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, autosp::a2a_push_kernel<uint4>);
+  cudaFuncGetAttributes(&a, autosp::a2a_push_kernel<uint2>);
+  cudaFuncGetAttributes(&a, autosp::a2a_push_kernel<uint32_t>);
+  cudaFuncGetAttributes(&a, autosp::a2a_push_kernel<uint16_t>);
+  cudaFuncGetAttributes(&a, autosp::a2a_handshake_kernel);
+  cudaFuncGetAttributes(&a, autosp::a2a_wait_kernel);
+  cudaFuncGetAttributes(&a, autosp::a2a_mark_ready_kernel);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}

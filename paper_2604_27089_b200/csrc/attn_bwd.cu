@@ -21,6 +21,7 @@
 //   bwd_post  dq = bf16(scale * dQacc)
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "../../include/autosp.h"
@@ -32,10 +33,11 @@ int autosp_check_attn_tensor(const autosp_attn_tensor& t, const char* name);
 
 namespace autosp {
 namespace bwd {
+long long* g_bwd_trace = nullptr;  // set by autosp_debug_set_bwd_trace (tools only)
 
 constexpr int BK = 128;  // keys per CTA
 constexpr int BQ = 128;  // queries per step
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;  // WG0 TMA/MMA, WG1+WG2 softmax-grad (column halves), WG3 dQ drain
 
 AUTOSP_DEV void tma_reduce_add_3d(const CUtensorMap* map, const void* smem, int c0, int c1,
                                   int c2) {
@@ -69,18 +71,21 @@ struct Cfg {
   static constexpr int LSE_OFF = DQ_OFF + 2 * 128 * 32 * 4;    // lse[st][128], delta[st][128]
   static constexpr int BAR_OFF = LSE_OFF + 4 * 128 * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  // TMEM columns.  d <= 64: S0 | S1 | dP (dS bf16 in cols 0..63, dQ fp32 in 64..64+D) | dV | dK
-  //                d = 128: S (dQ reuses it after dV consumed P) | dP | dV | dK
+  // TMEM columns.  d <= 64: S0 | S1 | dP | dV | dK; P^T(t) (bf16) occupies the first 64
+  //   columns of S buffer t%2 and dQ(t) (fp32) the last 64, so dP(t+1) never waits for the
+  //   dQ drain (only S(t+2) does).
+  // d = 128: S | dP | dV | dK; dQ(t) lands in the dP columns after dK(t) consumed dS(t),
+  //   so S(t+1) (and the exps of t+1) overlap the dQ drain; dP(t+1) waits for it.
   static constexpr uint32_t DP_COL = NSB * 128;
   static constexpr uint32_t DV_COL = DP_COL + 128;
   static constexpr uint32_t DK_COL = DV_COL + D;
-  static constexpr uint32_t DQ_COL = NSB == 2 ? DP_COL + 64 : 0;
   static_assert(DK_COL + D <= 512, "TMEM budget");
 };
 
 struct Params {
   CUtensorMap tm_q, tm_k, tm_v, tm_do, tm_dqacc, tm_lse, tm_dlt;
   int lse_tma;         // lse/delta rows staged by TMA with Q/dO (needs S % 4 == 0)
+  long long* trace;    // debug timeline (nullptr in production): [16 events][kTraceSteps]
   const float* lse;    // [B, Hq, S]
   const float* delta;  // [B, Hq, S]
   __nv_bfloat16* dk;
@@ -91,6 +96,13 @@ struct Params {
   int causal;
   int n_ktiles;
 };
+
+constexpr int kTraceSteps = 64;
+#define BWD_TRACE(ev, t)                                                                  \
+  do {                                                                                    \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (t) < kTraceSteps) \
+      p.trace[(ev) * kTraceSteps + (t)] = clock64();                                      \
+  } while (0)
 
 template <int D>
 AUTOSP_DEV uint64_t desc_kmajor(uint32_t tile_saddr, int kk) {
@@ -121,10 +133,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   uint64_t* kv_full = bars + 0;
   uint64_t* q_full = bars + 1;                  // [kQStages]
   uint64_t* q_empty = q_full + C::kQStages;     // [kQStages]
-  uint64_t* s_full = q_empty + C::kQStages;     // [NSB] S^T(t) in TMEM
+  uint64_t* s_full = q_empty + C::kQStages;     // [2] S^T(t) in TMEM
   uint64_t* dp_full = s_full + 2;               // dP^T(t) in TMEM
-  uint64_t* p_ready = dp_full + 1;              // P^T written (128 arrivals)
-  uint64_t* ds_ready = p_ready + 1;             // dS^T written to TMEM + smem (128 arrivals)
+  uint64_t* p_ready = dp_full + 1;              // P^T written (256 arrivals)
+  uint64_t* ds_ready = p_ready + 1;             // dS^T written to TMEM + smem (256 arrivals)
   uint64_t* dq_full = ds_ready + 1;             // dQ MMA complete
   uint64_t* dq_empty = dq_full + 1;             // dQ drained from TMEM (128 arrivals)
   uint64_t* acc_full = dq_empty + 1;            // final dK/dV complete
@@ -153,8 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     mbar_init(s_full + 0, 1);
     mbar_init(s_full + 1, 1);
     mbar_init(dp_full, 1);
-    mbar_init(p_ready, 128);
-    mbar_init(ds_ready, 128);
+    mbar_init(p_ready, 256);
+    mbar_init(ds_ready, 256);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 128);
     mbar_init(acc_full, 1);
@@ -179,6 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   const uint32_t s_q = smem_u32(smem + C::Q_OFF);
   const uint32_t s_do = smem_u32(smem + C::DO_OFF);
   const uint32_t s_ds = smem_u32(smem + C::DS_OFF);
+  // where dQ(t) accumulates (see Cfg)
+  auto dq_col = [&](int t) -> uint32_t {
+    return C::NSB == 2 ? (uint32_t)((t & 1) * 128 + 64) : C::DP_COL;
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -216,51 +232,68 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, 0, 0);   // K-major x K-major
       constexpr uint32_t idesc_g = make_idesc_bf16(128, D, 0, 1);     // TMEM A x MN-major B
       constexpr uint32_t idesc_q = make_idesc_bf16(128, D, 1, 1);     // MN-major A and B
-      auto issue_s = [&](int t) {  // S^T(t) = K Q(t)^T
-        const uint32_t qa = s_q + (t % C::kQStages) * C::TILE;
+      auto wait_q = [&](int t) {
         mbar_wait(q_full + (t % C::kQStages), (t / C::kQStages) & 1);
         tc_fence_after();
+      };
+      auto issue_s = [&](int t) {  // S^T(t) = K Q(t)^T into S buffer t % NSB
+        const uint32_t qa = s_q + (t % C::kQStages) * C::TILE;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           mma_ss(tmem + (t % C::NSB) * 128, desc_kmajor<D>(s_k, kk), desc_kmajor<D>(qa, kk),
                  idesc_s, kk > 0);
         tc_commit(s_full + (t % C::NSB));
       };
-      mbar_wait(kv_full, 0);
-      if (C::NSB == 2) issue_s(0);
-      for (int t = 0; t < T; ++t) {
-        const int st = t % C::kQStages;
-        const uint32_t qa = s_q + st * C::TILE;
-        const uint32_t da = s_do + st * C::TILE;
-        const uint32_t s_col = (t % C::NSB) * 128;
-        // the dP region (and for d = 128 the S region) held dQ(t-1): wait for its drain
-        if (t > 0) {
-          mbar_wait(dq_empty, (t - 1) & 1);
-          tc_fence_after();
-        }
-        if (C::NSB == 1) issue_s(t);
-        else {
-          mbar_wait(q_full + st, (t / C::kQStages) & 1);
-          tc_fence_after();
-        }
-        // dP^T(t) = V dO(t)^T
+      auto issue_dp = [&](int t) {  // dP^T(t) = V dO(t)^T
+        const uint32_t da = s_do + (t % C::kQStages) * C::TILE;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           mma_ss(tmem + C::DP_COL, desc_kmajor<D>(s_v, kk), desc_kmajor<D>(da, kk), idesc_s,
                  kk > 0);
         tc_commit(dp_full);
-        // S^T(t+1) overlaps the softmax of tile t (its buffer held P(t-1): consumed by
-        // dV(t-1), issued earlier -> in-order)
-        if (C::NSB == 2 && t + 1 < T) issue_s(t + 1);
+      };
+      mbar_wait(kv_full, 0);
+      wait_q(0);
+      issue_s(0);
+      for (int t = 0; t < T; ++t) {
+        const int st = t % C::kQStages;
+        const uint32_t qa = s_q + st * C::TILE;
+        const uint32_t da = s_do + st * C::TILE;
+        if (C::NSB == 2) {
+          // dP region: dS(t-1) was consumed by dK(t-1), issued earlier (in-order)
+          issue_dp(t);
+          BWD_TRACE(1, t);
+          if (t + 1 < T) {
+            // S buffer (t+1)%2 holds P(t-1) (consumed by dV(t-1)) and dQ(t-1): wait drain
+            if (t >= 1) {
+              mbar_wait(dq_empty, (t - 1) & 1);
+              BWD_TRACE(0, t);
+            }
+            wait_q(t + 1);
+            issue_s(t + 1);
+          }
+        } else {
+          // dQ(t-1) lives in the dP columns: dP(t) waits for its drain
+          if (t >= 1) {
+            mbar_wait(dq_empty, (t - 1) & 1);
+            BWD_TRACE(0, t);
+            tc_fence_after();
+          }
+          issue_dp(t);
+          BWD_TRACE(1, t);
+        }
         // dV += P^T dO once the exps of tile t are done
         mbar_wait(p_ready, t & 1);
+        BWD_TRACE(2, t);
         tc_fence_after();
+        const uint32_t s_col = (t % C::NSB) * 128;
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk)
           mma_ts(tmem + C::DV_COL, tmem + s_col + kk * 8, desc_mn<D>(da, kk), idesc_g,
                  (t > 0 || kk > 0) ? 1u : 0u);
         // dK += dS^T Q and dQ(t) = dS K once dS is in TMEM + smem
         mbar_wait(ds_ready, t & 1);
+        BWD_TRACE(3, t);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk)
@@ -269,161 +302,200 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         tc_commit(q_empty + st);
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk)
-          mma_ss(tmem + C::DQ_COL, desc_ds(s_ds, kk), desc_mn<D>(s_k, kk), idesc_q, kk > 0);
+          mma_ss(tmem + dq_col(t), desc_ds(s_ds, kk), desc_mn<D>(s_k, kk), idesc_q, kk > 0);
         tc_commit(dq_full);
+        BWD_TRACE(4, t);
+        // d = 128: S(t+1) reuses the S columns (P(t) consumed by dV(t) and by the softmax)
+        if (C::NSB == 1 && t + 1 < T) {
+          wait_q(t + 1);
+          issue_s(t + 1);
+        }
       }
       tc_commit(acc_full);
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ------------------------------------------------------------ softmax-grad warpgroup
+  } else if (warp >= 4 && warp < 12) {
+    // ------------------------------------------------------------ softmax-grad warpgroups
+    // WG1 (warps 4-7) owns query columns [0, 64), WG2 (warps 8-11) [64, 128); thread =
+    // key row (TMEM lane).  Part 1: P^T = exp2(S^T c - lse log2e) -> bf16 in S columns.
+    // Part 2: dS^T = P^T (dP^T - delta) -> bf16 in dP columns + 128B-swizzled smem.
+    const int half = (warp - 4) >> 2;
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;  // key row within the tile
     const int key = k0 + row;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t dp_addr = tmem + lane_base + C::DP_COL;
-    uint8_t* ds_row = smem + C::DS_OFF + row * 128;
+    uint8_t* ds_row = smem + C::DS_OFF + half * (128 * 128) + row * 128;
     const float LOG2E = 1.4426950408889634f;
+    const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
+    const uint64_t nl2e = f2_pack(-LOG2E, -LOG2E);
+    const bool row_dead = key >= p.S;
     for (int t = 0; t < T; ++t) {
       const int head = kvh * group + t / per_head;
       const int q0 = (m_first + t % per_head) * BQ;
       const uint32_t s_addr = tmem + lane_base + (t % C::NSB) * 128;
       const int st = t % C::kQStages;
-      float* lse_b = lse_s + st * 128;
-      float* dlt_b = dlt_s + st * 128;
+      const float* lse_b = lse_s + st * 128;
+      const float* dlt_b = dlt_s + st * 128;
       if (!p.lse_tma) {  // S % 4 != 0: stage lse/delta through registers (slow path)
-        if (t >= C::kQStages) named_bar_sync(1, 128);  // everyone done with this slot
-        const int q = q0 + row;
-        const int64_t idx = ((int64_t)batch * p.Hq + head) * p.S + q;
-        lse_b[row] = q < p.S ? p.lse[idx] : 0.f;
-        dlt_b[row] = q < p.S ? p.delta[idx] : 0.f;
-        named_bar_sync(1, 128);
-      }
-      const bool diag = p.causal && (q0 < k0 + BK);
-      const bool oob = (k0 + BK > p.S) || (q0 + BQ > p.S);
-      // ---- part 1: P^T = exp2(S^T c - lse) -> bf16 into the S columns
-      mbar_wait(s_full + (t % C::NSB), (t / C::NSB) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c4 = 0; c4 < BQ / 32; ++c4) {
-        uint32_t sr[32], pk[16];
-        tmem_ld32(s_addr + c4 * 32, sr);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float pv[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = c4 * 32 + 2 * c + e;
-            float pp = fast_exp2(fmaf(__uint_as_float(sr[2 * c + e]), p.scale_log2,
-                                      -lse_b[col] * LOG2E));
-            if ((diag || oob) &&
-                ((p.causal && key > q0 + col) || key >= p.S || q0 + col >= p.S))
-              pp = 0.f;
-            pv[e] = pp;
-          }
-          pk[c] = pack_bf16(pv[0], pv[1]);
+        if (t >= C::kQStages) named_bar_sync(1, 256);  // everyone done with this slot
+        if (half == 0) {
+          const int q = q0 + row;
+          const int64_t idx = ((int64_t)batch * p.Hq + head) * p.S + q;
+          lse_s[st * 128 + row] = q < p.S ? p.lse[idx] : 0.f;
+          dlt_s[st * 128 + row] = q < p.S ? p.delta[idx] : 0.f;
         }
-        tmem_st16(s_addr + c4 * 16, pk);
+        named_bar_sync(1, 256);
       }
+      // tiles that need element masks: the diagonal (causal) and the sequence tail
+      const bool masked = (p.causal && (q0 < k0 + BK)) || (k0 + BK > p.S) || (q0 + BQ > p.S);
+      const int col_lo = p.causal ? key - q0 : -1;  // col < col_lo -> masked (q < key)
+      const int col_hi = min(p.S - q0, BQ);          // col >= col_hi -> masked (q >= S)
+      mbar_wait(s_full + (t % C::NSB), (t / C::NSB) & 1);
+      if (threadIdx.x == 128) BWD_TRACE(5, t);
+      tc_fence_after();
+      auto part1 = [&](auto kMasked) {
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c4 = half * 2 + cc;  // 32-column chunk
+          uint32_t sr[32], pk[16];
+          tmem_ld32(s_addr + c4 * 32, sr);
+          const float4* l4 = reinterpret_cast<const float4*>(lse_b + c4 * 32);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c8 = 0; c8 < 8; ++c8) {
+            const float4 l = l4[c8];  // broadcast LDS.128
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = c8 * 2 + h;
+              const uint64_t lz = h ? f2_pack(l.z, l.w) : f2_pack(l.x, l.y);
+              const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(sr[2 * c]),
+                                                 __uint_as_float(sr[2 * c + 1])),
+                                         sl2, f2_mul(lz, nl2e));
+              float x0, x1;
+              f2_unpack(x2, x0, x1);
+              float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+              if constexpr (decltype(kMasked)::value) {
+                const int col = c4 * 32 + 2 * c;
+                e0 = (row_dead || col < col_lo || col >= col_hi) ? 0.f : e0;
+                e1 = (row_dead || col + 1 < col_lo || col + 1 >= col_hi) ? 0.f : e1;
+              }
+              pk[c] = pack_bf16(e0, e1);
+            }
+          }
+          tmem_st16(s_addr + c4 * 16, pk);
+        }
+      };
+      if (masked) part1(std::true_type{});
+      else part1(std::false_type{});
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_ready);
-      // ---- part 2: dS^T = P^T (dP^T - delta) -> bf16 into the dP columns and smem
+      if (threadIdx.x == 128) BWD_TRACE(6, t);
       // (dp_full(t) also implies dQ(t-1) finished reading the smem dS tile)
       mbar_wait(dp_full, t & 1);
+      if (threadIdx.x == 128) BWD_TRACE(7, t);
       tc_fence_after();
+      auto part2 = [&](auto kMasked) {
 #pragma unroll
-      for (int c4 = 0; c4 < BQ / 32; ++c4) {
-        uint32_t dr[32], pk[16];
-        tmem_ld32(dp_addr + c4 * 32, dr);
-        tmem_ld16(s_addr + c4 * 16, pk);  // P^T (bf16) written in part 1
-        tmem_wait_ld();
-        uint32_t dk[16];
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c4 = half * 2 + cc;
+          uint32_t dr[32], pk[16], dk[16];
+          tmem_ld32(dp_addr + c4 * 32, dr);
+          tmem_ld16(s_addr + c4 * 16, pk);  // P^T (bf16) written in part 1
+          const float4* d4 = reinterpret_cast<const float4*>(dlt_b + c4 * 32);
+          tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int col = c4 * 32 + 2 * c;
-          const float2 pf = __bfloat1622float2(
-              *reinterpret_cast<const __nv_bfloat162*>(&pk[c]));
-          float d0 = dlt_b[col], d1 = dlt_b[col + 1];
-          if (oob) {  // TMA zero-fills rows past S; keep 0 * (x - garbage) out of dS
-            d0 = (q0 + col < p.S) ? d0 : 0.f;
-            d1 = (q0 + col + 1 < p.S) ? d1 : 0.f;
+          for (int c8 = 0; c8 < 8; ++c8) {
+            float4 dl = d4[c8];
+            if constexpr (decltype(kMasked)::value) {  // rows past S (slow path garbage)
+              const int col = c4 * 32 + 4 * c8;
+              dl.x = col + 0 < col_hi ? dl.x : 0.f;
+              dl.y = col + 1 < col_hi ? dl.y : 0.f;
+              dl.z = col + 2 < col_hi ? dl.z : 0.f;
+              dl.w = col + 3 < col_hi ? dl.w : 0.f;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = c8 * 2 + h;
+              const float2 pf =
+                  __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[c]));
+              const uint64_t dd = f2_add(f2_pack(__uint_as_float(dr[2 * c]),
+                                                 __uint_as_float(dr[2 * c + 1])),
+                                         h ? f2_pack(-dl.z, -dl.w) : f2_pack(-dl.x, -dl.y));
+              float a, b;
+              f2_unpack(f2_mul(f2_pack(pf.x, pf.y), dd), a, b);
+              dk[c] = pack_bf16(a, b);
+            }
           }
-          dk[c] = pack_bf16(pf.x * (__uint_as_float(dr[2 * c]) - d0),
-                            pf.y * (__uint_as_float(dr[2 * c + 1]) - d1));
-        }
-        tmem_st16(dp_addr + c4 * 16, dk);
-        uint8_t* chunk = ds_row + (c4 >> 1) * (128 * 128);
+          tmem_st16(dp_addr + c4 * 16, dk);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int unit = (c4 & 1) * 4 + u;  // 16-byte unit within the 128 B row
-          *reinterpret_cast<uint4*>(chunk + ((unit ^ (row & 7)) << 4)) =
-              make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+          for (int u = 0; u < 4; ++u) {
+            const int unit = cc * 4 + u;  // 16-byte unit within this half's 128 B row
+            *reinterpret_cast<uint4*>(ds_row + ((unit ^ (row & 7)) << 4)) =
+                make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+          }
         }
-      }
+      };
+      if (masked) part2(std::true_type{});
+      else part2(std::false_type{});
       tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(ds_ready);
+      if (threadIdx.x == 128) BWD_TRACE(8, t);
     }
-    // ---- epilogue: dV, dK (scaled) straight from TMEM
+    // ---- epilogue: dV (WG1) / dK scaled (WG2) straight from TMEM
     if (T > 0) {
       mbar_wait(acc_full, 0);
       tc_fence_after();
-      const uint32_t dv_addr = tmem + lane_base + C::DV_COL;
-      const uint32_t dk_addr = tmem + lane_base + C::DK_COL;
-      __nv_bfloat16* dvrow = p.dv + (int64_t)batch * p.dv_sb + (int64_t)kvh * p.dv_sh +
-                             (int64_t)key * p.dv_ss;
-      __nv_bfloat16* dkrow = p.dk + (int64_t)batch * p.dk_sb + (int64_t)kvh * p.dk_sh +
-                             (int64_t)key * p.dk_ss;
+      const uint32_t src = tmem + lane_base + (half ? C::DK_COL : C::DV_COL);
+      const float sc = half ? p.scale : 1.f;
+      __nv_bfloat16* dst =
+          half ? p.dk + (int64_t)batch * p.dk_sb + (int64_t)kvh * p.dk_sh + (int64_t)key * p.dk_ss
+               : p.dv + (int64_t)batch * p.dv_sb + (int64_t)kvh * p.dv_sh + (int64_t)key * p.dv_ss;
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
-        uint32_t a[32], g[32];
-        tmem_ld32(dv_addr + c, a);
-        tmem_ld32(dk_addr + c, g);
+        uint32_t a[32];
+        tmem_ld32(src + c, a);
         tmem_wait_ld();
         if (key < p.S) {
 #pragma unroll
           for (int t4 = 0; t4 < 4; ++t4) {
-            uint4 va, vg;
-            va.x = pack_bf16(__uint_as_float(a[8 * t4 + 0]), __uint_as_float(a[8 * t4 + 1]));
-            va.y = pack_bf16(__uint_as_float(a[8 * t4 + 2]), __uint_as_float(a[8 * t4 + 3]));
-            va.z = pack_bf16(__uint_as_float(a[8 * t4 + 4]), __uint_as_float(a[8 * t4 + 5]));
-            va.w = pack_bf16(__uint_as_float(a[8 * t4 + 6]), __uint_as_float(a[8 * t4 + 7]));
-            vg.x = pack_bf16(__uint_as_float(g[8 * t4 + 0]) * p.scale,
-                             __uint_as_float(g[8 * t4 + 1]) * p.scale);
-            vg.y = pack_bf16(__uint_as_float(g[8 * t4 + 2]) * p.scale,
-                             __uint_as_float(g[8 * t4 + 3]) * p.scale);
-            vg.z = pack_bf16(__uint_as_float(g[8 * t4 + 4]) * p.scale,
-                             __uint_as_float(g[8 * t4 + 5]) * p.scale);
-            vg.w = pack_bf16(__uint_as_float(g[8 * t4 + 6]) * p.scale,
-                             __uint_as_float(g[8 * t4 + 7]) * p.scale);
-            reinterpret_cast<uint4*>(dvrow + c)[t4] = va;
-            reinterpret_cast<uint4*>(dkrow + c)[t4] = vg;
+            uint4 va;
+            va.x = pack_bf16(__uint_as_float(a[8 * t4 + 0]) * sc, __uint_as_float(a[8 * t4 + 1]) * sc);
+            va.y = pack_bf16(__uint_as_float(a[8 * t4 + 2]) * sc, __uint_as_float(a[8 * t4 + 3]) * sc);
+            va.z = pack_bf16(__uint_as_float(a[8 * t4 + 4]) * sc, __uint_as_float(a[8 * t4 + 5]) * sc);
+            va.w = pack_bf16(__uint_as_float(a[8 * t4 + 6]) * sc, __uint_as_float(a[8 * t4 + 7]) * sc);
+            reinterpret_cast<uint4*>(dst + c)[t4] = va;
           }
         }
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 12) {
     // ------------------------------------------------------------ dQ drain warpgroup
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;  // query row within the step
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t dq_addr = tmem + lane_base + C::DQ_COL;
-    const bool leader = (warp == 8 && lane == 0);
+    const bool leader = (warp == 12 && lane == 0);
     for (int t = 0; t < T; ++t) {
       const int head = kvh * group + t / per_head;
       const int q0 = (m_first + t % per_head) * BQ;
+      const uint32_t dq_addr = tmem + lane_base + dq_col(t);
       mbar_wait(dq_full, t & 1);
+      if (threadIdx.x == 384) BWD_TRACE(9, t);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         float* slot = reinterpret_cast<float*>(smem + C::DQ_OFF) + (c & 1) * (128 * 32);
-        if (leader) bulk_wait_read1();  // the reduce that last used this slot has read it
-        named_bar_sync(2, 128);
         uint32_t v[32];
         tmem_ld32(dq_addr + c * 32, v);
+        if (leader) bulk_wait_read1();  // the reduce that last used this slot has read it
+        named_bar_sync(2, 128);
         tmem_wait_ld();
+        if (c == D / 32 - 1) {  // all of dQ(t) is in registers: release the TMEM columns
+          tc_fence_before();
+          mbar_arrive(dq_empty);
+        }
         uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
@@ -436,8 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           bulk_commit();
         }
       }
-      tc_fence_before();
-      mbar_arrive(dq_empty);
+      if (threadIdx.x == 384) BWD_TRACE(10, t);
     }
     if (leader) bulk_wait0();
   }
@@ -588,6 +659,7 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   }
   p.lse = lse;
   p.delta = delta;
+  p.trace = g_bwd_trace;
   p.dk = static_cast<__nv_bfloat16*>(const_cast<void*>(dk.ptr));
   p.dv = static_cast<__nv_bfloat16*>(const_cast<void*>(dv.ptr));
   p.dk_sb = dk.stride_b; p.dk_sh = dk.stride_h; p.dk_ss = dk.stride_s;
@@ -659,4 +731,20 @@ extern "C" int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autos
       autosp_set_error("attn_bwd: head_dim %d unsupported (32, 64, 128)", d);
       return AUTOSP_ERR_UNSUPPORTED;
   }
+}
+
+// Debug-only (tools/bwd_trace.py): record a per-step timeline of CTA (0,0,0).
+extern "C" AUTOSP_API int autosp_debug_set_bwd_trace(long long* dev_buf) {
+  autosp::bwd::g_bwd_trace = dev_buf;
+  return AUTOSP_OK;
+}
+
+int autosp_preload_bwd() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<32>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<64>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<128>);
+  cudaFuncGetAttributes(&a, autosp::bwd::bwd_pre_kernel);
+  cudaFuncGetAttributes(&a, autosp::bwd::bwd_post_kernel);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }

@@ -16,6 +16,7 @@
 //    O(s^2) probabilities, SURVEY §0 finding 3).
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "../../include/autosp.h"
@@ -39,6 +40,9 @@ struct Cfg {
   static constexpr int NCH = D / CE;                        // chunks per row
   static constexpr int TILE_BYTES = BM * D * 2;             // 128 x D bf16
   static constexpr int kStages = D == 128 ? 2 : (D == 64 ? 3 : 4);
+  // exps per 8 computed by the FMA-pipe polynomial instead of MUFU (MUFU is the
+  // bottleneck when the tile's MMA work is small: d = 32 / 64)
+  static constexpr int kEmuPer8 = D == 128 ? 2 : 3;
   static constexpr int LAYOUT = SW == 128 ? 2 : (SW == 64 ? 4 : 6);
   static constexpr int SBO = 8 * SW;  // 8-row swizzle atom
   // smem: Q[2] | K[kStages] | V[kStages] | barriers
@@ -237,46 +241,88 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     for (int j = 0; j < n; ++j) {
       mbar_wait(s_full + i, j & 1);
       tc_fence_after();
-      uint32_t sr[BN];
-      tmem_ld32(s_addr + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      tmem_ld32(s_addr + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
-      tmem_ld32(s_addr + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
-      tmem_wait_ld();
-      float* s = reinterpret_cast<float*>(sr);
       const int k0 = j * BN;
       const bool need_mask = (p.causal && k0 + BN - 1 > q0 + i * BM) || (k0 + BN > p.S);
-      if (need_mask) {
-        const int lim = p.causal ? min(qi + 1, p.S) : p.S;  // keys < lim are valid
-#pragma unroll
-        for (int c = 0; c < BN; ++c)
-          if (k0 + c >= lim) s[c] = -INFINITY;
-      }
-      float mx = s[0];
-#pragma unroll
-      for (int c = 1; c < BN; ++c) mx = fmaxf(mx, s[c]);
-      const float m_cand = mx * p.scale_log2;
+      const int lim = p.causal ? min(qi + 1, p.S) : p.S;  // keys < lim are valid
       float alpha = 1.f;
       bool rescale = false;
-      if (m_cand > m + 8.f) {  // lazy rescale (also taken on the first tile)
-        alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - m_cand);
-        rescale = (j > 0);
-        m = m_cand;
-      }
-      const float moff = (m == -INFINITY) ? 0.f : m;
       float rs = 0.f;
+      // Two passes over S in TMEM (row max, then exp) keep only 64 scores in registers.
+      // Two code versions: element masks only on diagonal / tail tiles; the exp loop is
+      // branch-free so independent exps interleave.
+      auto body = [&](auto kMasked) {
+        constexpr bool M = decltype(kMasked)::value;
+        float mx = -INFINITY;
 #pragma unroll
-      for (int c4 = 0; c4 < BN / 32; ++c4) {
-        uint32_t pk[16];
+        for (int h = 0; h < 2; ++h) {
+          uint32_t sr[64];
+          tmem_ld32(s_addr + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+          tmem_ld32(s_addr + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+          tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const float a = fast_exp2(fmaf(s[c4 * 32 + 2 * c], p.scale_log2, -moff));
-          const float b = fast_exp2(fmaf(s[c4 * 32 + 2 * c + 1], p.scale_log2, -moff));
-          rs += a + b;
-          pk[c] = pack_bf16(a, b);
+          for (int c = 0; c < 64; c += 2) {
+            float a = __uint_as_float(sr[c]), b = __uint_as_float(sr[c + 1]);
+            if constexpr (M) {
+              a = (k0 + h * 64 + c >= lim) ? -INFINITY : a;
+              b = (k0 + h * 64 + c + 1 >= lim) ? -INFINITY : b;
+            }
+            mx = fmax3(mx, a, b);
+          }
         }
-        tmem_st16(s_addr + c4 * 16, pk);
-      }
+        const float m_cand = mx * p.scale_log2;
+        if (m_cand > m + 8.f) {  // lazy rescale (also taken on the first tile)
+          alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - m_cand);
+          rescale = (j > 0);
+          m = m_cand;
+        }
+        const float moff = (m == -INFINITY) ? 0.f : m;
+        const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
+        const uint64_t nm2 = f2_pack(-moff, -moff);
+        uint64_t rs2a = f2_pack(0.f, 0.f), rs2b = f2_pack(0.f, 0.f);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t sr[64];
+          tmem_ld32(s_addr + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+          tmem_ld32(s_addr + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              float a = __uint_as_float(sr[q * 32 + 2 * c]);
+              float b = __uint_as_float(sr[q * 32 + 2 * c + 1]);
+              if constexpr (M) {
+                const int col = k0 + h * 64 + q * 32 + 2 * c;
+                a = (col >= lim) ? -INFINITY : a;
+                b = (col + 1 >= lim) ? -INFINITY : b;
+              }
+              const uint64_t x2 = f2_fma(f2_pack(a, b), sl2, nm2);
+              uint64_t e2;
+              if (!M && (c & 7) >= 8 - C::kEmuPer8) {
+                e2 = f2_exp2_poly(x2);  // FMA pipe
+              } else {
+                float x0, x1;
+                f2_unpack(x2, x0, x1);
+                e2 = f2_pack(fast_exp2(x0), fast_exp2(x1));  // MUFU
+              }
+              if (c & 1) rs2b = f2_add(rs2b, e2);
+              else rs2a = f2_add(rs2a, e2);
+              float ea, eb;
+              f2_unpack(e2, ea, eb);
+              pk[c] = pack_bf16(ea, eb);
+            }
+            // P chunk (h*2+q) -> cols [16*(2h+q), +16): only already-read columns
+            tmem_st16(s_addr + (h * 2 + q) * 16, pk);
+          }
+        }
+        float r0, r1, r2, r3;
+        f2_unpack(rs2a, r0, r1);
+        f2_unpack(rs2b, r2, r3);
+        rs = (r0 + r1) + (r2 + r3);
+      };
+      if (need_mask) body(std::true_type{});
+      else body(std::false_type{});
       if (__any_sync(0xffffffffu, rescale)) {
         // O holds tiles < j: wait for the PV of tile j-1 before touching it
         mbar_wait(o_done + i, (j - 1) & 1);
@@ -420,4 +466,12 @@ extern "C" int autosp_attn_fwd(autosp_attn_tensor q, autosp_attn_tensor k, autos
       autosp_set_error("attn_fwd: head_dim %d unsupported (32, 64, 128)", d);
       return AUTOSP_ERR_UNSUPPORTED;
   }
+}
+
+int autosp_preload_fwd() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, autosp::fwd::attn_fwd_kernel<32>);
+  cudaFuncGetAttributes(&a, autosp::fwd::attn_fwd_kernel<64>);
+  cudaFuncGetAttributes(&a, autosp::fwd::attn_fwd_kernel<128>);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }

@@ -85,3 +85,16 @@ extern "C" int autosp_memset_async(void* dev_ptr, int value, size_t bytes, void*
   if (e != cudaSuccess) return cuda_fail(e, "memset_async");
   return AUTOSP_OK;
 }
+
+int autosp_preload_a2a();
+int autosp_preload_fwd();
+int autosp_preload_bwd();
+
+extern "C" int autosp_preload_kernels(void) {
+  int rc = autosp_preload_a2a() | autosp_preload_fwd() | autosp_preload_bwd();
+  if (rc) {
+    autosp_set_error("preloading kernels failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return AUTOSP_ERR_CUDA;
+  }
+  return AUTOSP_OK;
+}
