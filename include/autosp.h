@@ -140,8 +140,30 @@ AUTOSP_API int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autos
                     void* workspace, int b, int hq, int hkv, int s, int d, float scale,
                     int causal, void* stream);
 
+/* ------------------------------------------------------------------ fused elementwise
+ * HBM-bound bf16 kernels for the layer around the Ulysses path (fp32 math):
+ *   swiglu: out[r, :] = silu(gu[r, :F]) * gu[r, F:2F]        (reference silu executor.py:33-34,
+ *           silu_dx :85-88);  bwd writes dgu = [dg | du]
+ *   rope:   rotate-half RoPE of x [b, s, h, d] (strided) with angles pos[t] * theta^(-2i/d);
+ *           inverse = 1 rotates by the negative angle (the backward)
+ *   ce:     per-row log-sum-exp / cross entropy over bf16 logits [rows, vocab] (leading dim
+ *           ld); ce_bwd overwrites the logits with g * (softmax - onehot(label))          */
+AUTOSP_API int autosp_swiglu_fwd(const void* gu, void* out, int64_t rows, int ffn, int64_t ld_gu,
+                                 int64_t ld_out, void* stream);
+AUTOSP_API int autosp_swiglu_bwd(const void* gu, const void* dout, void* dgu, int64_t rows,
+                                 int ffn, int64_t ld_gu, int64_t ld_dout, int64_t ld_dgu,
+                                 void* stream);
+AUTOSP_API int autosp_rope(const void* x, void* y, int b, int s, int h, int d, int64_t xsb,
+                           int64_t xss, int64_t xsh, int64_t ysb, int64_t yss, int64_t ysh,
+                           const float* pos, float theta, int inverse, void* stream);
+AUTOSP_API int autosp_ce_fwd(const void* logits, const int64_t* labels, float* lse, float* loss,
+                             int64_t rows, int64_t vocab, int64_t ld, void* stream);
+AUTOSP_API int autosp_ce_bwd(void* logits, const int64_t* labels, const float* lse, float g,
+                             int64_t rows, int64_t vocab, int64_t ld, void* stream);
+
 /* debug only: per-step timeline of the backward's first CTA into dev_buf (16 x 64 int64) */
 AUTOSP_API int autosp_debug_set_bwd_trace(long long* dev_buf);
+AUTOSP_API int autosp_debug_set_fwd_trace(long long* dev_buf);
 
 #ifdef __cplusplus
 }

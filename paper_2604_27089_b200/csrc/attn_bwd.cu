@@ -37,7 +37,14 @@ long long* g_bwd_trace = nullptr;  // set by autosp_debug_set_bwd_trace (tools o
 
 constexpr int BK = 128;  // keys per CTA
 constexpr int BQ = 128;  // queries per step
-constexpr int kThreads = 512;  // WG0 TMA/MMA, WG1+WG2 softmax-grad (column halves), WG3 dQ drain
+constexpr int kThreads = 512;
+// Warp roles (the issue arbiter favours higher warp ids: the single-thread TMA / MMA
+// producers sit on top, the dQ drain above the instruction-heavy softmax warpgroups).
+constexpr int kSoftWarp0 = 0;   // warps 0-3: query columns [0,64), 4-7: [64,128)
+constexpr int kDrainWarp0 = 8;  // warps 8-11
+constexpr int kAllocWarp = 12;
+constexpr int kTmaWarp = 14;
+constexpr int kMmaWarp = 15;
 
 AUTOSP_DEV void tma_reduce_add_3d(const CUtensorMap* map, const void* smem, int c0, int c1,
                                   int c2) {
@@ -62,6 +69,8 @@ struct Cfg {
   static constexpr int kQStages = D == 128 ? 1 : 2;
   // S^T buffers in TMEM: two (S(t+1) overlaps the softmax of t) when d <= 64
   static constexpr int NSB = D == 128 ? 1 : 2;
+  // exps per 8 done on the FMA pipe (part 1 is MUFU-bound at 16 exp/clk/SM)
+  static constexpr int kEmuPer8 = D == 128 ? 1 : 2;
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = TILE;
   static constexpr int Q_OFF = 2 * TILE;                       // Q[st]
@@ -111,6 +120,10 @@ AUTOSP_DEV uint64_t desc_kmajor(uint32_t tile_saddr, int kk) {
   return make_smem_desc(tile_saddr + (e / C::CE) * (128 * C::SW) + (e % C::CE) * 2, 16, C::SBO,
                         C::LAYOUT);
 }
+template <int D>
+__host__ __device__ constexpr uint64_t kmajor_off(int kk) {  // (byte offset of K-step kk) >> 4
+  return (uint64_t)((((kk * 16) / Cfg<D>::CE) * (128 * Cfg<D>::SW) + ((kk * 16) % Cfg<D>::CE) * 2) >> 4);
+}
 // MN-major operand stored as [128 K-rows x D] in NCH chunks: step kk covers 16 K-rows.
 template <int D>
 AUTOSP_DEV uint64_t desc_mn(uint32_t tile_saddr, int kk) {
@@ -156,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   const int per_head = n_qtiles - m_first;
   const int T = per_head * group;  // steps of this CTA
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kTmaWarp && lane == 0) {
     mbar_init(kv_full, 1);
     for (int s = 0; s < C::kQStages; ++s) {
       mbar_init(q_full + s, 1);
@@ -181,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       tma_prefetch_desc(&p.tm_dlt);
     }
   }
-  if (warp == 2) tmem_alloc<512>(tmem_holder);
+  if (warp == kAllocWarp) tmem_alloc<512>(tmem_holder);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -196,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     return C::NSB == 2 ? (uint32_t)((t & 1) * 128 + 64) : C::DP_COL;
   };
 
-  if (warp == 0) {
+  if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && T > 0) {
       const uint64_t pol_last = policy_evict_last();
@@ -226,48 +239,62 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && T > 0) {
+    // Whole warp runs the schedule (uniform control flow keeps descriptors in uniform
+    // registers); one elected lane issues each batch.  Descriptors are built per tile and
+    // advanced by compile-time offsets.
+    if (T > 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, 0, 0);   // K-major x K-major
       constexpr uint32_t idesc_g = make_idesc_bf16(128, D, 0, 1);     // TMEM A x MN-major B
       constexpr uint32_t idesc_q = make_idesc_bf16(128, D, 1, 1);     // MN-major A and B
+      const uint64_t dk_k = make_smem_desc(s_k, 16, C::SBO, C::LAYOUT);        // K, K-major
+      const uint64_t dv_k = make_smem_desc(s_v, 16, C::SBO, C::LAYOUT);        // V, K-major
+      const uint64_t dk_mn = make_smem_desc(s_k, 128 * C::SW, C::SBO, C::LAYOUT);  // K, MN
+      const uint64_t dds = make_smem_desc(s_ds, 128 * 128, 1024, 2);           // dS^T tile
       auto wait_q = [&](int t) {
         mbar_wait(q_full + (t % C::kQStages), (t / C::kQStages) & 1);
         tc_fence_after();
       };
       auto issue_s = [&](int t) {  // S^T(t) = K Q(t)^T into S buffer t % NSB
-        const uint32_t qa = s_q + (t % C::kQStages) * C::TILE;
+        const uint64_t dq = make_smem_desc(s_q + (t % C::kQStages) * C::TILE, 16, C::SBO, C::LAYOUT);
+        const uint32_t d_tm = tmem + (t % C::NSB) * 128;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tmem + (t % C::NSB) * 128, desc_kmajor<D>(s_k, kk), desc_kmajor<D>(qa, kk),
-                 idesc_s, kk > 0);
-        tc_commit(s_full + (t % C::NSB));
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_ss(d_tm, dk_k + kmajor_off<D>(kk), dq + kmajor_off<D>(kk), idesc_s, kk > 0);
+          tc_commit(s_full + (t % C::NSB));
+        }
+        __syncwarp();
       };
       auto issue_dp = [&](int t) {  // dP^T(t) = V dO(t)^T
-        const uint32_t da = s_do + (t % C::kQStages) * C::TILE;
+        const uint64_t ddo = make_smem_desc(s_do + (t % C::kQStages) * C::TILE, 16, C::SBO, C::LAYOUT);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tmem + C::DP_COL, desc_kmajor<D>(s_v, kk), desc_kmajor<D>(da, kk), idesc_s,
-                 kk > 0);
-        tc_commit(dp_full);
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_ss(tmem + C::DP_COL, dv_k + kmajor_off<D>(kk), ddo + kmajor_off<D>(kk), idesc_s,
+                   kk > 0);
+          tc_commit(dp_full);
+        }
+        __syncwarp();
       };
       mbar_wait(kv_full, 0);
       wait_q(0);
       issue_s(0);
       for (int t = 0; t < T; ++t) {
         const int st = t % C::kQStages;
-        const uint32_t qa = s_q + st * C::TILE;
-        const uint32_t da = s_do + st * C::TILE;
+        const uint64_t dq_mn = make_smem_desc(s_q + st * C::TILE, 128 * C::SW, C::SBO, C::LAYOUT);
+        const uint64_t ddo_mn = make_smem_desc(s_do + st * C::TILE, 128 * C::SW, C::SBO, C::LAYOUT);
+        const uint32_t acc0 = t > 0 ? 1u : 0u;
         if (C::NSB == 2) {
           // dP region: dS(t-1) was consumed by dK(t-1), issued earlier (in-order)
           issue_dp(t);
-          BWD_TRACE(1, t);
+          if (lane == 0) BWD_TRACE(1, t);
           if (t + 1 < T) {
             // S buffer (t+1)%2 holds P(t-1) (consumed by dV(t-1)) and dQ(t-1): wait drain
             if (t >= 1) {
               mbar_wait(dq_empty, (t - 1) & 1);
-              BWD_TRACE(0, t);
+              if (lane == 0) BWD_TRACE(0, t);
             }
             wait_q(t + 1);
             issue_s(t + 1);
@@ -276,49 +303,57 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           // dQ(t-1) lives in the dP columns: dP(t) waits for its drain
           if (t >= 1) {
             mbar_wait(dq_empty, (t - 1) & 1);
-            BWD_TRACE(0, t);
+            if (lane == 0) BWD_TRACE(0, t);
             tc_fence_after();
           }
           issue_dp(t);
-          BWD_TRACE(1, t);
+          if (lane == 0) BWD_TRACE(1, t);
         }
         // dV += P^T dO once the exps of tile t are done
         mbar_wait(p_ready, t & 1);
-        BWD_TRACE(2, t);
+        if (lane == 0) BWD_TRACE(2, t);
         tc_fence_after();
         const uint32_t s_col = (t % C::NSB) * 128;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BQ / 16; ++kk)
-          mma_ts(tmem + C::DV_COL, tmem + s_col + kk * 8, desc_mn<D>(da, kk), idesc_g,
-                 (t > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BQ / 16; ++kk)
+            mma_ts(tmem + C::DV_COL, tmem + s_col + kk * 8,
+                   ddo_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_g, kk > 0 ? 1u : acc0);
+        }
+        __syncwarp();
         // dK += dS^T Q and dQ(t) = dS K once dS is in TMEM + smem
         mbar_wait(ds_ready, t & 1);
-        BWD_TRACE(3, t);
+        if (lane == 0) BWD_TRACE(3, t);
         tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BQ / 16; ++kk)
-          mma_ts(tmem + C::DK_COL, tmem + C::DP_COL + kk * 8, desc_mn<D>(qa, kk), idesc_g,
-                 (t > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(q_empty + st);
+          for (int kk = 0; kk < BQ / 16; ++kk)
+            mma_ts(tmem + C::DK_COL, tmem + C::DP_COL + kk * 8,
+                   dq_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_g, kk > 0 ? 1u : acc0);
+          tc_commit(q_empty + st);
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk)
-          mma_ss(tmem + dq_col(t), desc_ds(s_ds, kk), desc_mn<D>(s_k, kk), idesc_q, kk > 0);
-        tc_commit(dq_full);
-        BWD_TRACE(4, t);
+          for (int kk = 0; kk < BK / 16; ++kk)
+            mma_ss(tmem + dq_col(t), dds + (uint64_t)((kk * 16 * 128) >> 4),
+                   dk_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_q, kk > 0);
+          tc_commit(dq_full);
+        }
+        __syncwarp();
+        if (lane == 0) BWD_TRACE(4, t);
         // d = 128: S(t+1) reuses the S columns (P(t) consumed by dV(t) and by the softmax)
         if (C::NSB == 1 && t + 1 < T) {
           wait_q(t + 1);
           issue_s(t + 1);
         }
       }
-      tc_commit(acc_full);
+      if (elect_one()) tc_commit(acc_full);
+      __syncwarp();
     }
-  } else if (warp >= 4 && warp < 12) {
+  } else if (warp >= kSoftWarp0 && warp < kSoftWarp0 + 8) {
     // ------------------------------------------------------------ softmax-grad warpgroups
     // WG1 (warps 4-7) owns query columns [0, 64), WG2 (warps 8-11) [64, 128); thread =
     // key row (TMEM lane).  Part 1: P^T = exp2(S^T c - lse log2e) -> bf16 in S columns.
     // Part 2: dS^T = P^T (dP^T - delta) -> bf16 in dP columns + 128B-swizzled smem.
-    const int half = (warp - 4) >> 2;
+    const int half = (warp - kSoftWarp0) >> 2;
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;  // key row within the tile
     const int key = k0 + row;
@@ -351,16 +386,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       const int col_lo = p.causal ? key - q0 : -1;  // col < col_lo -> masked (q < key)
       const int col_hi = min(p.S - q0, BQ);          // col >= col_hi -> masked (q >= S)
       mbar_wait(s_full + (t % C::NSB), (t / C::NSB) & 1);
-      if (threadIdx.x == 128) BWD_TRACE(5, t);
+      if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(5, t);
       tc_fence_after();
+      uint32_t pkeep[32];  // this thread's 64 P^T values (bf16 pairs), reused by part 2
       auto part1 = [&](auto kMasked) {
+        uint32_t sr2[2][32];  // both 32-column chunks in flight: one TMEM round trip
+        tmem_ld32(s_addr + (half * 2) * 32, sr2[0]);
+        tmem_ld32(s_addr + (half * 2 + 1) * 32, sr2[1]);
+        tmem_wait_ld();
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int c4 = half * 2 + cc;  // 32-column chunk
-          uint32_t sr[32], pk[16];
-          tmem_ld32(s_addr + c4 * 32, sr);
+          const uint32_t* sr = sr2[cc];
           const float4* l4 = reinterpret_cast<const float4*>(lse_b + c4 * 32);
-          tmem_wait_ld();
 #pragma unroll
           for (int c8 = 0; c8 < 8; ++c8) {
             const float4 l = l4[c8];  // broadcast LDS.128
@@ -371,18 +409,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
               const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(sr[2 * c]),
                                                  __uint_as_float(sr[2 * c + 1])),
                                          sl2, f2_mul(lz, nl2e));
-              float x0, x1;
-              f2_unpack(x2, x0, x1);
-              float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+              float e0, e1;
+              if (!decltype(kMasked)::value && (c & 7) >= 8 - C::kEmuPer8) {
+                f2_unpack(f2_exp2_poly(x2), e0, e1);  // FMA pipe (offloads MUFU)
+              } else {
+                float x0, x1;
+                f2_unpack(x2, x0, x1);
+                e0 = fast_exp2(x0);
+                e1 = fast_exp2(x1);
+              }
               if constexpr (decltype(kMasked)::value) {
                 const int col = c4 * 32 + 2 * c;
                 e0 = (row_dead || col < col_lo || col >= col_hi) ? 0.f : e0;
                 e1 = (row_dead || col + 1 < col_lo || col + 1 >= col_hi) ? 0.f : e1;
               }
-              pk[c] = pack_bf16(e0, e1);
+              pkeep[cc * 16 + c] = pack_bf16(e0, e1);
             }
           }
-          tmem_st16(s_addr + c4 * 16, pk);
+          tmem_st16(s_addr + c4 * 16, *reinterpret_cast<uint32_t(*)[16]>(&pkeep[cc * 16]));
         }
       };
       if (masked) part1(std::true_type{});
@@ -390,20 +434,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_ready);
-      if (threadIdx.x == 128) BWD_TRACE(6, t);
+      if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(6, t);
       // (dp_full(t) also implies dQ(t-1) finished reading the smem dS tile)
       mbar_wait(dp_full, t & 1);
-      if (threadIdx.x == 128) BWD_TRACE(7, t);
+      if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(7, t);
       tc_fence_after();
       auto part2 = [&](auto kMasked) {
+        uint32_t dr2[2][32];
+        tmem_ld32(dp_addr + (half * 2) * 32, dr2[0]);
+        tmem_ld32(dp_addr + (half * 2 + 1) * 32, dr2[1]);
+        tmem_wait_ld();
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int c4 = half * 2 + cc;
-          uint32_t dr[32], pk[16], dk[16];
-          tmem_ld32(dp_addr + c4 * 32, dr);
-          tmem_ld16(s_addr + c4 * 16, pk);  // P^T (bf16) written in part 1
+          const uint32_t* dr = dr2[cc];
+          uint32_t dk[16];
           const float4* d4 = reinterpret_cast<const float4*>(dlt_b + c4 * 32);
-          tmem_wait_ld();
 #pragma unroll
           for (int c8 = 0; c8 < 8; ++c8) {
             float4 dl = d4[c8];
@@ -417,8 +463,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int c = c8 * 2 + h;
-              const float2 pf =
-                  __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[c]));
+              const float2 pf = __bfloat1622float2(
+                  *reinterpret_cast<const __nv_bfloat162*>(&pkeep[cc * 16 + c]));
               const uint64_t dd = f2_add(f2_pack(__uint_as_float(dr[2 * c]),
                                                  __uint_as_float(dr[2 * c + 1])),
                                          h ? f2_pack(-dl.z, -dl.w) : f2_pack(-dl.x, -dl.y));
@@ -442,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(ds_ready);
-      if (threadIdx.x == 128) BWD_TRACE(8, t);
+      if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(8, t);
     }
     // ---- epilogue: dV (WG1) / dK scaled (WG2) straight from TMEM
     if (T > 0) {
@@ -471,18 +517,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         }
       }
     }
-  } else if (warp >= 12) {
+  } else if (warp >= kDrainWarp0 && warp < kDrainWarp0 + 4) {
     // ------------------------------------------------------------ dQ drain warpgroup
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;  // query row within the step
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const bool leader = (warp == 12 && lane == 0);
+    const bool leader = (warp == kDrainWarp0 && lane == 0);
     for (int t = 0; t < T; ++t) {
       const int head = kvh * group + t / per_head;
       const int q0 = (m_first + t % per_head) * BQ;
       const uint32_t dq_addr = tmem + lane_base + dq_col(t);
       mbar_wait(dq_full, t & 1);
-      if (threadIdx.x == 384) BWD_TRACE(9, t);
+      if (threadIdx.x == kDrainWarp0 * 32) BWD_TRACE(9, t);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
@@ -508,13 +554,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           bulk_commit();
         }
       }
-      if (threadIdx.x == 384) BWD_TRACE(10, t);
+      if (threadIdx.x == kDrainWarp0 * 32) BWD_TRACE(10, t);
     }
     if (leader) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc<512>(tmem);
+  if (warp == kAllocWarp) tmem_dealloc<512>(tmem);
 }
 
 // ---------------------------------------------------------------------------- pre / post

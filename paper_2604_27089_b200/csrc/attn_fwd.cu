@@ -31,7 +31,14 @@ namespace fwd {
 constexpr int BM = 128;  // query rows per tile
 constexpr int BN = 128;  // keys per tile
 constexpr int kThreads = 384;
-constexpr int kSoftmaxWarp0 = 4;
+// Warp roles.  The issue arbiter favours HIGHER warp ids, so the latency-critical
+// single-thread producers (TMA, MMA) get the top ids and are never starved by the
+// instruction-heavy softmax warpgroups (which must be whole, aligned warpgroups for
+// TMEM lane access).
+constexpr int kSoftmaxWarp0 = 0;   // warps 0-3: Q tile 0, 4-7: Q tile 1
+constexpr int kAllocWarp = 8;
+constexpr int kTmaWarp = 10;
+constexpr int kMmaWarp = 11;
 
 template <int D>
 struct Cfg {
@@ -52,8 +59,15 @@ struct Cfg {
   static constexpr int BAR_OFF = V_OFF + kStages * TILE_BYTES;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;  // + alignment slack
   static constexpr uint32_t TMEM_COLS = 512;
-  static constexpr uint32_t S_COL = 0;      // S_i at i*128
-  static constexpr uint32_t O_COL = 256;    // O_i at 256 + i*D
+  // d <= 64: separate bf16 P buffers so S_i(j+1) = Q_i K^T can be issued as soon as the
+  // softmax has READ S_i(j), overlapping the rest of the softmax and PV_i(j):
+  //   S0 | S1 | P0 | P1 (64 cols each) | O0 | O1.     d = 128: S0 | S1 | O0 | O1, P aliases S.
+  static constexpr bool SEP_P = D <= 64;
+  static constexpr uint32_t S_COL = 0;                    // S_i at i*128
+  static constexpr uint32_t P_COL = SEP_P ? 256 : 0;      // P_i at P_COL + i*(SEP_P ? 64 : 128)
+  static constexpr uint32_t P_STRIDE = SEP_P ? 64 : 128;
+  static constexpr uint32_t O_COL = SEP_P ? 384 : 256;    // O_i at O_COL + i*D
+  static_assert(O_COL + 2 * D <= TMEM_COLS, "TMEM budget");
 };
 
 struct Params {
@@ -65,7 +79,15 @@ struct Params {
   float scale_log2;
   int causal;
   int n_qblk;
+  long long* trace;  // debug timeline of the heaviest CTA (nullptr in production)
 };
+constexpr int kTraceSteps = 64;
+#define FWD_TRACE(ev, t)                                                                   \
+  do {                                                                                     \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (t) < kTraceSteps) \
+      p.trace[(ev) * kTraceSteps + (t)] = clock64();                                       \
+  } while (0)
+long long* g_fwd_trace = nullptr;
 
 // K-major operand tile [128 rows x D] stored as NCH swizzled chunks of [128 x SW bytes].
 template <int D>
@@ -74,6 +96,11 @@ AUTOSP_DEV uint64_t desc_kmajor(uint32_t tile_saddr, int kk) {
   const int e = kk * 16;  // element offset along K
   const uint32_t addr = tile_saddr + (e / C::CE) * (BM * C::SW) + (e % C::CE) * 2;
   return make_smem_desc(addr, 16, C::SBO, C::LAYOUT);
+}
+// byte offset >> 4 of K-step kk inside a K-major tile (added to the descriptor's address)
+template <int D>
+__host__ __device__ constexpr uint64_t kmajor_off(int kk) {
+  return (uint64_t)((((kk * 16) / Cfg<D>::CE) * (BM * Cfg<D>::SW) + ((kk * 16) % Cfg<D>::CE) * 2) >> 4);
 }
 // MN-major B operand V [128 keys x D] (N = D contiguous), K-step kk covers 16 keys.
 template <int D>
@@ -98,7 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   uint64_t* s_full = v_empty + C::kStages;  // [2]
   uint64_t* p_full = s_full + 2;            // [2]
   uint64_t* o_done = p_full + 2;            // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* s_free = o_done + 2;            // [2] softmax finished reading S_i (SEP_P)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_free + 2);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -117,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   }
   const int n_max = max(n_tiles[0], n_tiles[1]);
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kTmaWarp && lane == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(k_full + s, 1);
@@ -129,13 +157,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       mbar_init(s_full + i, 1);
       mbar_init(p_full + i, 128);
       mbar_init(o_done + i, 1);
+      mbar_init(s_free + i, 128);
     }
     fence_mbar_init();
     tma_prefetch_desc(&p.tm_q);
     tma_prefetch_desc(&p.tm_k);
     tma_prefetch_desc(&p.tm_v);
   }
-  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  if (warp == kAllocWarp) tmem_alloc<C::TMEM_COLS>(tmem_holder);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -144,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   const uint32_t sk = smem_u32(smem + C::K_OFF);
   const uint32_t sv = smem_u32(smem + C::V_OFF);
 
-  if (warp == 0) {
+  if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && n_max > 0) {
       const uint64_t pol_q = policy_evict_first();
@@ -169,27 +198,52 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                       v_full + st, c * C::CE, j * BN, kvhead, batch, pol_kv);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && n_max > 0) {
+    // The whole warp runs the schedule (warp-uniform control flow keeps descriptors in
+    // uniform registers); one elected lane issues each batch of tcgen05.mma + commit.
+    // Descriptors are built once per tile and advanced by compile-time byte offsets.
+    if (n_max > 0) {
       constexpr uint32_t idesc_qk = make_idesc_bf16(BM, BN, 0, 0);
       constexpr uint32_t idesc_pv = make_idesc_bf16(BM, D, 0, 1);
       auto issue_qk = [&](int i, int j) {
         const int st = j % C::kStages;
-        const uint32_t qa = sq + i * C::TILE_BYTES;
-        const uint32_t kb = sk + st * C::TILE_BYTES;
+        const uint64_t da = make_smem_desc(sq + i * C::TILE_BYTES, 16, C::SBO, C::LAYOUT);
+        const uint64_t db = make_smem_desc(sk + st * C::TILE_BYTES, 16, C::SBO, C::LAYOUT);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tmem + C::S_COL + i * BN, desc_kmajor<D>(qa, kk), desc_kmajor<D>(kb, kk),
-                 idesc_qk, kk > 0);
-        tc_commit(s_full + i);
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_ss(tmem + C::S_COL + i * BN, da + kmajor_off<D>(kk), db + kmajor_off<D>(kk),
+                   idesc_qk, kk > 0);
+          tc_commit(s_full + i);
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int i, int j) {
+        const int st = j % C::kStages;
+        const uint64_t dv = make_smem_desc(sv + st * C::TILE_BYTES, BN * C::SW, C::SBO, C::LAYOUT);
+        const uint32_t pa = tmem + C::P_COL + i * C::P_STRIDE;
+        const uint32_t oa = tmem + C::O_COL + i * D;
+        const uint32_t acc0 = j > 0 ? 1u : 0u;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            mma_ts(oa, pa + kk * 8, dv + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_pv,
+                   kk > 0 ? 1u : acc0);
+          tc_commit(o_done + i);
+        }
+        __syncwarp();
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) tc_commit(bar);
+        __syncwarp();
       };
       mbar_wait(q_full, 0);
       mbar_wait(k_full + 0, 0);
       tc_fence_after();
       for (int i = 0; i < 2; ++i)
         if (n_tiles[i] > 0) issue_qk(i, 0);
-      tc_commit(k_empty + 0);
+      commit(k_empty + 0);
       for (int j = 0; j < n_max; ++j) {
         const int st = j % C::kStages;
         const uint32_t ph = (j / C::kStages) & 1;
@@ -197,36 +251,43 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         const int st1 = (j + 1) % C::kStages;
         const uint32_t ph1 = ((j + 1) / C::kStages) & 1;
         mbar_wait(v_full + st, ph);
+        if (lane == 0) FWD_TRACE(14, j);
         bool k_next_ready = false;
+        auto need_k_next = [&]() {
+          if (!k_next_ready) {
+            mbar_wait(k_full + st1, ph1);
+            tc_fence_after();
+            k_next_ready = true;
+          }
+        };
         for (int i = 0; i < 2; ++i) {
           if (j >= n_tiles[i]) continue;
+          if (C::SEP_P && j + 1 < n_tiles[i]) {
+            // S_i(j+1) as soon as the softmax has read S_i(j)
+            mbar_wait(s_free + i, j & 1);
+            if (lane == 0 && i == 0) FWD_TRACE(12, j);
+            need_k_next();
+            issue_qk(i, j + 1);
+            if (lane == 0 && i == 0) FWD_TRACE(13, j);
+          }
           mbar_wait(p_full + i, j & 1);
+          if (lane == 0) FWD_TRACE(0 + i, j);
           tc_fence_after();
-          const uint32_t vb = sv + st * C::TILE_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk)
-            mma_ts(tmem + C::O_COL + i * D, tmem + C::S_COL + i * BN + kk * 8, desc_v<D>(vb, kk),
-                   idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
-          tc_commit(o_done + i);
-          if (j + 1 < n_tiles[i]) {
-            if (!k_next_ready) {
-              mbar_wait(k_full + st1, ph1);
-              tc_fence_after();
-              k_next_ready = true;
-            }
+          issue_pv(i, j);
+          if (lane == 0) FWD_TRACE(2 + i, j);
+          if (!C::SEP_P && j + 1 < n_tiles[i]) {  // P aliases S: QK after PV (in-order)
+            need_k_next();
             issue_qk(i, j + 1);
           }
         }
-        tc_commit(v_empty + st);
+        commit(v_empty + st);
         if (next) {
-          if (!k_next_ready) {  // K_{j+1} loaded but unused by either tile: still release it
-            mbar_wait(k_full + st1, ph1);
-          }
-          tc_commit(k_empty + st1);
+          if (!k_next_ready) mbar_wait(k_full + st1, ph1);  // unused K_{j+1}: still release
+          commit(k_empty + st1);
         }
       }
     }
-  } else if (warp >= kSoftmaxWarp0) {
+  } else if (warp >= kSoftmaxWarp0 && warp < kSoftmaxWarp0 + 8) {
     // ------------------------------------------------------------ softmax warpgroups
     const int i = (warp - kSoftmaxWarp0) / 4;  // Q tile
     const int quarter = warp & 3;              // TMEM lane quarter
@@ -234,12 +295,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     const int qi = q0 + i * BM + row;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t s_addr = tmem + lane_base + C::S_COL + i * BN;
+    const uint32_t p_addr = tmem + lane_base + C::P_COL + i * C::P_STRIDE;
     const uint32_t o_addr = tmem + lane_base + C::O_COL + i * D;
     const int n = n_tiles[i];
     float m = -INFINITY;  // running max in log2 units
     float l = 0.f;
     for (int j = 0; j < n; ++j) {
       mbar_wait(s_full + i, j & 1);
+      if (lane == 0 && (warp & 3) == 0) FWD_TRACE(4 + i, j);
       tc_fence_after();
       const int k0 = j * BN;
       const bool need_mask = (p.causal && k0 + BN - 1 > q0 + i * BM) || (k0 + BN > p.S);
@@ -250,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       // Two passes over S in TMEM (row max, then exp) keep only 64 scores in registers.
       // Two code versions: element masks only on diagonal / tail tiles; the exp loop is
       // branch-free so independent exps interleave.
-      auto body = [&](auto kMasked) {
+      auto pass1 = [&](auto kMasked) -> float {  // row max over the (masked) scores
         constexpr bool M = decltype(kMasked)::value;
         float mx = -INFINITY;
 #pragma unroll
@@ -269,13 +332,35 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             mx = fmax3(mx, a, b);
           }
         }
-        const float m_cand = mx * p.scale_log2;
-        if (m_cand > m + 8.f) {  // lazy rescale (also taken on the first tile)
-          alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - m_cand);
-          rescale = (j > 0);
-          m = m_cand;
+        return mx;
+      };
+      const float mx = need_mask ? pass1(std::true_type{}) : pass1(std::false_type{});
+      const float m_cand = mx * p.scale_log2;
+      if (m_cand > m + 8.f) {  // lazy rescale (also taken on the first tile)
+        alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - m_cand);
+        rescale = (j > 0);
+        m = m_cand;
+      }
+      // PV_i(j-1) must be complete before O is rescaled and (SEP_P) before P_i is
+      // overwritten; it was issued a whole softmax ago, so this rarely waits.
+      if (j > 0 && (C::SEP_P || __any_sync(0xffffffffu, rescale))) {
+        mbar_wait(o_done + i, (j - 1) & 1);
+        tc_fence_after();
+      }
+      if (rescale) {
+#pragma unroll 1
+        for (int c = 0; c < D; c += 32) {
+          uint32_t orr[32];
+          tmem_ld32(o_addr + c, orr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int t = 0; t < 32; ++t) orr[t] = __float_as_uint(__uint_as_float(orr[t]) * alpha);
+          tmem_st32(o_addr + c, orr);
         }
-        const float moff = (m == -INFINITY) ? 0.f : m;
+      }
+      const float moff = (m == -INFINITY) ? 0.f : m;
+      auto pass2 = [&](auto kMasked) -> float {  // P = exp2(s c - m) -> bf16, row sum
+        constexpr bool M = decltype(kMasked)::value;
         const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
         const uint64_t nm2 = f2_pack(-moff, -moff);
         uint64_t rs2a = f2_pack(0.f, 0.f), rs2b = f2_pack(0.f, 0.f);
@@ -285,6 +370,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           tmem_ld32(s_addr + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
           tmem_ld32(s_addr + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
           tmem_wait_ld();
+          if (C::SEP_P && h == 1) {  // S_i fully read: the MMA may overwrite it with S_i(j+1)
+            tc_fence_before();
+            mbar_arrive(s_free + i);
+            if (lane == 0 && warp == 0) FWD_TRACE(15, j);
+          }
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             uint32_t pk[16];
@@ -312,38 +402,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
               f2_unpack(e2, ea, eb);
               pk[c] = pack_bf16(ea, eb);
             }
-            // P chunk (h*2+q) -> cols [16*(2h+q), +16): only already-read columns
-            tmem_st16(s_addr + (h * 2 + q) * 16, pk);
+            // P chunk (h*2+q) -> cols [16*(2h+q), +16) of the P buffer (aliasing S for
+            // d = 128: only already-read columns)
+            tmem_st16(p_addr + (h * 2 + q) * 16, pk);
           }
         }
         float r0, r1, r2, r3;
         f2_unpack(rs2a, r0, r1);
         f2_unpack(rs2b, r2, r3);
-        rs = (r0 + r1) + (r2 + r3);
+        return (r0 + r1) + (r2 + r3);
       };
-      if (need_mask) body(std::true_type{});
-      else body(std::false_type{});
-      if (__any_sync(0xffffffffu, rescale)) {
-        // O holds tiles < j: wait for the PV of tile j-1 before touching it
-        mbar_wait(o_done + i, (j - 1) & 1);
-        tc_fence_after();
-        if (rescale) {
-#pragma unroll
-          for (int c = 0; c < D; c += 32) {
-            uint32_t orr[32];
-            tmem_ld32(o_addr + c, orr);
-            tmem_wait_ld();
-#pragma unroll
-            for (int t = 0; t < 32; ++t)
-              orr[t] = __float_as_uint(__uint_as_float(orr[t]) * alpha);
-            tmem_st32(o_addr + c, orr);
-          }
-        }
-      }
+      rs = need_mask ? pass2(std::true_type{}) : pass2(std::false_type{});
       l = l * alpha + rs;
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_full + i);
+      if (lane == 0 && (warp & 3) == 0) FWD_TRACE(6 + i, j);
+      if (lane == 0 && i == 0) FWD_TRACE(8 + (warp & 3), j);
     }
     // ---- epilogue: O / l -> bf16, LSE
     if (n > 0) {
@@ -381,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem);
+  if (warp == kAllocWarp) tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
 template <int D>
@@ -411,6 +486,7 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   p.scale_log2 = scale * 1.4426950408889634f;
   p.causal = causal;
   p.n_qblk = (S + 2 * BM - 1) / (2 * BM);
+  p.trace = g_fwd_trace;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -474,4 +550,9 @@ int autosp_preload_fwd() {
   cudaFuncGetAttributes(&a, autosp::fwd::attn_fwd_kernel<64>);
   cudaFuncGetAttributes(&a, autosp::fwd::attn_fwd_kernel<128>);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
+extern "C" AUTOSP_API int autosp_debug_set_fwd_trace(long long* dev_buf) {
+  autosp::fwd::g_fwd_trace = dev_buf;
+  return AUTOSP_OK;
 }

@@ -89,9 +89,11 @@ extern "C" int autosp_memset_async(void* dev_ptr, int value, size_t bytes, void*
 int autosp_preload_a2a();
 int autosp_preload_fwd();
 int autosp_preload_bwd();
+int autosp_preload_fused();
 
 extern "C" int autosp_preload_kernels(void) {
-  int rc = autosp_preload_a2a() | autosp_preload_fwd() | autosp_preload_bwd();
+  int rc = autosp_preload_a2a() | autosp_preload_fwd() | autosp_preload_bwd() |
+           autosp_preload_fused();
   if (rc) {
     autosp_set_error("preloading kernels failed: %s", cudaGetErrorString(cudaGetLastError()));
     return AUTOSP_ERR_CUDA;

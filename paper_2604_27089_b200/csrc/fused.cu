@@ -1,0 +1,307 @@
+// HBM-bound fused elementwise kernels for the non-attention block of the transformer
+// layer around the Ulysses path (recompute-friendly kernels that
+// sp_ac re-runs in backward).  All bf16 in / bf16 out with fp32 math, 16-byte vectors,
+// grid-stride loops sized to the SM count.
+//   swiglu  out = silu(g) * u over gu = [g | u]        (+ backward)
+//   rope    rotate-half RoPE of q/k heads with positions (rank offset applied by auto_sp)
+//   ce      row-wise log-sum-exp cross entropy over bf16 logits (+ in-place gradient)
+#include <cmath>
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/autosp.h"
+
+extern "C" void autosp_set_error(const char* fmt, ...);
+
+namespace autosp {
+namespace fused {
+
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 v;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return v;
+}
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+
+// ---------------------------------------------------------------- SwiGLU
+__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out,
+                                  int64_t rows, int ffn, int64_t ld_gu, int64_t ld_out) {
+  const int vpr = ffn / 8;
+  const int64_t total = rows * vpr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / vpr;
+    const int c = (int)(i - r * vpr) * 8;
+    float g[8], u[8], o[8];
+    unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + c), g);
+    unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + ffn + c), u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = g[k] * sigmoidf_(g[k]) * u[k];
+    *reinterpret_cast<uint4*>(out + r * ld_out + c) = pack8(o);
+  }
+}
+
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu,
+                                  const __nv_bfloat16* __restrict__ dout,
+                                  __nv_bfloat16* __restrict__ dgu, int64_t rows, int ffn,
+                                  int64_t ld_gu, int64_t ld_dout, int64_t ld_dgu) {
+  const int vpr = ffn / 8;
+  const int64_t total = rows * vpr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / vpr;
+    const int c = (int)(i - r * vpr) * 8;
+    float g[8], u[8], dy[8], dg[8], du[8];
+    unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + c), g);
+    unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + ffn + c), u);
+    unpack8(*reinterpret_cast<const uint4*>(dout + r * ld_dout + c), dy);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float sg = sigmoidf_(g[k]);
+      du[k] = dy[k] * g[k] * sg;
+      dg[k] = dy[k] * u[k] * sg * (1.f + g[k] * (1.f - sg));  // silu_dx (executor.py:85-88)
+    }
+    *reinterpret_cast<uint4*>(dgu + r * ld_dgu + c) = pack8(dg);
+    *reinterpret_cast<uint4*>(dgu + r * ld_dgu + ffn + c) = pack8(du);
+  }
+}
+
+// ---------------------------------------------------------------- RoPE
+// x, y: [b, s, h, d] strided (d contiguous); one thread = (token, 8 rotation pairs),
+// looping over every head so each angle's sincos is computed once per token.
+struct RopeArgs {
+  const __nv_bfloat16* x;
+  __nv_bfloat16* y;
+  int64_t xsb, xss, xsh, ysb, yss, ysh;
+  const float* pos;  // [s] positions (already rank-offset by auto_sp)
+  int b, s, h, d;
+  float log2_theta;
+  int inverse;       // 1: rotate by -angle (the backward)
+};
+
+__global__ void rope_kernel(const __grid_constant__ RopeArgs a) {
+  const int half = a.d / 2;
+  const int vpt = half / 8;  // 8-pair vectors per token
+  const int64_t total = (int64_t)a.b * a.s * vpt;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(i % vpt);
+    const int64_t bt = i / vpt;
+    const int t = (int)(bt % a.s);
+    const int bi = (int)(bt / a.s);
+    const float p = a.pos[t];
+    float cs[8], sn[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int j = v * 8 + k;
+      const float inv_freq = exp2f(-(2.f * j / a.d) * a.log2_theta);
+      sincosf(p * inv_freq, &sn[k], &cs[k]);
+      if (a.inverse) sn[k] = -sn[k];
+    }
+    for (int hh = 0; hh < a.h; ++hh) {
+      const __nv_bfloat16* xr = a.x + (int64_t)bi * a.xsb + (int64_t)t * a.xss + (int64_t)hh * a.xsh;
+      __nv_bfloat16* yr = a.y + (int64_t)bi * a.ysb + (int64_t)t * a.yss + (int64_t)hh * a.ysh;
+      float x1[8], x2[8], y1[8], y2[8];
+      unpack8(*reinterpret_cast<const uint4*>(xr + v * 8), x1);
+      unpack8(*reinterpret_cast<const uint4*>(xr + half + v * 8), x2);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        y1[k] = x1[k] * cs[k] - x2[k] * sn[k];
+        y2[k] = x2[k] * cs[k] + x1[k] * sn[k];
+      }
+      *reinterpret_cast<uint4*>(yr + v * 8) = pack8(y1);
+      *reinterpret_cast<uint4*>(yr + half + v * 8) = pack8(y2);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- cross entropy
+// one CTA per row: online max/sum over the bf16 logits row, target logit gathered.
+constexpr int kCeThreads = 512;
+
+__device__ __forceinline__ void online_merge(float& m, float& s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  if (mn == -INFINITY) return;
+  s = s * __expf(m - mn) + s2 * __expf(m2 - mn);
+  m = mn;
+}
+
+__global__ void __launch_bounds__(kCeThreads) ce_fwd_kernel(const __nv_bfloat16* __restrict__ logits,
+                                                            const int64_t* __restrict__ labels,
+                                                            float* __restrict__ lse,
+                                                            float* __restrict__ loss, int64_t vocab,
+                                                            int64_t ld) {
+  const int64_t row = blockIdx.x;
+  const __nv_bfloat16* x = logits + row * ld;
+  float m = -INFINITY, s = 0.f;
+  const int64_t nv = vocab / 8;
+  for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(x + i * 8), f);
+    float lm = f[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) lm = fmaxf(lm, f[k]);
+    float ls = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ls += __expf(f[k] - lm);
+    online_merge(m, s, lm, ls);
+  }
+  for (int64_t i = nv * 8 + threadIdx.x; i < vocab; i += blockDim.x)
+    online_merge(m, s, __bfloat162float(x[i]), 1.f);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+    online_merge(m, s, m2, s2);
+  }
+  __shared__ float sm[kCeThreads / 32], ss[kCeThreads / 32];
+  if ((threadIdx.x & 31) == 0) {
+    sm[threadIdx.x / 32] = m;
+    ss[threadIdx.x / 32] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = sm[0], Ssum = ss[0];
+    for (int w = 1; w < kCeThreads / 32; ++w) online_merge(M, Ssum, sm[w], ss[w]);
+    const float l = M + logf(Ssum);
+    lse[row] = l;
+    loss[row] = l - __bfloat162float(x[labels[row]]);
+  }
+}
+
+// in place: logits -> g * (softmax - onehot(label))
+__global__ void __launch_bounds__(kCeThreads) ce_bwd_kernel(__nv_bfloat16* __restrict__ logits,
+                                                            const int64_t* __restrict__ labels,
+                                                            const float* __restrict__ lse,
+                                                            float g, int64_t vocab, int64_t ld) {
+  const int64_t row = blockIdx.x;
+  __nv_bfloat16* x = logits + row * ld;
+  const float l = lse[row];
+  const int64_t lab = labels[row];
+  const int64_t nv = vocab / 8;
+  for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(x + i * 8), f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) f[k] = g * (__expf(f[k] - l) - (i * 8 + k == lab ? 1.f : 0.f));
+    *reinterpret_cast<uint4*>(x + i * 8) = pack8(f);
+  }
+  for (int64_t i = nv * 8 + threadIdx.x; i < vocab; i += blockDim.x)
+    x[i] = __float2bfloat16(g * (__expf(__bfloat162float(x[i]) - l) - (i == lab ? 1.f : 0.f)));
+}
+
+int grid_for(int64_t work, int threads) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int64_t blocks = (work + threads - 1) / threads;
+  const int64_t cap = (int64_t)sms * 8;
+  return (int)(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+}
+
+int launched(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    autosp_set_error("%s launch failed: %s", what, cudaGetErrorString(e));
+    return AUTOSP_ERR_CUDA;
+  }
+  return AUTOSP_OK;
+}
+
+}  // namespace fused
+}  // namespace autosp
+
+using namespace autosp::fused;
+
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+extern "C" int autosp_swiglu_fwd(const void* gu, void* out, int64_t rows, int ffn, int64_t ld_gu,
+                                 int64_t ld_out, void* stream) {
+  if (!gu || !out || rows < 0 || ffn % 8 || ld_gu % 8 || ld_out % 8 || !al16(gu) || !al16(out)) {
+    autosp_set_error("swiglu_fwd: pointers 16B aligned, ffn and leading dims multiples of 8");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (rows == 0) return AUTOSP_OK;
+  const int64_t work = rows * (ffn / 8);
+  swiglu_fwd_kernel<<<grid_for(work, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(gu), static_cast<__nv_bfloat16*>(out), rows, ffn, ld_gu,
+      ld_out);
+  return launched("swiglu_fwd");
+}
+
+extern "C" int autosp_swiglu_bwd(const void* gu, const void* dout, void* dgu, int64_t rows,
+                                 int ffn, int64_t ld_gu, int64_t ld_dout, int64_t ld_dgu,
+                                 void* stream) {
+  if (!gu || !dout || !dgu || rows < 0 || ffn % 8 || ld_gu % 8 || ld_dout % 8 || ld_dgu % 8 ||
+      !al16(gu) || !al16(dout) || !al16(dgu)) {
+    autosp_set_error("swiglu_bwd: pointers 16B aligned, ffn and leading dims multiples of 8");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (rows == 0) return AUTOSP_OK;
+  const int64_t work = rows * (ffn / 8);
+  swiglu_bwd_kernel<<<grid_for(work, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(gu), static_cast<const __nv_bfloat16*>(dout),
+      static_cast<__nv_bfloat16*>(dgu), rows, ffn, ld_gu, ld_dout, ld_dgu);
+  return launched("swiglu_bwd");
+}
+
+extern "C" int autosp_rope(const void* x, void* y, int b, int s, int h, int d, int64_t xsb,
+                           int64_t xss, int64_t xsh, int64_t ysb, int64_t yss, int64_t ysh,
+                           const float* pos, float theta, int inverse, void* stream) {
+  if (!x || !y || !pos || d % 16 || !al16(x) || !al16(y) || xsb % 8 || xss % 8 || xsh % 8 ||
+      ysb % 8 || yss % 8 || ysh % 8 || theta <= 1.f) {
+    autosp_set_error("rope: d multiple of 16, 16B-aligned views, theta > 1");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if ((int64_t)b * s * h == 0) return AUTOSP_OK;
+  RopeArgs a{static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), xsb, xss, xsh,
+             ysb, yss, ysh, pos, b, s, h, d, log2f(theta), inverse};
+  const int64_t work = (int64_t)b * s * (d / 16);
+  rope_kernel<<<grid_for(work, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return launched("rope");
+}
+
+extern "C" int autosp_ce_fwd(const void* logits, const int64_t* labels, float* lse, float* loss,
+                             int64_t rows, int64_t vocab, int64_t ld, void* stream) {
+  if (!logits || !labels || !lse || !loss || ld % 8 || !al16(logits) || vocab < 1) {
+    autosp_set_error("ce_fwd: logits 16B aligned with leading dim multiple of 8");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (rows == 0) return AUTOSP_OK;
+  ce_fwd_kernel<<<(unsigned)rows, kCeThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(logits), labels, lse, loss, vocab, ld);
+  return launched("ce_fwd");
+}
+
+extern "C" int autosp_ce_bwd(void* logits, const int64_t* labels, const float* lse, float g,
+                             int64_t rows, int64_t vocab, int64_t ld, void* stream) {
+  if (!logits || !labels || !lse || ld % 8 || !al16(logits) || vocab < 1) {
+    autosp_set_error("ce_bwd: logits 16B aligned with leading dim multiple of 8");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (rows == 0) return AUTOSP_OK;
+  ce_bwd_kernel<<<(unsigned)rows, kCeThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<__nv_bfloat16*>(logits), labels, lse, g, vocab, ld);
+  return launched("ce_bwd");
+}
+
+int autosp_preload_fused() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, swiglu_fwd_kernel);
+  cudaFuncGetAttributes(&a, swiglu_bwd_kernel);
+  cudaFuncGetAttributes(&a, rope_kernel);
+  cudaFuncGetAttributes(&a, ce_fwd_kernel);
+  cudaFuncGetAttributes(&a, ce_bwd_kernel);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}

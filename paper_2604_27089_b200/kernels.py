@@ -196,3 +196,76 @@ def a2a_loopback(direction: str, shards: list[torch.Tensor]) -> list[torch.Tenso
     for r in range(P):
         a2a_wait(fptr[r], P, r, 1)
     return outs
+
+
+# ----------------------------------------------------------------------------- fused elementwise
+def _bf16_rows(t: torch.Tensor, name: str) -> int:
+    if not t.is_cuda or t.dtype != torch.bfloat16 or t.stride(-1) != 1:
+        raise ValidationError(f"{name}: expected a CUDA bf16 tensor with contiguous last dim")
+    return t.stride(-2) if t.dim() >= 2 else t.shape[-1]
+
+
+def swiglu_fwd(gu: torch.Tensor) -> torch.Tensor:
+    """gu [..., 2F] -> silu(gu[..., :F]) * gu[..., F:]."""
+    g2 = gu.reshape(-1, gu.shape[-1])
+    F = g2.shape[1] // 2
+    out = torch.empty(g2.shape[0], F, dtype=gu.dtype, device=gu.device)
+    rc = _lib.load().autosp_swiglu_fwd(g2.data_ptr(), out.data_ptr(), g2.shape[0], F,
+                                       _bf16_rows(g2, "gu"), F, _stream())
+    _lib.check(rc, "swiglu_fwd")
+    LOG.end("swiglu", None, 1)
+    return out.view(*gu.shape[:-1], F)
+
+
+def swiglu_bwd(gu: torch.Tensor, dout: torch.Tensor) -> torch.Tensor:
+    g2 = gu.reshape(-1, gu.shape[-1])
+    d2 = dout.reshape(-1, dout.shape[-1])
+    if d2.stride(-1) != 1:
+        d2 = d2.contiguous()
+    F = g2.shape[1] // 2
+    dgu = torch.empty_like(g2)
+    rc = _lib.load().autosp_swiglu_bwd(g2.data_ptr(), d2.data_ptr(), dgu.data_ptr(), g2.shape[0],
+                                       F, _bf16_rows(g2, "gu"), _bf16_rows(d2, "dout"),
+                                       dgu.stride(0), _stream())
+    _lib.check(rc, "swiglu_bwd")
+    LOG.end("swiglu", None, 1)
+    return dgu.view(gu.shape)
+
+
+def rope(x: torch.Tensor, pos: torch.Tensor, theta: float, inverse: bool = False) -> torch.Tensor:
+    """x [b, s, h, d] (strided view, d contiguous) -> rotated contiguous [b, s, h, d]."""
+    if x.stride(-1) != 1 or x.dtype != torch.bfloat16 or not x.is_cuda:
+        raise ValidationError("rope: CUDA bf16 [b, s, h, d] view with contiguous d required")
+    b, s, h, d = x.shape
+    y = torch.empty((b, s, h, d), dtype=x.dtype, device=x.device)
+    pos = pos.to(torch.float32).contiguous()
+    rc = _lib.load().autosp_rope(x.data_ptr(), y.data_ptr(), b, s, h, d, x.stride(0), x.stride(1),
+                                 x.stride(2), y.stride(0), y.stride(1), y.stride(2),
+                                 pos.data_ptr(), float(theta), int(inverse), _stream())
+    _lib.check(rc, "rope")
+    LOG.end("rope", None, 1)
+    return y
+
+
+def ce_fwd(logits: torch.Tensor, labels: torch.Tensor):
+    """Row-wise (lse, loss) of bf16 logits [n, V] (leading dim may exceed V)."""
+    n, V = logits.shape
+    lse = torch.empty(n, dtype=torch.float32, device=logits.device)
+    loss = torch.empty(n, dtype=torch.float32, device=logits.device)
+    labels = labels.to(torch.int64).contiguous()
+    rc = _lib.load().autosp_ce_fwd(logits.data_ptr(), labels.data_ptr(), lse.data_ptr(),
+                                   loss.data_ptr(), n, V, _bf16_rows(logits, "logits"), _stream())
+    _lib.check(rc, "ce_fwd")
+    LOG.end("ce", None, 1)
+    return lse, loss
+
+
+def ce_bwd_(logits: torch.Tensor, labels: torch.Tensor, lse: torch.Tensor, g: float) -> torch.Tensor:
+    """In place: logits <- g * (softmax(logits) - onehot(labels))."""
+    n, V = logits.shape
+    labels = labels.to(torch.int64).contiguous()
+    rc = _lib.load().autosp_ce_bwd(logits.data_ptr(), labels.data_ptr(), lse.data_ptr(), float(g),
+                                   n, V, _bf16_rows(logits, "logits"), _stream())
+    _lib.check(rc, "ce_bwd")
+    LOG.end("ce", None, 1)
+    return logits

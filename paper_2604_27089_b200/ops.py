@@ -190,3 +190,64 @@ def ulysses_attention(q, k, v, group: str, is_causal=True, scale=None):
     oh = _sdpa(qh, kh, vh, is_causal, scale)
     (o,) = all_to_all([oh], HEAD_TO_SEQ_DIR, group)
     return o if dt is None else o.to(dt)
+
+
+# ----------------------------------------------------------------------------- fused layer ops
+# HBM-bound kernels for the layer around the Ulysses path (csrc/fused.cu); recomputable
+# by sp_ac (never guarded).
+@torch.library.custom_op("autosp::swiglu", mutates_args=(), device_types="cuda")
+def swiglu(gu: torch.Tensor) -> torch.Tensor:
+    return kernels.swiglu_fwd(gu)
+
+
+@swiglu.register_fake
+def _swiglu_fake(gu):
+    return gu.new_empty((*gu.shape[:-1], gu.shape[-1] // 2))
+
+
+@torch.library.custom_op("autosp::swiglu_backward", mutates_args=(), device_types="cuda")
+def swiglu_backward(gu: torch.Tensor, dout: torch.Tensor) -> torch.Tensor:
+    return kernels.swiglu_bwd(gu, dout)
+
+
+@swiglu_backward.register_fake
+def _swiglu_backward_fake(gu, dout):
+    return gu.new_empty(gu.shape)
+
+
+def _swiglu_setup(ctx, inputs, output):
+    ctx.save_for_backward(inputs[0])
+
+
+def _swiglu_bwd(ctx, dout):
+    (gu,) = ctx.saved_tensors
+    return swiglu_backward(gu, dout)
+
+
+swiglu.register_autograd(_swiglu_bwd, setup_context=_swiglu_setup)
+
+
+@torch.library.custom_op("autosp::rope", mutates_args=(), device_types="cuda")
+def rope(x: torch.Tensor, pos: torch.Tensor, theta: float, inverse: bool) -> torch.Tensor:
+    return kernels.rope(x, pos, theta, inverse)
+
+
+@rope.register_fake
+def _rope_fake(x, pos, theta, inverse):
+    return x.new_empty(x.shape)
+
+
+def _rope_setup(ctx, inputs, output):
+    x, pos, theta, inverse = inputs
+    ctx.save_for_backward(pos)
+    ctx.theta, ctx.inverse = theta, inverse
+
+
+def _rope_bwd(ctx, dy):
+    (pos,) = ctx.saved_tensors
+    if dy.stride(-1) != 1:
+        dy = dy.contiguous()
+    return rope(dy, pos, ctx.theta, not ctx.inverse), None, None, None
+
+
+rope.register_autograd(_rope_bwd, setup_context=_rope_setup)

@@ -135,11 +135,12 @@ def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
 
 
 class LlamaBlock(nn.Module):
-    def __init__(self, cfg: LlamaConfig, dtype, device):
+    def __init__(self, cfg: LlamaConfig, dtype, device, fused: bool = True):
         super().__init__()
         d, hd = cfg.d_model, cfg.head_dim
         kw = dict(dtype=dtype, device=device)
         self.cfg = cfg
+        self.fused = fused
         self.norm1 = nn.Parameter(torch.ones(d, **kw))
         self.wqkv = nn.Parameter(torch.empty((cfg.hq + 2 * cfg.hkv) * hd, d, **kw))
         self.wo = nn.Parameter(torch.empty(d, cfg.hq * hd, **kw))
@@ -147,18 +148,29 @@ class LlamaBlock(nn.Module):
         self.w13 = nn.Parameter(torch.empty(2 * cfg.d_ffn, d, **kw))
         self.w2 = nn.Parameter(torch.empty(d, cfg.d_ffn, **kw))
 
-    def forward(self, x, cos, sin):
+    def forward(self, x, cos, sin, pos):
         cfg = self.cfg
         b, s, _ = x.shape
         hd = cfg.head_dim
-        h = rmsnorm(x, self.norm1, cfg.eps)
-        qkv = (h @ self.wqkv.t()).view(b, s, cfg.hq + 2 * cfg.hkv, hd)
-        q = rope(qkv[:, :, :cfg.hq], cos, sin)
-        k = rope(qkv[:, :, cfg.hq:cfg.hq + cfg.hkv], cos, sin)
+        if self.fused:
+            from . import ops
+            h = F.rms_norm(x, (cfg.d_model,), self.norm1, cfg.eps)
+            qkv = (h @ self.wqkv.t()).view(b, s, cfg.hq + 2 * cfg.hkv, hd)
+            q = ops.rope(qkv[:, :, :cfg.hq], pos, cfg.rope_theta, False)
+            k = ops.rope(qkv[:, :, cfg.hq:cfg.hq + cfg.hkv], pos, cfg.rope_theta, False)
+        else:
+            h = rmsnorm(x, self.norm1, cfg.eps)
+            qkv = (h @ self.wqkv.t()).view(b, s, cfg.hq + 2 * cfg.hkv, hd)
+            q = rope(qkv[:, :, :cfg.hq], cos, sin)
+            k = rope(qkv[:, :, cfg.hq:cfg.hq + cfg.hkv], cos, sin)
         v = qkv[:, :, cfg.hq + cfg.hkv:]
         o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
                                            v.transpose(1, 2), is_causal=True, enable_gqa=True)
         x = x + o.transpose(1, 2).reshape(b, s, cfg.hq * hd) @ self.wo.t()
+        if self.fused:
+            from . import ops
+            h = F.rms_norm(x, (cfg.d_model,), self.norm2, cfg.eps)
+            return x + ops.swiglu(h @ self.w13.t()) @ self.w2.t()
         h = rmsnorm(x, self.norm2, cfg.eps)
         g, u = (h @ self.w13.t()).chunk(2, dim=-1)
         return x + (F.silu(g) * u) @ self.w2.t()
@@ -167,12 +179,15 @@ class LlamaBlock(nn.Module):
 class LlamaDecoder(nn.Module):
     """Compiled body: embedding -> blocks -> final norm (hidden states out)."""
 
-    def __init__(self, cfg: LlamaConfig, dtype=torch.bfloat16, device=None, init_std=0.02):
+    def __init__(self, cfg: LlamaConfig, dtype=torch.bfloat16, device=None, init_std=0.02,
+                 fused: bool = True):
         super().__init__()
         self.cfg = cfg
+        self.fused = fused
         kw = dict(dtype=dtype, device=device)
         self.embed = nn.Parameter(torch.empty(cfg.vocab, cfg.d_model, **kw))
-        self.blocks = nn.ModuleList(LlamaBlock(cfg, dtype, device) for _ in range(cfg.layers))
+        self.blocks = nn.ModuleList(LlamaBlock(cfg, dtype, device, fused)
+                                    for _ in range(cfg.layers))
         self.norm = nn.Parameter(torch.ones(cfg.d_model, **kw))
         self.lm_head = nn.Parameter(torch.empty(cfg.vocab, cfg.d_model, **kw))
         inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, cfg.head_dim, 2, dtype=torch.float32,
@@ -186,28 +201,33 @@ class LlamaDecoder(nn.Module):
     def forward(self, ids: torch.Tensor) -> torch.Tensor:
         b, s = ids.shape
         pos = positions(s, device=ids.device).float()  # auto_sp adds rank * s/P
-        fr = pos[:, None] * self.inv_freq[None, :]
-        cos, sin = fr.cos(), fr.sin()
+        cos = sin = None
+        if not self.fused:
+            fr = pos[:, None] * self.inv_freq[None, :]
+            cos, sin = fr.cos(), fr.sin()
         x = F.embedding(ids, self.embed)
         for blk in self.blocks:
-            x = blk(x, cos, sin)
+            x = blk(x, cos, sin, pos)
+        if self.fused:
+            return F.rms_norm(x, (self.cfg.d_model,), self.norm, self.cfg.eps)
         return rmsnorm(x, self.norm, self.cfg.eps)
 
 
 class ChunkedLMLoss(torch.autograd.Function):
-    """Sum of token cross-entropies without materialising [tokens, vocab] logits: the
-    logits are produced chunk by chunk in forward and recomputed in backward."""
+    """Sum of token cross-entropies without materialising [tokens, vocab] fp32 logits: bf16
+    logits are produced chunk by chunk (cuBLAS) and reduced by the fused CE kernel in
+    forward; in backward they are recomputed and turned into dlogits in place."""
 
     @staticmethod
     def forward(ctx, hidden, weight, labels, chunk):
+        from . import kernels
         n = hidden.shape[0]
         total = torch.zeros((), dtype=torch.float32, device=hidden.device)
         lses = []
         for i in range(0, n, chunk):
-            logits = (hidden[i:i + chunk] @ weight.t()).float()
-            lse = torch.logsumexp(logits, dim=-1)
-            tgt = logits.gather(1, labels[i:i + chunk, None])[:, 0]
-            total += (lse - tgt).sum()
+            logits = hidden[i:i + chunk] @ weight.t()
+            lse, loss = kernels.ce_fwd(logits, labels[i:i + chunk])
+            total += loss.sum()
             lses.append(lse)
         ctx.save_for_backward(hidden, weight, labels, torch.cat(lses))
         ctx.chunk = chunk
@@ -215,18 +235,18 @@ class ChunkedLMLoss(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, g):
+        from . import kernels
         hidden, weight, labels, lse = ctx.saved_tensors
         chunk = ctx.chunk
+        gv = float(g)
         dh = torch.empty_like(hidden)
-        dw = torch.zeros(weight.shape, dtype=torch.float32, device=weight.device)
+        dw = torch.zeros_like(weight)
         for i in range(0, hidden.shape[0], chunk):
             h = hidden[i:i + chunk]
-            p = torch.exp((h @ weight.t()).float() - lse[i:i + chunk, None])
-            p[torch.arange(h.shape[0], device=h.device), labels[i:i + chunk]] -= 1.0
-            p = (p * g).to(hidden.dtype)
-            dh[i:i + chunk] = p @ weight
-            dw += (p.t() @ h).float()
-        return dh, dw.to(weight.dtype), None, None
+            dl = kernels.ce_bwd_(h @ weight.t(), labels[i:i + chunk], lse[i:i + chunk], gv)
+            torch.matmul(dl, weight, out=dh[i:i + chunk])
+            dw.addmm_(dl.t(), h)
+        return dh, dw, None, None
 
 
 def lm_loss(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor,

@@ -1,0 +1,125 @@
+"""GPU numerics of the fused layer kernels (csrc/fused.cu) against plain PyTorch fp32
+references of the same ops, and of the fused Llama block against the unfused one."""
+
+import math
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2  # max|a - ref| / max|ref|, bf16 outputs
+
+
+def _rel(a, b):
+    a, b = a.float(), b.float()
+    return float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2604_27089_b200 import _build, _lib
+    _build.build()
+    _lib.load()
+
+
+@pytest.mark.parametrize("rows,ffn", [(1, 8), (37, 64), (512, 8192)])
+def test_swiglu_fwd_bwd(rows, ffn):
+    from paper_2604_27089_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    gu = torch.randn(rows, 2 * ffn, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    dout = torch.randn(rows, ffn, device="cuda", generator=g).bfloat16()
+    y = ops.swiglu(gu)
+    y.backward(dout)
+    ref_in = gu.detach().float().requires_grad_(True)
+    a, b = ref_in.chunk(2, dim=-1)
+    ref = F.silu(a) * b
+    ref.backward(dout.float())
+    assert _rel(y, ref) < TOL
+    assert _rel(gu.grad, ref_in.grad) < TOL
+
+
+def _rope_ref(x, pos, theta):
+    d = x.shape[-1]
+    inv = 1.0 / (theta ** (torch.arange(0, d, 2, device=x.device, dtype=torch.float64) / d))
+    fr = pos.double()[:, None] * inv[None, :]
+    c, s = fr.cos()[None, :, None, :], fr.sin()[None, :, None, :]
+    x1, x2 = x[..., : d // 2].double(), x[..., d // 2:].double()
+    return torch.cat((x1 * c - x2 * s, x2 * c + x1 * s), dim=-1)
+
+
+@pytest.mark.parametrize("b,s,h,d,off", [(1, 64, 4, 64, 0), (2, 33, 3, 128, 4096),
+                                          (1, 256, 8, 64, 131072)])
+def test_rope_fwd_bwd_with_rank_offset(b, s, h, d, off):
+    from paper_2604_27089_b200 import ops
+    theta = 500000.0
+    full = torch.randn(b, s, h + 2, d, device="cuda").bfloat16()
+    x = full[:, :, 1:h + 1].requires_grad_(False)  # strided view, like q inside qkv
+    xr = x.clone().requires_grad_(True)
+    pos = torch.arange(off, off + s, device="cuda").float()
+    y = ops.rope(xr, pos, theta, False)
+    ref = _rope_ref(x, pos, theta)
+    assert _rel(y, ref) < TOL
+    dy = torch.randn_like(y)
+    y.backward(dy)
+    # rotation is orthogonal: dx = R(-angle) dy
+    assert _rel(xr.grad, _rope_ref(dy, pos, theta) * 0 + _inv_rot(dy, pos, theta)) < TOL
+    back = ops.rope(y.detach(), pos, theta, True)
+    assert _rel(back, x) < TOL
+
+
+def _inv_rot(dy, pos, theta):
+    d = dy.shape[-1]
+    inv = 1.0 / (theta ** (torch.arange(0, d, 2, device=dy.device, dtype=torch.float64) / d))
+    fr = pos.double()[:, None] * inv[None, :]
+    c, s = fr.cos()[None, :, None, :], fr.sin()[None, :, None, :]
+    y1, y2 = dy[..., : d // 2].double(), dy[..., d // 2:].double()
+    return torch.cat((y1 * c + y2 * s, y2 * c - y1 * s), dim=-1)
+
+
+@pytest.mark.parametrize("n,V", [(3, 64), (17, 1000), (256, 128256)])
+def test_cross_entropy_fwd_bwd(n, V):
+    from paper_2604_27089_b200 import kernels
+    g = torch.Generator(device="cuda").manual_seed(V)
+    logits = (torch.randn(n, V, device="cuda", generator=g) * 3).bfloat16()
+    labels = torch.randint(0, V, (n,), device="cuda", generator=g)
+    lse, loss = kernels.ce_fwd(logits, labels)
+    ref_lse = torch.logsumexp(logits.float(), -1)
+    ref_loss = F.cross_entropy(logits.float(), labels, reduction="none")
+    assert float((lse - ref_lse).abs().max()) < 1e-3 * max(1.0, float(ref_lse.abs().max()))
+    assert float((loss - ref_loss).abs().max()) < 1e-3 * max(1.0, float(ref_loss.abs().max()))
+    lf = logits.float().requires_grad_(True)
+    F.cross_entropy(lf, labels, reduction="sum").mul(0.5).backward()
+    dl = kernels.ce_bwd_(logits.clone(), labels, lse, 0.5)
+    assert _rel(dl, lf.grad) < TOL
+
+
+def test_fused_llama_block_matches_unfused():
+    """Same weights, fused (autosp rope/swiglu/F.rms_norm) vs plain torch block, fwd+bwd."""
+    from paper_2604_27089_b200 import ops
+    from paper_2604_27089_b200.workloads import LlamaBlock, LlamaConfig
+    cfg = LlamaConfig("tiny", 256, 1, 4, 2, 512, vocab=1000)
+    torch.manual_seed(0)
+    a = LlamaBlock(cfg, torch.bfloat16, "cuda", fused=True)
+    bblk = LlamaBlock(cfg, torch.bfloat16, "cuda", fused=False)
+    with torch.no_grad():
+        for pa, pb in zip(a.parameters(), bblk.parameters()):
+            pa.copy_(torch.randn_like(pa) * 0.05 if pa.dim() == 2 else torch.ones_like(pa))
+            pb.copy_(pa)
+    s = 256
+    x = torch.randn(1, s, cfg.d_model, device="cuda").bfloat16()
+    pos = torch.arange(s, device="cuda").float()
+    inv = 1.0 / (cfg.rope_theta ** (torch.arange(0, cfg.head_dim, 2, device="cuda").float()
+                                    / cfg.head_dim))
+    fr = pos[:, None] * inv[None, :]
+    xa = x.clone().requires_grad_(True)
+    xb = x.clone().requires_grad_(True)
+    ya = a(xa, None, None, pos)
+    yb = bblk(xb, fr.cos(), fr.sin(), pos)
+    assert _rel(ya, yb) < TOL
+    dy = torch.randn_like(ya)
+    ya.backward(dy)
+    yb.backward(dy)
+    assert _rel(xa.grad, xb.grad) < 5e-2
+    for pa, pb in zip(a.parameters(), bblk.parameters()):
+        assert _rel(pa.grad, pb.grad) < 5e-2
