@@ -80,9 +80,9 @@ struct Cfg {
   static constexpr int LSE_OFF = DQ_OFF + 2 * 128 * 32 * 4;    // lse[st][128], delta[st][128]
   static constexpr int BAR_OFF = LSE_OFF + 4 * 128 * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  // TMEM columns.  d <= 64: S0 | S1 | dP | dV | dK; P^T(t) (bf16) occupies the first 64
-  //   columns of S buffer t%2 and dQ(t) (fp32) the last 64, so dP(t+1) never waits for the
-  //   dQ drain (only S(t+2) does).
+  // TMEM columns.  d <= 64: S0 | S1 | dP | dV | dK; P^T(t) (bf16) occupies columns
+  //   [0,32) and [96,128) of S buffer t%2 and dQ(t) (fp32) columns [32, 32+d), so dP(t+1)
+  //   never waits for the dQ drain (only S(t+2) does).
   // d = 128: S | dP | dV | dK; dQ(t) lands in the dP columns after dK(t) consumed dS(t),
   //   so S(t+1) (and the exps of t+1) overlap the dQ drain; dP(t+1) waits for it.
   static constexpr uint32_t DP_COL = NSB * 128;
@@ -206,8 +206,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   const uint32_t s_ds = smem_u32(smem + C::DS_OFF);
   // where dQ(t) accumulates (see Cfg)
   auto dq_col = [&](int t) -> uint32_t {
-    return C::NSB == 2 ? (uint32_t)((t & 1) * 128 + 64) : C::DP_COL;
+    return C::NSB == 2 ? (uint32_t)((t & 1) * 128 + 32) : C::DP_COL;
   };
+  // bf16 P^T / dS^T of query-column half h (64 queries = 32 packed columns) are written
+  // inside the columns that half itself read: h = 0 -> cols [0, 32), h = 1 -> [96, 128).
+  // (Writing them densely would overwrite fp32 scores the other half may still be
+  // reading.)  K-step kk (16 queries) of the TS-MMA A operand therefore lives at:
+  auto pk_col = [](int kk) -> uint32_t { return kk < 4 ? kk * 8 : 96 + (kk - 4) * 8; };
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk)
-            mma_ts(tmem + C::DV_COL, tmem + s_col + kk * 8,
+            mma_ts(tmem + C::DV_COL, tmem + s_col + pk_col(kk),
                    ddo_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_g, kk > 0 ? 1u : acc0);
         }
         __syncwarp();
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk)
-            mma_ts(tmem + C::DK_COL, tmem + C::DP_COL + kk * 8,
+            mma_ts(tmem + C::DK_COL, tmem + C::DP_COL + pk_col(kk),
                    dq_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_g, kk > 0 ? 1u : acc0);
           tc_commit(q_empty + st);
 #pragma unroll
@@ -426,7 +431,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
               pkeep[cc * 16 + c] = pack_bf16(e0, e1);
             }
           }
-          tmem_st16(s_addr + c4 * 16, *reinterpret_cast<uint32_t(*)[16]>(&pkeep[cc * 16]));
+          tmem_st16(s_addr + half * 96 + cc * 16,
+                    *reinterpret_cast<uint32_t(*)[16]>(&pkeep[cc * 16]));
         }
       };
       if (masked) part1(std::true_type{});
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
               dk[c] = pack_bf16(a, b);
             }
           }
-          tmem_st16(dp_addr + c4 * 16, dk);
+          tmem_st16(dp_addr + half * 96 + cc * 16, dk);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int unit = cc * 4 + u;  // 16-byte unit within this half's 128 B row
@@ -532,7 +538,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
-        float* slot = reinterpret_cast<float*>(smem + C::DQ_OFF) + (c & 1) * (128 * 32);
+        // alternate the two staging slots across ALL chunks (also across steps when
+        // D / 32 is odd), so wait_group.read 1 always covers the slot's previous reduce
+        const int chunk_id = t * (D / 32) + c;
+        float* slot = reinterpret_cast<float*>(smem + C::DQ_OFF) + (chunk_id & 1) * (128 * 32);
         uint32_t v[32];
         tmem_ld32(dq_addr + c * 32, v);
         if (leader) bulk_wait_read1();  // the reduce that last used this slot has read it
