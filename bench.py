@@ -189,7 +189,9 @@ def main():
     ap.add_argument("--model", default="llama3.2-1b")
     ap.add_argument("--seq", type=int, default=32768)
     ap.add_argument("--batch", type=int, default=1)
-    ap.add_argument("--ac-mode", default="seq-aware")
+    ap.add_argument("--ac-mode", default="auto",
+                    help="sp_ac policy: auto (recompute only if the step would not fit), "
+                         "seq-aware, conservative, seq-aware-all")
     ap.add_argument("--no-sp-ac", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layers", type=int, default=None, help="override (debug only; invalid bench)")
@@ -326,6 +328,7 @@ def main():
                                f"(BASELINE.json configs[1]; at N=1 the single-GPU case)",
                    "model": cfg.name, "global_batch": b, "seq_len": S,
                    "parallelism": f"sp{P}", "passes": passes, "ac_mode": args.ac_mode,
+                   "ac_applied": sp_ac.LAST_PLAN.get("mode_applied"),
                    "l2": "working set (weights 2.5 GB + activations) >> 126 MB L2; no flush"},
         "e2e": e2e,
         "gpu_launches": launches,

@@ -20,11 +20,11 @@ from .sp_ac import AcMode, make_partition_fn
 
 KNOWN_PASSES = ("auto_sp", "sp_ac")
 _PASSES: list[str] = []
-_AC_MODE = AcMode.SEQ_AWARE_NON_ATTENTION
+_AC_MODE = AcMode.AUTO
 LAST_INFO: dict = {}
 
 
-def reg_passes(passes: list[str], ac_mode: str | AcMode = AcMode.SEQ_AWARE_NON_ATTENTION) -> None:
+def reg_passes(passes: list[str], ac_mode: str | AcMode = AcMode.AUTO) -> None:
     global _AC_MODE
     unknown = [p for p in passes if p not in KNOWN_PASSES]
     if unknown:

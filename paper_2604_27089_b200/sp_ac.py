@@ -36,6 +36,15 @@ class AcMode(str, Enum):  # ac_pass.py:26-29
     CONSERVATIVE = "conservative"
     SEQ_AWARE_NON_ATTENTION = "seq-aware"
     SEQ_AWARE_ALL = "seq-aware-all"
+    # trainability planner (the paper enables SAC only when the
+    # un-checkpointed step would not fit): keep every activation the
+    # backward needs if that fits the device budget, else fall back to seq-aware.
+    AUTO = "auto"
+
+
+MEMORY_FRACTION = 0.90   # of total device memory usable by one step
+STATE_MULTIPLIER = 4     # params + grads + 2 optimizer moments, in the parameter dtype
+TRANSIENT_MARGIN = 1.25  # backward working set on top of the saved activations
 
 
 RECOMPUTE_PENALTY = 0.05  # fraction of a node's bytes charged when it is recomputed
@@ -155,12 +164,48 @@ def plan(joint_module: fx.GraphModule, num_fwd_outputs: int, mode: AcMode):
 LAST_PLAN: dict = {}
 
 
+def _tensor_bytes(nodes) -> int:
+    tot = 0
+    for n in nodes:
+        v = n.meta.get("val") if isinstance(n, fx.Node) else None
+        if isinstance(v, torch.Tensor):
+            tot += v.numel() * v.element_size()
+    return tot
+
+
+def _save_all_fits(joint_module, fw_mod, num_fwd_outputs) -> tuple[bool, dict]:
+    out = next(n for n in fw_mod.graph.nodes if n.op == "output")
+    saved = _tensor_bytes(list(out.args[0])[num_fwd_outputs:])
+    primals = [n for n in joint_module.graph.nodes
+               if n.op == "placeholder" and "primals" in str(n.target)]
+    state = STATE_MULTIPLIER * _tensor_bytes(primals)
+    total = torch.cuda.get_device_properties(0).total_memory if torch.cuda.is_available() \
+        else 0
+    budget = MEMORY_FRACTION * total - state
+    return saved * TRANSIENT_MARGIN < budget, {"save_all_bytes": saved, "budget_bytes": int(budget)}
+
+
 def make_partition_fn(mode: AcMode = AcMode.SEQ_AWARE_NON_ATTENTION):
-    from torch._functorch.partitioners import (_extract_fwd_bwd_modules,
+    from torch._functorch.partitioners import (_extract_fwd_bwd_modules, default_partition,
                                                reordering_to_mimic_autograd_engine)
 
     def partition(joint_module: fx.GraphModule, _joint_inputs, *, num_fwd_outputs, **kwargs):
-        saved_vals, saved_sym, stats = plan(joint_module, num_fwd_outputs, mode)
+        eff = mode
+        auto_stats = {}
+        if mode is AcMode.AUTO:
+            fw_mod, bw_mod = default_partition(joint_module, _joint_inputs,
+                                               num_fwd_outputs=num_fwd_outputs, **kwargs)
+            fits, auto_stats = _save_all_fits(joint_module, fw_mod, num_fwd_outputs)
+            if fits:
+                LAST_PLAN.clear()
+                LAST_PLAN.update(auto_stats, mode="auto", mode_applied="save-all",
+                                 bw_recomputes_attention=False,
+                                 fw_collectives=sum(is_autosp_collective(n) for n in fw_mod.graph.nodes),
+                                 bw_collectives=sum(is_autosp_collective(n) for n in bw_mod.graph.nodes))
+                return fw_mod, bw_mod
+            eff = AcMode.SEQ_AWARE_NON_ATTENTION
+        saved_vals, saved_sym, stats = plan(joint_module, num_fwd_outputs, eff)
+        stats.update(auto_stats, mode=mode.value, mode_applied=eff.value)
         fw_mod, bw_mod = _extract_fwd_bwd_modules(joint_module, saved_vals, saved_sym,
                                                   num_fwd_outputs=num_fwd_outputs)
         # recompute each value just before its first backward use (ref schedule.py:45-85)

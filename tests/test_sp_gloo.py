@@ -82,7 +82,7 @@ def _run(world, dims_t, seed, passes=("auto_sp", "sp_ac"), mode="seq-aware"):
     return [res[r] for r in range(world)]
 
 
-@pytest.mark.parametrize("mode", ["seq-aware", "conservative", "seq-aware-all"])
+@pytest.mark.parametrize("mode", ["seq-aware", "conservative", "seq-aware-all", "auto"])
 def test_auto_sp_sp_ac_world2_matches_oracle(mode):
     dims_t = (1, 16, 4, 4, 8, 2, 64)  # b, s, h, d, d_ffn, layers, vocab
     out = _run(2, dims_t, seed=3, mode=mode)
