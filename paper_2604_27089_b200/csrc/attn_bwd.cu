@@ -179,10 +179,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     mbar_init(s_full + 0, 1);
     mbar_init(s_full + 1, 1);
     mbar_init(dp_full, 1);
-    mbar_init(p_ready, 256);
-    mbar_init(ds_ready, 256);
+    mbar_init(p_ready, 8);     // one arrival per softmax warp
+    mbar_init(ds_ready, 8);
     mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 128);
+    mbar_init(dq_empty, 4);
     mbar_init(acc_full, 1);
     fence_mbar_init();
     tma_prefetch_desc(&p.tm_q);
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       else part1(std::false_type{});
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(p_ready);
+      mbar_arrive_warp(p_ready);
       if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(6, t);
       // (dp_full(t) also implies dQ(t-1) finished reading the smem dS tile)
       mbar_wait(dp_full, t & 1);
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(ds_ready);
+      mbar_arrive_warp(ds_ready);
       if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(8, t);
     }
     // ---- epilogue: dV (WG1) / dK scaled (WG2) straight from TMEM
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         tmem_wait_ld();
         if (c == D / 32 - 1) {  // all of dQ(t) is in registers: release the TMEM columns
           tc_fence_before();
-          mbar_arrive(dq_empty);
+          mbar_arrive_warp(dq_empty);
         }
         uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
 #pragma unroll
@@ -636,10 +636,10 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
       }
       mbar_init(s_full, 1);
       mbar_init(dp_full, 1);
-      mbar_init(p_ready, 512);
-      mbar_init(ds_ready, 512);
+      mbar_init(p_ready, 16);
+      mbar_init(ds_ready, 16);
       mbar_init(dq_full, 1);
-      mbar_init(dq_empty, 128);
+      mbar_init(dq_empty, 4);
       mbar_init(acc_full, 1);
       fence_mbar_init();
       tma_prefetch_desc(&p.tm_q);
@@ -860,7 +860,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
       tmem_st16(s_addr + 32 * g, pk);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(p_ready);
+      mbar_arrive_warp(p_ready);
       if (threadIdx.x == 0) BWD_TRACE(6, t);
       mbar_wait(dp_full, t & 1);  // also: dQ(t-1) finished reading the smem dS tile
       if (threadIdx.x == 0) BWD_TRACE(7, t);
@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
       tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(ds_ready);
+      mbar_arrive_warp(ds_ready);
       if (threadIdx.x == 0) BWD_TRACE(8, t);
     }
     // ---- epilogue: group 0 writes dV, group 1 writes dK (scaled)
@@ -955,7 +955,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
         tmem_wait_ld();
         if (c == D / 32 - 1) {
           tc_fence_before();
-          mbar_arrive(dq_empty);
+          mbar_arrive_warp(dq_empty);
         }
         uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
 #pragma unroll

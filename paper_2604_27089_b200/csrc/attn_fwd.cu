@@ -155,9 +155,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + i, 1);
-      mbar_init(p_full + i, 128);
+      mbar_init(p_full + i, 4);   // one arrival per softmax warp
       mbar_init(o_done + i, 1);
-      mbar_init(s_free + i, 128);
+      mbar_init(s_free + i, 4);
     }
     fence_mbar_init();
     tma_prefetch_desc(&p.tm_q);
@@ -315,7 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       // branch-free so independent exps interleave.
       auto pass1 = [&](auto kMasked) -> float {  // row max over the (masked) scores
         constexpr bool M = decltype(kMasked)::value;
-        float mx = -INFINITY;
+        // 8 independent FMNMX3 chains (a single running max is a 64-deep dependency chain)
+        float mx8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t sr[64];
@@ -329,10 +332,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
               a = (k0 + h * 64 + c >= lim) ? -INFINITY : a;
               b = (k0 + h * 64 + c + 1 >= lim) ? -INFINITY : b;
             }
-            mx = fmax3(mx, a, b);
+            mx8[(c >> 1) & 7] = fmax3(mx8[(c >> 1) & 7], a, b);
           }
         }
-        return mx;
+        return fmaxf(fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), mx8[6]),
+                     mx8[7]);
       };
       const float mx = need_mask ? pass1(std::true_type{}) : pass1(std::false_type{});
       const float m_cand = mx * p.scale_log2;
@@ -363,7 +367,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         constexpr bool M = decltype(kMasked)::value;
         const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
         const uint64_t nm2 = f2_pack(-moff, -moff);
-        uint64_t rs2a = f2_pack(0.f, 0.f), rs2b = f2_pack(0.f, 0.f);
+        uint64_t rs2[4] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f),
+                           f2_pack(0.f, 0.f)};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t sr[64];
@@ -372,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           tmem_wait_ld();
           if (C::SEP_P && h == 1) {  // S_i fully read: the MMA may overwrite it with S_i(j+1)
             tc_fence_before();
-            mbar_arrive(s_free + i);
+            mbar_arrive_warp(s_free + i);
             if (lane == 0 && warp == 0) FWD_TRACE(15, j);
           }
 #pragma unroll
@@ -396,8 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
                 f2_unpack(x2, x0, x1);
                 e2 = f2_pack(fast_exp2(x0), fast_exp2(x1));  // MUFU
               }
-              if (c & 1) rs2b = f2_add(rs2b, e2);
-              else rs2a = f2_add(rs2a, e2);
+              rs2[c & 3] = f2_add(rs2[c & 3], e2);
               float ea, eb;
               f2_unpack(e2, ea, eb);
               pk[c] = pack_bf16(ea, eb);
@@ -408,15 +412,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           }
         }
         float r0, r1, r2, r3;
-        f2_unpack(rs2a, r0, r1);
-        f2_unpack(rs2b, r2, r3);
-        return (r0 + r1) + (r2 + r3);
+        f2_unpack(f2_add(f2_add(rs2[0], rs2[1]), f2_add(rs2[2], rs2[3])), r0, r1);
+        (void)r2; (void)r3;
+        return r0 + r1;
       };
       rs = need_mask ? pass2(std::true_type{}) : pass2(std::false_type{});
       l = l * alpha + rs;
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(p_full + i);
+      mbar_arrive_warp(p_full + i);
       if (lane == 0 && (warp & 3) == 0) FWD_TRACE(6 + i, j);
       if (lane == 0 && i == 0) FWD_TRACE(8 + (warp & 3), j);
     }

@@ -53,6 +53,13 @@ AUTOSP_DEV void fence_mbar_init() {
 AUTOSP_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// One arrival per WARP (barrier count = number of warps): every lane has already done
+// its own fences; __syncwarp orders them before lane 0's arrive.  32x fewer arrivals
+// also means 32x fewer wake-ups of the (high-priority) warps sleeping on the barrier.
+AUTOSP_DEV void mbar_arrive_warp(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
 AUTOSP_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
