@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           const float4* l4 = reinterpret_cast<const float4*>(lse_b + c4 * 32);
 #pragma unroll
           for (int c8 = 0; c8 < 8; ++c8) {
-            const float4 l = l4[c8];  // broadcast LDS.128
+            const float4 l = lds128(l4 + c8);  // broadcast LDS.128
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int c = c8 * 2 + h;
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           const float4* d4 = reinterpret_cast<const float4*>(dlt_b + c4 * 32);
 #pragma unroll
           for (int c8 = 0; c8 < 8; ++c8) {
-            float4 dl = d4[c8];
+            float4 dl = lds128(d4 + c8);
             if constexpr (decltype(kMasked)::value) {  // rows past S (slow path garbage)
               const int col = c4 * 32 + 4 * c8;
               dl.x = col + 0 < col_hi ? dl.x : 0.f;
@@ -470,14 +470,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int c = c8 * 2 + h;
-              const float2 pf = __bfloat1622float2(
-                  *reinterpret_cast<const __nv_bfloat162*>(&pkeep[cc * 16 + c]));
+              // (dP - delta) in fp32, rounded once to bf16x2, times P (already bf16x2):
+              // FADD2 + F2FP + HMUL2 per pair, no unpacking of P
               const uint64_t dd = f2_add(f2_pack(__uint_as_float(dr[2 * c]),
                                                  __uint_as_float(dr[2 * c + 1])),
                                          h ? f2_pack(-dl.z, -dl.w) : f2_pack(-dl.x, -dl.y));
               float a, b;
-              f2_unpack(f2_mul(f2_pack(pf.x, pf.y), dd), a, b);
-              dk[c] = pack_bf16(a, b);
+              f2_unpack(dd, a, b);
+              dk[c] = bf16x2_mul(pkeep[cc * 16 + c], pack_bf16(a, b));
             }
           }
           tmem_st16(dp_addr + half * 96 + cc * 16, dk);
@@ -828,7 +828,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
         auto body = [&](auto kMasked) {
 #pragma unroll
           for (int c8 = 0; c8 < 8; ++c8) {
-            const float4 l = reinterpret_cast<const float4*>(lse_b)[c8];
+            const float4 l = lds128(reinterpret_cast<const float4*>(lse_b) + c8);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int c = c8 * 2 + h;
@@ -869,9 +869,10 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
         uint32_t dr[32], dk[16];
         tmem_ld32(dp_addr + 32 * g, dr);
         tmem_wait_ld();
+        if (threadIdx.x == 0) BWD_TRACE(11, t);
 #pragma unroll
         for (int c8 = 0; c8 < 8; ++c8) {
-          float4 dl = reinterpret_cast<const float4*>(dlt_b)[c8];
+          float4 dl = lds128(reinterpret_cast<const float4*>(dlt_b) + c8);
           if (masked) {
             const int col = 4 * c8;
             dl.x = col + 0 < col_hi ? dl.x : 0.f;
@@ -882,15 +883,15 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int c = c8 * 2 + h;
-            const float2 pf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[c]));
             const uint64_t dd = f2_add(f2_pack(__uint_as_float(dr[2 * c]), __uint_as_float(dr[2 * c + 1])),
                                        h ? f2_pack(-dl.z, -dl.w) : f2_pack(-dl.x, -dl.y));
             float a, b;
-            f2_unpack(f2_mul(f2_pack(pf.x, pf.y), dd), a, b);
-            dk[c] = pack_bf16(a, b);
+            f2_unpack(dd, a, b);
+            dk[c] = bf16x2_mul(pk[c], pack_bf16(a, b));
           }
         }
         tmem_st16(dp_addr + 32 * g, dk);
+        if (threadIdx.x == 0) BWD_TRACE(12, t);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int unit = (g & 1) * 4 + u;
@@ -898,8 +899,11 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
               make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
         }
       }
+      if (threadIdx.x == 0) BWD_TRACE(13, t);
       tmem_wait_st();
+      if (threadIdx.x == 0) BWD_TRACE(14, t);
       fence_proxy_async_smem();
+      if (threadIdx.x == 0) BWD_TRACE(15, t);
       tc_fence_before();
       mbar_arrive_warp(ds_ready);
       if (threadIdx.x == 0) BWD_TRACE(8, t);

@@ -43,6 +43,16 @@ AUTOSP_DEV void reg_dealloc() {  // whole warpgroup
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
 }
 
+// explicit shared-memory vector load (a generic-pointer load of smem data compiles to a
+// generic LD with extra address-space resolution latency)
+AUTOSP_DEV float4 lds128(const void* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+
 // ------------------------------------------------------------------ mbarrier
 AUTOSP_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -306,6 +316,12 @@ AUTOSP_DEV uint64_t f2_exp2_poly(uint64_t x2) {
   const uint32_t r0 = __float_as_uint(p0) + (__float_as_uint(t0) << 23);
   const uint32_t r1 = __float_as_uint(p1) + (__float_as_uint(t1) << 23);
   return f2_pack(__uint_as_float(r0), __uint_as_float(r1));
+}
+
+AUTOSP_DEV uint32_t bf16x2_mul(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmul2(*reinterpret_cast<__nv_bfloat162*>(&a),
+                             *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
 }
 
 // ------------------------------------------------------------------ system-scope flags
