@@ -311,7 +311,7 @@ def main():
     traffic = None
     try:
         prof = json.loads((ROOT / "profiles" / "roofline_traffic.json").read_text())
-        traffic = prof.get(f"{cfg.name}_s{sl * P}_p{P}_attn_bwd_dram_bytes_per_launch")
+        traffic = prof.get(f"{cfg.name}_s{S}_p{P}_attn_bwd_dram_bytes_per_launch")
     except Exception:
         pass
     step_ms = t_ms / args.steps

@@ -31,7 +31,18 @@ from . import _lib
 from .errors import ValidationError
 
 FLAG_BYTES = 4096  # flag block (256 B used) padded to keep the receive region aligned
-DEFAULT_POOL_BYTES = int(os.environ.get("AUTOSP_POOL_BYTES", str(8 << 30)))
+POOL_FRACTION = 0.12  # of device memory reserved per rank for a2a receive slots
+
+
+def default_pool_bytes(device) -> int:
+    """The a2a outputs that sp_ac keeps (q/k/v head shards + o seq shard per layer) live in
+    the pool until their backward, so size it with the device (override:
+    AUTOSP_POOL_BYTES or dist.init(pool_bytes=...))."""
+    env = os.environ.get("AUTOSP_POOL_BYTES")
+    if env:
+        return int(env)
+    total = torch.cuda.get_device_properties(device).total_memory
+    return int(total * POOL_FRACTION) // (1 << 20) * (1 << 20)
 
 
 class _DLDevice(C.Structure):
@@ -71,7 +82,8 @@ def _raw_tensor(ptr: int, nbytes: int, device) -> torch.Tensor:
     shape = (C.c_int64 * 1)(nbytes)
     mt = _DLManagedTensor()
     mt.dl_tensor.data = ptr
-    mt.dl_tensor.device = _DLDevice(2, device.index or 0)  # kDLCUDA
+    cuda = torch.device(device).type == "cuda"
+    mt.dl_tensor.device = _DLDevice(2 if cuda else 1, (torch.device(device).index or 0) if cuda else 0)
     mt.dl_tensor.ndim = 1
     mt.dl_tensor.dtype = _DLDataType(1, 8, 1)  # uint8
     mt.dl_tensor.shape = shape
@@ -152,7 +164,9 @@ class SymmetricPool:
         base = _raw_tensor(self.region_ptrs[self.rank] + off, nbytes, self.device)
         self.slots.append(_Slot(off, nbytes, base))
         self.high_water = max(self.high_water, off + need)
-        return off, base
+        # hand out a VIEW: the caller's reference then holds the slot's storage (the
+        # pool's own `base` alone does not count as busy)
+        return off, base.view(-1)
 
     def next_epoch(self) -> int:
         self.epoch += 1
@@ -218,8 +232,8 @@ def init(sp_group_size: int, pool_bytes: int | None = None, backend: str | None 
             if rank in ranks:
                 st.dp_group = pg
     if sp_group_size > 1 and device.type == "cuda":
-        st.pool = SymmetricPool(pool_bytes or DEFAULT_POOL_BYTES, sp_group_size, st.rank, device,
-                                group=st.group)
+        st.pool = SymmetricPool(pool_bytes or default_pool_bytes(device), sp_group_size, st.rank,
+                                device, group=st.group)
     _STATE = st
     _REGISTRY[st.name] = st
     return st
