@@ -351,7 +351,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         mbar_wait(o_done + i, (j - 1) & 1);
         tc_fence_after();
       }
-      if (rescale) {
+      // tcgen05.ld/st are .sync.aligned: the whole warp must execute them, so the rescale
+      // is warp-uniform (alpha == 1 for the lanes whose max did not move)
+      if (__any_sync(0xffffffffu, rescale)) {
+        if (!rescale) alpha = 1.f;
 #pragma unroll 1
         for (int c = 0; c < D; c += 32) {
           uint32_t orr[32];

@@ -3,6 +3,7 @@
 // kernels read as algorithms.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -93,6 +94,8 @@ AUTOSP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint64_t t0 = globaltimer();
   while (!mbar_try_wait(bar, parity)) {
     if (globaltimer() - t0 > 4000000000ull) {
+      printf("autosp: mbarrier wait timed out (block %d,%d,%d thread %d, smem bar 0x%x, parity %u)\n",
+             blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, smem_u32(bar), parity);
       asm volatile("trap;");
     }
   }

@@ -188,3 +188,30 @@ def test_attn_bwd_matches_oracle(b, hq, hkv, s, d, causal):
         got = got.float().cpu().permute(0, 2, 1, 3).numpy()
         err = orc.norm_rel_err(got, ref)
         assert err < GRAD_TOL, (name, err)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_attn_fwd_bwd_running_max_jumps(d):
+    """Scores that grow along the sequence force the lazy O rescale on some rows of a warp
+    but not others (a divergent-lane path: tcgen05.ld/st must stay warp-uniform)."""
+    b, h, s = 1, 2, 1024
+    g = torch.Generator().manual_seed(d)
+    base = torch.randn(b, s, h, d, generator=g)
+    ramp = torch.linspace(0.0, 6.0, s).view(1, s, 1, 1) * torch.rand(1, 1, h, 1, generator=g)
+    q = base * (1.0 + ramp)
+    k = torch.randn(b, s, h, d, generator=g) * (1.0 + ramp.flip(1))
+    k[:, s // 2:] *= 4.0  # a late jump of the running max for some rows only
+    v = torch.randn(b, s, h, d, generator=g)
+    do = torch.randn(b, s, h, d, generator=g)
+    qb, kb, vb, dob = (x.bfloat16().double().numpy() for x in (q, k, v, do))
+    o_ref, lse_ref = orc.attention_fwd(qb, kb, vb)
+    K = _k()
+    qd, kd, vd, dod = (_to_dev(x, "bhsd") for x in (q, k, v, do))
+    o, lse = K.attn_fwd(qd, kd, vd)
+    torch.cuda.synchronize()
+    assert orc.norm_rel_err(o.float().cpu().permute(0, 2, 1, 3).numpy(), o_ref) < O_TOL
+    assert float(np.max(np.abs(lse.cpu().numpy() - lse_ref))) < LSE_TOL
+    dq, dk, dv = K.attn_bwd(qd, kd, vd, o, dod, lse)
+    torch.cuda.synchronize()
+    for got, ref in zip((dq, dk, dv), orc.attention_bwd(qb, kb, vb, dob)):
+        assert orc.norm_rel_err(got.float().cpu().permute(0, 2, 1, 3).numpy(), ref) < GRAD_TOL

@@ -52,9 +52,10 @@ print(json.dumps({{"ok": True, "step_s": time.perf_counter() - t0,
     if r.returncode == 0 and lines:
         out.update(json.loads(lines[-1]))
     else:
-        err = (r.stderr or "")[-400:]
+        err = (r.stderr or "").strip()
+        tail = [l for l in err.splitlines() if l.strip()]
         out.update(ok=False, oom="out of memory" in err.lower() or "OutOfMemory" in err,
-                   error=err.splitlines()[-1] if err else f"rc={r.returncode}")
+                   error=(tail[-1][-300:] if tail else f"rc={r.returncode}"))
     print(json.dumps(out), flush=True)
     return out
 
