@@ -81,9 +81,24 @@ def _nbytes(n: fx.Node) -> int | None:
     return None  # tuples / lists: cannot be saved as a unit
 
 
+_NORMS = {"aten::_fused_rms_norm", "aten::rms_norm", "aten::native_layer_norm"}
+
+
+def is_residual_boundary(n: fx.Node) -> bool:
+    """Values entering a normalisation = the residual stream at a layer boundary.  Guarding
+    them gives per-layer checkpoints: everything between two boundaries (norms,
+    projections, RoPE, MLP) is recomputable, attention and the a2a outputs are saved, and
+    the min-cut never "recomputes" a residual value through the whole network (which costs
+    0 bytes in a pure byte min-cut but O(L^2) time)."""
+    return any(u.op == "call_function" and _opname(u) in _NORMS and u.args and u.args[0] is n
+               for u in n.users)
+
+
 def guarded(n: fx.Node, mode: AcMode) -> bool:
     """Forward nodes that must not be recomputed (ac_pass.py:103-114 + the AutoSP guard)."""
     if is_autosp_collective(n) or is_autosp_attention(n):
+        return True
+    if is_residual_boundary(n):
         return True
     if n.op == "call_function" and n.target is operator.getitem:
         src = n.args[0]

@@ -41,12 +41,16 @@ for it in range(2):
     loss = lm_loss(cm(ids[:, :-1]), m.lm_head, ids[:, 1:])
     loss.backward(); opt.step(); opt.zero_grad(set_to_none=True)
     torch.cuda.synchronize()
+from paper_2604_27089_b200 import sp_ac
+pl = sp_ac.LAST_PLAN
 print(json.dumps({{"ok": True, "step_s": time.perf_counter() - t0,
-                  "peak_gb": torch.cuda.max_memory_allocated() / 1e9, "loss": float(loss)}}))
+                  "peak_gb": torch.cuda.max_memory_allocated() / 1e9, "loss": float(loss),
+                  "ac_applied": pl.get("mode_applied"), "saved_gb": pl.get("cut_bytes", pl.get("save_all_bytes", 0)) / 1e9}}))
 """
     t0 = time.time()
+    env = dict(os.environ, PYTORCH_CUDA_ALLOC_CONF="expandable_segments:True")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
-                       timeout=3600)
+                       timeout=3600, env=env)
     out = {"seq": seq, "sp_ac": sp_ac, "wall_s": round(time.time() - t0, 1)}
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     if r.returncode == 0 and lines:
