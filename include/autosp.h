@@ -72,6 +72,11 @@ AUTOSP_API int autosp_symm_open(const void* ipc_handle, void** dev_ptr);
 AUTOSP_API int autosp_symm_close(void* peer_ptr);
 AUTOSP_API int autosp_symm_free(void* dev_ptr);
 AUTOSP_API int autosp_memset_async(void* dev_ptr, int value, size_t bytes, void* stream);
+/* A DLPack (v0.8 DLManagedTensor, capsule name "dltensor") 1-D uint8 view of `nbytes`
+ * of memory owned by this library (receive-region slots), allocated in C with a C deleter
+ * so the framework can drop the view at any time -- including interpreter shutdown --
+ * without calling back into the host language.  device_type: 2 = CUDA, 1 = CPU. */
+AUTOSP_API void* autosp_dlpack_wrap(void* ptr, int64_t nbytes, int device_type, int device_id);
 
 /* ------------------------------------------------------------------ all-to-all reshard
  * One logical [b, s, h, d] tensor (head_dim d contiguous).  Strides are in ELEMENTS.

@@ -48,6 +48,7 @@ EXPORTS = {
     "autosp_symm_close": (C.c_int, [C.c_void_p]),
     "autosp_symm_free": (C.c_int, [C.c_void_p]),
     "autosp_memset_async": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t, C.c_void_p]),
+    "autosp_dlpack_wrap": (C.c_void_p, [C.c_void_p, C.c_int64, C.c_int, C.c_int]),
     "autosp_a2a": (C.c_int, [C.c_int, C.POINTER(A2ATensor), C.c_int, C.c_int, C.c_int, C.c_int,
                              C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p),
                              C.POINTER(C.c_void_p), C.c_uint32, C.c_void_p]),

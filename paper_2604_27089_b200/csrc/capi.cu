@@ -2,6 +2,8 @@
 // memory.  The compute entry points live next to their kernels (a2a.cu, attn_*.cu).
 #include <cstdarg>
 #include <cstdio>
+#include <cstddef>
+#include <cstdint>
 #include <cstring>
 #include <cuda_runtime.h>
 
@@ -84,6 +86,42 @@ extern "C" int autosp_memset_async(void* dev_ptr, int value, size_t bytes, void*
   cudaError_t e = cudaMemsetAsync(dev_ptr, value, bytes, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "memset_async");
   return AUTOSP_OK;
+}
+
+// Minimal DLPack (v0.8) ABI: what torch.utils.dlpack.from_dlpack reads from a "dltensor"
+// capsule.  The struct and its shape live in one C allocation freed by the C deleter.
+namespace {
+struct DLDevice { int device_type; int device_id; };
+struct DLDataType { uint8_t code; uint8_t bits; uint16_t lanes; };
+struct DLTensor {
+  void* data; DLDevice device; int ndim; DLDataType dtype;
+  int64_t* shape; int64_t* strides; uint64_t byte_offset;
+};
+struct DLManagedTensor {
+  DLTensor dl_tensor; void* manager_ctx; void (*deleter)(DLManagedTensor*);
+};
+struct Wrapped { DLManagedTensor mt; int64_t shape[1]; };
+void wrapped_deleter(DLManagedTensor* mt) { delete reinterpret_cast<Wrapped*>(mt); }
+}  // namespace
+
+extern "C" void* autosp_dlpack_wrap(void* ptr, int64_t nbytes, int device_type, int device_id) {
+  if (!ptr || nbytes < 0) {
+    autosp_set_error("dlpack_wrap: bad arguments");
+    return nullptr;
+  }
+  Wrapped* w = new Wrapped{};
+  w->shape[0] = nbytes;
+  w->mt.dl_tensor.data = ptr;
+  w->mt.dl_tensor.device = DLDevice{device_type, device_id};
+  w->mt.dl_tensor.ndim = 1;
+  w->mt.dl_tensor.dtype = DLDataType{1, 8, 1};  // kDLUInt, 8 bits
+  w->mt.dl_tensor.shape = w->shape;
+  w->mt.dl_tensor.strides = nullptr;
+  w->mt.dl_tensor.byte_offset = 0;
+  w->mt.manager_ctx = nullptr;
+  w->mt.deleter = wrapped_deleter;
+  static_assert(offsetof(Wrapped, mt) == 0, "DLManagedTensor first");
+  return &w->mt;
 }
 
 int autosp_preload_a2a();

@@ -45,54 +45,23 @@ def default_pool_bytes(device) -> int:
     return int(total * POOL_FRACTION) // (1 << 20) * (1 << 20)
 
 
-class _DLDevice(C.Structure):
-    _fields_ = [("device_type", C.c_int), ("device_id", C.c_int)]
-
-
-class _DLDataType(C.Structure):
-    _fields_ = [("code", C.c_uint8), ("bits", C.c_uint8), ("lanes", C.c_uint16)]
-
-
-class _DLTensor(C.Structure):
-    _fields_ = [("data", C.c_void_p), ("device", _DLDevice), ("ndim", C.c_int),
-                ("dtype", _DLDataType), ("shape", C.POINTER(C.c_int64)),
-                ("strides", C.POINTER(C.c_int64)), ("byte_offset", C.c_uint64)]
-
-
-class _DLManagedTensor(C.Structure):
-    pass
-
-
-_DLManagedTensor._fields_ = [("dl_tensor", _DLTensor), ("manager_ctx", C.c_void_p),
-                             ("deleter", C.CFUNCTYPE(None, C.POINTER(_DLManagedTensor)))]
 _PyCapsule_New = C.pythonapi.PyCapsule_New
 _PyCapsule_New.restype = C.py_object
 _PyCapsule_New.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
-_KEEP: dict[int, tuple] = {}
-
-
-@C.CFUNCTYPE(None, C.POINTER(_DLManagedTensor))
-def _dl_deleter(ptr):
-    _KEEP.pop(C.addressof(ptr.contents), None)
 
 
 def _raw_tensor(ptr: int, nbytes: int, device) -> torch.Tensor:
     """Zero-copy uint8 tensor over raw device memory we own (its own StorageImpl, no
-    allocator involvement and -- unlike __cuda_array_interface__ -- no stream sync)."""
-    shape = (C.c_int64 * 1)(nbytes)
-    mt = _DLManagedTensor()
-    mt.dl_tensor.data = ptr
-    cuda = torch.device(device).type == "cuda"
-    mt.dl_tensor.device = _DLDevice(2 if cuda else 1, (torch.device(device).index or 0) if cuda else 0)
-    mt.dl_tensor.ndim = 1
-    mt.dl_tensor.dtype = _DLDataType(1, 8, 1)  # uint8
-    mt.dl_tensor.shape = shape
-    mt.dl_tensor.strides = None
-    mt.dl_tensor.byte_offset = 0
-    mt.deleter = _dl_deleter
-    _KEEP[C.addressof(mt)] = (mt, shape)
-    cap = _PyCapsule_New(C.addressof(mt), b"dltensor", None)
-    return torch.utils.dlpack.from_dlpack(cap)
+    allocator involvement and -- unlike __cuda_array_interface__ -- no stream sync).  The
+    DLPack struct is allocated and freed in C (autosp_dlpack_wrap), so dropping the view
+    never calls back into Python (a Python deleter segfaulted at interpreter shutdown)."""
+    dev = torch.device(device)
+    cuda = dev.type == "cuda"
+    mt = _lib.load().autosp_dlpack_wrap(ptr, nbytes, 2 if cuda else 1,
+                                        (dev.index or 0) if cuda else 0)
+    if not mt:
+        _lib.check(2, "dlpack_wrap")
+    return torch.utils.dlpack.from_dlpack(_PyCapsule_New(mt, b"dltensor", None))
 
 
 @dataclass

@@ -82,23 +82,70 @@ def _nbytes(n: fx.Node) -> int | None:
 
 
 _NORMS = {"aten::_fused_rms_norm", "aten::rms_norm", "aten::native_layer_norm"}
+_CASTS = {"aten::_to_copy", "prims::convert_element_type"}
+
+
+def _norm_input(n: fx.Node) -> bool:
+    """n enters a normalisation: a fused norm op, or a decomposed RMSNorm
+    ``x * rsqrt(mean(x^2) + eps)`` (possibly after an fp32 cast of x)."""
+    for u in n.users:
+        if u.op != "call_function":
+            continue
+        name = _opname(u)
+        if name in _NORMS and u.args and u.args[0] is n:
+            return True
+        if name in _CASTS and _norm_input_decomposed(u):
+            return True
+    return _norm_input_decomposed(n)
+
+
+def _norm_input_decomposed(n: fx.Node) -> bool:
+    users = [u for u in n.users if u.op == "call_function"]
+    has_sq = any(_opname(u) == "aten::pow" for u in users)
+    has_scale = any(_opname(u) == "aten::mul" and any(
+        isinstance(a, fx.Node) and _opname(a) == "aten::rsqrt" for a in u.args) for u in users)
+    return has_sq and has_scale
 
 
 def is_residual_boundary(n: fx.Node) -> bool:
-    """Values entering a normalisation = the residual stream at a layer boundary.  Guarding
-    them gives per-layer checkpoints: everything between two boundaries (norms,
-    projections, RoPE, MLP) is recomputable, attention and the a2a outputs are saved, and
-    the min-cut never "recomputes" a residual value through the whole network (which costs
-    0 bytes in a pure byte min-cut but O(L^2) time)."""
-    return any(u.op == "call_function" and _opname(u) in _NORMS and u.args and u.args[0] is n
-               for u in n.users)
+    """Values entering a normalisation = the residual stream (x_in before attention,
+    x_mid before the MLP, the final hidden state)."""
+    return n.op == "call_function" and _norm_input(n)
+
+
+def is_layer_boundary(n: fx.Node, max_nodes: int = 256) -> bool:
+    """The residual value entering a layer's pre-attention norm (x_in).  Guarding these
+    gives per-layer checkpoints: everything from x_in to the next x_in except attention
+    and the a2a outputs (norms, projections, RoPE, the mid-layer residual x_mid, the MLP)
+    is recomputable; the min-cut cannot "recompute" a residual value through the whole
+    network (0 bytes in a pure byte min-cut but O(L^2) time).  x_in is recognised by
+    reaching an attention / all-to-all through exactly one projection matmul without
+    crossing another residual value."""
+    if not is_residual_boundary(n):
+        return False
+    seen = {n}
+    frontier = [(u, 0) for u in n.users]
+    while frontier and len(seen) < max_nodes:
+        u, mm = frontier.pop()
+        if u in seen or u.op != "call_function":
+            continue
+        seen.add(u)
+        if is_autosp_attention(u) or is_autosp_collective(u):
+            return True
+        if is_residual_boundary(u):
+            continue
+        k = mm + (1 if _is_matmul(u) else 0)
+        if k > 1:
+            continue
+        frontier.extend((w, k) for w in u.users)
+    return False
 
 
 def guarded(n: fx.Node, mode: AcMode) -> bool:
     """Forward nodes that must not be recomputed (ac_pass.py:103-114 + the AutoSP guard)."""
     if is_autosp_collective(n) or is_autosp_attention(n):
         return True
-    if is_residual_boundary(n):
+    if is_layer_boundary(n):
         return True
     if n.op == "call_function" and n.target is operator.getitem:
         src = n.args[0]
