@@ -22,6 +22,7 @@ KNOWN_PASSES = ("auto_sp", "sp_ac")
 _PASSES: list[str] = []
 _AC_MODE = AcMode.AUTO
 LAST_INFO: dict = {}
+_COMPILER_OVERRIDE = None  # debug tools (tools/mem_trace.py) swap in a tracing executor
 
 
 def reg_passes(passes: list[str], ac_mode: str | AcMode = AcMode.AUTO) -> None:
@@ -49,6 +50,8 @@ def backend(passes: list[str] | None = None, ac_mode: AcMode | None = None):
     mode = _AC_MODE if ac_mode is None else AcMode(ac_mode)
 
     def _compiler(gm, example_inputs):
+        if _COMPILER_OVERRIDE is not None:
+            return _COMPILER_OVERRIDE(gm, example_inputs)
         return make_boxed_func(gm.forward)
 
     def _backend(gm: torch.fx.GraphModule, example_inputs):

@@ -72,6 +72,21 @@ def _is_matmul(n: fx.Node) -> bool:
     return name.startswith("aten::") and name[6:] in _MATMULS
 
 
+_VIEWS = {"aten::t", "aten::view", "aten::_unsafe_view", "aten::transpose", "aten::permute",
+          "aten::expand", "aten::slice", "aten::alias", "aten::detach", "aten::reshape",
+          "aten::unsqueeze", "aten::squeeze"}
+
+
+def _aliases_input(n: fx.Node) -> bool:
+    """A graph input (parameter / user input) or a view of one: alive anyway during the
+    backward, so keeping it costs no memory (a pure byte min-cut would charge the weight
+    transposes every layer's matmul backward needs)."""
+    while n.op == "call_function" and _opname(n) in _VIEWS and n.args and \
+            isinstance(n.args[0], fx.Node):
+        n = n.args[0]
+    return n.op == "placeholder"
+
+
 def _nbytes(n: fx.Node) -> int | None:
     v = n.meta.get("val")
     if isinstance(v, torch.Tensor):
@@ -113,21 +128,22 @@ def is_residual_boundary(n: fx.Node) -> bool:
     return n.op == "call_function" and _norm_input(n)
 
 
-def is_layer_boundary(n: fx.Node, max_nodes: int = 256) -> bool:
+def is_layer_boundary(n: fx.Node, fw: set | None = None, max_nodes: int = 512) -> bool:
     """The residual value entering a layer's pre-attention norm (x_in).  Guarding these
     gives per-layer checkpoints: everything from x_in to the next x_in except attention
     and the a2a outputs (norms, projections, RoPE, the mid-layer residual x_mid, the MLP)
     is recomputable; the min-cut cannot "recompute" a residual value through the whole
     network (0 bytes in a pure byte min-cut but O(L^2) time).  x_in is recognised by
     reaching an attention / all-to-all through exactly one projection matmul without
-    crossing another residual value."""
+    crossing another residual value (searching forward nodes only when the joint graph's
+    forward set ``fw`` is given: backward nodes reach everything)."""
     if not is_residual_boundary(n):
         return False
     seen = {n}
     frontier = [(u, 0) for u in n.users]
     while frontier and len(seen) < max_nodes:
         u, mm = frontier.pop()
-        if u in seen or u.op != "call_function":
+        if u in seen or u.op != "call_function" or (fw is not None and u not in fw):
             continue
         seen.add(u)
         if is_autosp_attention(u) or is_autosp_collective(u):
@@ -141,11 +157,11 @@ def is_layer_boundary(n: fx.Node, max_nodes: int = 256) -> bool:
     return False
 
 
-def guarded(n: fx.Node, mode: AcMode) -> bool:
+def guarded(n: fx.Node, mode: AcMode, fw: set | None = None) -> bool:
     """Forward nodes that must not be recomputed (ac_pass.py:103-114 + the AutoSP guard)."""
     if is_autosp_collective(n) or is_autosp_attention(n):
         return True
-    if is_layer_boundary(n):
+    if is_layer_boundary(n, fw):
         return True
     if n.op == "call_function" and n.target is operator.getitem:
         src = n.args[0]
@@ -184,8 +200,10 @@ def plan(joint_module: fx.GraphModule, num_fwd_outputs: int, mode: AcMode):
             b = _nbytes(n)
             sym = isinstance(n.meta.get("val"), torch.SymInt)
             cap = None if (b is None and not sym) else (b or 1)
+            if cap is not None and _aliases_input(n):
+                cap = 1
             add(n.name + "_in", n.name + "_out", cap)
-            if guarded(n, mode):
+            if guarded(n, mode, fw):
                 add("source", n.name + "_in")
             elif n.op != "placeholder" and b:
                 # recompute is not free: a node recomputed in backward (n_in on the sink
@@ -219,6 +237,9 @@ def plan(joint_module: fx.GraphModule, num_fwd_outputs: int, mode: AcMode):
     saved_vals = [n for n in saved if isinstance(n.meta.get("val"), torch.Tensor)]
     recomputed = [n for n in fw if n.op != "placeholder" and n.name + "_out" not in reach]
     stats = {"cut_bytes": int(cut_value), "saved": [n.name for n in saved_vals],
+             "saved_bytes": _tensor_bytes([n for n in saved_vals if not _aliases_input(n)]),
+             "saved_detail": [(n.name, _opname(n), tuple(n.meta["val"].shape))
+                              for n in saved_vals],
              "recomputed_candidates": len(recomputed), "mode": mode.value}
     return saved_vals, saved_sym, stats
 

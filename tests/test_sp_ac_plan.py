@@ -1,0 +1,51 @@
+"""sp_ac plan structure on a Llama-shaped graph (CPU, compile-time only: the partition
+runs while tracing; execution is not needed).  The policy being pinned:
+per layer the backward keeps the layer-input residual value, the attention output O
+and its LSE — nothing O(s * d_ffn), no recomputed attention — so saved bytes grow
+linearly in layers with a small per-layer constant (the reference's seq-aware guard set,
+ac_pass.py:103-114, plus the AutoSP guards)."""
+
+import pytest
+import torch
+
+
+def _plan(layers, s, mode="seq-aware"):
+    torch._dynamo.reset()
+    import paper_2604_27089_b200 as autosp
+    from paper_2604_27089_b200 import sp_ac, testing
+    from paper_2604_27089_b200.workloads import LlamaConfig, LlamaDecoder
+    testing.enable_cpu_lowering()
+    cfg = LlamaConfig("t", 256, layers, 4, 2, 512, vocab=128)
+    autosp.reg_passes(["auto_sp", "sp_ac"], ac_mode=mode)
+    autosp.dist.init(1)
+    torch.manual_seed(0)
+    m = LlamaDecoder(cfg, dtype=torch.float32, device="cpu", fused=False)
+    cm = autosp.compile(m)
+    out = cm(torch.randint(0, 128, (1, s)))
+    out.sum().backward()
+    return cfg, dict(sp_ac.LAST_PLAN)
+
+
+@pytest.mark.parametrize("layers", [2, 8])
+def test_seq_aware_keeps_one_residual_per_layer(layers):
+    s = 256
+    cfg, plan = _plan(layers, s)
+    det = plan["saved_detail"]
+    resid = [d for d in det if d[2] == (1, s, cfg.d_model)]
+    attn_o = [d for d in det if d[2] == (1, cfg.hq, s, cfg.head_dim) and d[1] == "getitem"]
+    lse = [d for d in det if d[2] == (1, cfg.hq, s)]
+    ffn = [d for d in det if d[2][0] == 1 and (cfg.d_ffn in d[2][1:] or 2 * cfg.d_ffn in d[2][1:])]
+    assert len(resid) == layers, resid
+    assert len(attn_o) == layers and len(lse) == layers
+    assert not ffn, ffn
+    assert not plan["bw_recomputes_attention"]
+
+
+def test_layer_boundary_detection_is_per_layer():
+    """Deep graphs: the boundary search must stay in the forward graph (backward nodes
+    reach everything), so every layer gets its checkpoint, not only the first few."""
+    _, p2 = _plan(2, 128)
+    _, p8 = _plan(8, 128)
+    per_layer_2 = p2["saved_bytes"] / 2
+    per_layer_8 = p8["saved_bytes"] / 8
+    assert per_layer_8 < 1.5 * per_layer_2

@@ -36,14 +36,35 @@ opt = torch.optim.AdamW(m.parameters(), lr=1e-4, fused=True)
 cm = autosp.compile(m)
 ids = torch.randint(0, cfg.vocab, (1, {seq} + 1), device='cuda')
 t0 = None
-for it in range(2):
-    torch.cuda.synchronize(); t0 = time.perf_counter()
-    loss = lm_loss(cm(ids[:, :-1]), m.lm_head, ids[:, 1:])
-    loss.backward(); opt.step(); opt.zero_grad(set_to_none=True)
-    torch.cuda.synchronize()
 from paper_2604_27089_b200 import sp_ac
+phase = "init"
+gb = lambda: round(torch.cuda.memory_allocated() / 1e9, 2)
+marks = {{"static_gb": gb()}}
+try:
+    for it in range(2):
+        torch.cuda.synchronize(); t0 = time.perf_counter()
+        phase = "forward"
+        hidden = cm(ids[:, :-1])
+        marks["after_fwd_gb"] = gb(); marks["fwd_peak_gb"] = round(torch.cuda.max_memory_allocated() / 1e9, 2)
+        phase = "loss"
+        loss = lm_loss(hidden, m.lm_head, ids[:, 1:])
+        del hidden
+        phase = "backward"
+        loss.backward()
+        marks["after_bwd_gb"] = gb()
+        phase = "optimizer"
+        opt.step(); opt.zero_grad(set_to_none=True)
+        torch.cuda.synchronize()
+except torch.OutOfMemoryError as e:
+    msg = str(e).split("\\n")[0]
+    pl = sp_ac.LAST_PLAN
+    print(json.dumps({{"ok": False, "oom": True, "phase": phase, "iter": it, "error": msg[:400],
+                      "marks": marks, "peak_gb": torch.cuda.max_memory_allocated() / 1e9,
+                      "ac_applied": pl.get("mode_applied"), "n_saved": len(pl.get("saved", [])),
+                      "saved_gb": pl.get("cut_bytes", 0) / 1e9}}))
+    sys.exit(3)
 pl = sp_ac.LAST_PLAN
-print(json.dumps({{"ok": True, "step_s": time.perf_counter() - t0,
+print(json.dumps({{"ok": True, "step_s": time.perf_counter() - t0, "marks": marks,
                   "peak_gb": torch.cuda.max_memory_allocated() / 1e9, "loss": float(loss),
                   "ac_applied": pl.get("mode_applied"), "saved_gb": pl.get("cut_bytes", pl.get("save_all_bytes", 0)) / 1e9}}))
 """
@@ -53,7 +74,7 @@ print(json.dumps({{"ok": True, "step_s": time.perf_counter() - t0,
                        timeout=3600, env=env)
     out = {"seq": seq, "sp_ac": sp_ac, "wall_s": round(time.time() - t0, 1)}
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
-    if r.returncode == 0 and lines:
+    if lines:
         out.update(json.loads(lines[-1]))
     else:
         err = (r.stderr or "").strip()
