@@ -67,6 +67,7 @@ struct Cfg {
   static constexpr int LAYOUT = SW == 128 ? 2 : (SW == 64 ? 4 : 6);
   static constexpr int SBO = 8 * SW;
   static constexpr int TILE = 128 * D * 2;  // one [128 x D] bf16 tile
+  // Q/dO(+lse/delta) ring depth (3 measured slower than 2 for d = 64)
   static constexpr int kQStages = D == 128 ? 1 : 2;
   // S^T buffers in TMEM: two (S(t+1) overlaps the softmax of t) when d <= 64
   static constexpr int NSB = D == 128 ? 1 : 2;
@@ -78,8 +79,8 @@ struct Cfg {
   static constexpr int DO_OFF = Q_OFF + kQStages * TILE;       // dO[st]
   static constexpr int DS_OFF = DO_OFF + kQStages * TILE;      // dS^T [128 keys x 128 q] bf16
   static constexpr int DQ_OFF = DS_OFF + 128 * 128 * 2;        // 2 fp32 chunks [128 x 32]
-  static constexpr int LSE_OFF = DQ_OFF + 2 * 128 * 32 * 4;    // lse[st][128], delta[st][128]
-  static constexpr int BAR_OFF = LSE_OFF + 4 * 128 * 4;
+  static constexpr int LSE_OFF = DQ_OFF + 2 * 128 * 32 * 4;    // lse[kQStages][128], delta[kQStages][128]
+  static constexpr int BAR_OFF = LSE_OFF + 2 * kQStages * 128 * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   // TMEM columns.  d <= 64: S0 | S1 | dP | dV | dK; P^T(t) (bf16) occupies columns
   //   [0,32) and [96,128) of S buffer t%2 and dQ(t) (fp32) columns [32, 32+d), so dP(t+1)
@@ -96,6 +97,7 @@ struct Params {
   CUtensorMap tm_q, tm_k, tm_v, tm_do, tm_dqacc, tm_lse, tm_dlt;
   int lse_tma;         // lse/delta rows staged by TMA with Q/dO (needs S % 4 == 0)
   long long* trace;    // debug timeline (nullptr in production): [16 events][kTraceSteps]
+  float* dqacc;        // [B, Hq, S, D] fp32 accumulator (red.global.add from the drain)
   const float* lse;    // [B, Hq, S]
   const float* delta;  // [B, Hq, S]
   __nv_bfloat16* dk;
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   uint64_t* acc_full = dq_empty + 1;            // final dK/dV complete
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_full + 1);
   float* lse_s = reinterpret_cast<float*>(smem + C::LSE_OFF);  // [kQStages][128]
-  float* dlt_s = lse_s + 256;                                   // [kQStages][128]
+  float* dlt_s = lse_s + C::kQStages * 128;                                   // [kQStages][128]
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -303,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
               if (lane == 0) BWD_TRACE(0, t);
             }
             wait_q(t + 1);
+            if (lane == 0) BWD_TRACE(11, t);
             issue_s(t + 1);
           }
         } else {
@@ -526,10 +529,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     }
   } else if (warp >= kDrainWarp0 && warp < kDrainWarp0 + 4) {
     // ------------------------------------------------------------ dQ drain warpgroup
+    // thread = query row.  dQ(t) leaves TMEM 64 columns at a time (one TMEM round trip);
+    // the columns are released as soon as the last chunk is in registers (S(t+2) reuses
+    // them), then each 32-column chunk is staged through a 128B-swizzled smem slot and
+    // TMA-reduce-added (fp32) into the accumulator.  (Per-thread red.global.add.v4 was
+    // tried: 2048 L2 atomics per step flood the LSU and stall the softmax's smem stores.)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;  // query row within the step
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const bool leader = (warp == kDrainWarp0 && lane == 0);
+    constexpr int NC = D / 32;  // 32-column chunks
     for (int t = 0; t < T; ++t) {
       const int head = kvh * group + t / per_head;
       const int q0 = (m_first + t % per_head) * BQ;
@@ -538,30 +547,36 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       if (threadIdx.x == kDrainWarp0 * 32) BWD_TRACE(9, t);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        // alternate the two staging slots across ALL chunks (also across steps when
-        // D / 32 is odd), so wait_group.read 1 always covers the slot's previous reduce
-        const int chunk_id = t * (D / 32) + c;
-        float* slot = reinterpret_cast<float*>(smem + C::DQ_OFF) + (chunk_id & 1) * (128 * 32);
-        uint32_t v[32];
-        tmem_ld32(dq_addr + c * 32, v);
-        if (leader) bulk_wait_read1();  // the reduce that last used this slot has read it
-        named_bar_sync(2, 128);
+      for (int c2 = 0; c2 < NC; c2 += 2) {
+        uint32_t v[2][32];
+        tmem_ld32(dq_addr + c2 * 32, v[0]);
+        if (c2 + 1 < NC) tmem_ld32(dq_addr + (c2 + 1) * 32, v[1]);
         tmem_wait_ld();
-        if (c == D / 32 - 1) {  // all of dQ(t) is in registers: release the TMEM columns
+        if (c2 + 2 >= NC) {  // all of dQ(t) is in registers: release the TMEM columns
           tc_fence_before();
           mbar_arrive_warp(dq_empty);
         }
-        uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          *reinterpret_cast<uint4*>(srow + ((u ^ (row & 7)) << 4)) =
-              make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
-        fence_proxy_async_smem();
-        named_bar_sync(2, 128);
-        if (leader) {
-          tma_reduce_add_3d(&p.tm_dqacc, slot, c * 32, q0, batch * p.Hq + head);
-          bulk_commit();
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = c2 + cc;
+          if (c >= NC) break;
+          // alternate the two staging slots across ALL chunks (also across steps when
+          // NC is odd), so wait_group.read 1 always covers the slot's previous reduce
+          const int chunk_id = t * NC + c;
+          float* slot = reinterpret_cast<float*>(smem + C::DQ_OFF) + (chunk_id & 1) * (128 * 32);
+          if (leader) bulk_wait_read1();  // the reduce that last used this slot has read it
+          named_bar_sync(2, 128);
+          uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<uint4*>(srow + ((u ^ (row & 7)) << 4)) =
+                make_uint4(v[cc][4 * u], v[cc][4 * u + 1], v[cc][4 * u + 2], v[cc][4 * u + 3]);
+          fence_proxy_async_smem();
+          named_bar_sync(2, 128);
+          if (leader) {
+            tma_reduce_add_3d(&p.tm_dqacc, slot, c * 32, q0, batch * p.Hq + head);
+            bulk_commit();
+          }
         }
       }
       if (threadIdx.x == kDrainWarp0 * 32) BWD_TRACE(10, t);
@@ -614,7 +629,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
   uint64_t* acc_full = dq_empty + 1;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_full + 1);
   float* lse_s = reinterpret_cast<float*>(smem + C::LSE_OFF);  // [kQStages][128]
-  float* dlt_s = lse_s + 256;
+  float* dlt_s = lse_s + C::kQStages * 128;
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -1124,6 +1139,7 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   }
   p.lse = lse;
   p.delta = delta;
+  p.dqacc = dqacc;
   p.trace = g_bwd_trace;
   p.dk = static_cast<__nv_bfloat16*>(const_cast<void*>(dk.ptr));
   p.dv = static_cast<__nv_bfloat16*>(const_cast<void*>(dv.ptr));

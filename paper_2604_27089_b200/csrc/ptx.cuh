@@ -142,6 +142,12 @@ AUTOSP_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "
 AUTOSP_DEV void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+// 16-byte fp32 reduction into global memory (sm_90+): no smem staging, no TMA engine
+AUTOSP_DEV void red_add_v4(float* gaddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gaddr), "r"(a), "r"(b),
+               "r"(c), "r"(d)
+               : "memory");
+}
 AUTOSP_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 AUTOSP_DEV void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -20,9 +20,9 @@ lib.autosp_debug_set_bwd_trace(None)
 t = buf.view(16, 64).cpu()
 names = ["mma:dq_empty", "mma:dP_issued", "mma:p_ready", "mma:ds_ready", "mma:dQ_issued",
          "sm:s_full", "sm:p_arrive", "sm:dp_full", "sm:ds_arrive", "dr:dq_full", "dr:dq_empty",
-         "p2:ld_done", "p2:sttm_issued", "p2:sts_done", "p2:wait_st", "p2:fence_async"]
+         "mma:q_next"]
 base = int(t[1, 0])
 for step in range(8, 16):
-    row = "  ".join(f"{n}={int(t[i, step]) - base:8d}" for i, n in enumerate(names))
+    row = "  ".join(f"{n}={int(t[i, step]) - base:8d}" for i, n in enumerate(names) if int(t[i, step]) > 0)
     print(f"t={step}: {row}")
 print("per-step cycles (dP issue deltas):", [int(t[1, i + 1] - t[1, i]) for i in range(8, 40)])
