@@ -65,6 +65,109 @@ AUTOSP_DEV void spin_until_epoch(const uint32_t* p, uint32_t e) {
   }
 }
 
+// Completion of one push launch: the CTA's (remote) stores are ordered before thread 0's
+// system-scope fence by the barrier (fences are cumulative), then the last CTA publishes
+// arrive[rank] = epoch (+ the offset check word) in every peer's flag block.
+AUTOSP_DEV void push_complete(const A2AParams& p) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    uint32_t* ctr = p.peer_flags[p.rank] + kCounterWord;
+    const uint32_t old = atom_add_acqrel_gpu(ctr, 1u);
+    if (old == gridDim.x - 1) {
+      *ctr = 0u;
+      __threadfence_system();
+      for (int j = 0; j < p.P; ++j)
+        if (j != p.rank) {
+          p.peer_flags[j][kCheckWord + p.rank] = p.check;
+          st_release_sys(p.peer_flags[j] + kArriveWord + p.rank, p.epoch);
+        }
+    }
+  }
+}
+
+// Fast path: 16-byte vectors, rows of ROWB = d * elem_bytes in {64, 128, 256} bytes.  A
+// warp owns (tensor, batch, head, 16-token tile); everything but the token offset is
+// hoisted out of the row loop (the generic kernel below recomputed 64-bit strided
+// addresses and integer divisions for all 16 possible row passes, predicated, and was
+// instruction-bound at ~0.5 TB/s).
+template <int ROWB>
+__global__ void __launch_bounds__(kA2AThreads) a2a_push_fast(const __grid_constant__ A2AParams p) {
+  constexpr int VPR = ROWB / 16;          // vectors per row
+  constexpr int RPP = 32 / VPR;           // rows per pass
+  constexpr int PASSES = kTileTokens / RPP;
+  const int lane = threadIdx.x & 31;
+  const int r_in = lane / VPR;
+  const int voff = (lane % VPR) * 16;
+  const bool s2h = p.dir == AUTOSP_SEQ_TO_HEAD;
+  const int s_src = s2h ? p.s_loc : p.s_glob;
+  const int warps_total = gridDim.x * (kA2AThreads / 32);
+  const int gw = blockIdx.x * (kA2AThreads / 32) + (threadIdx.x >> 5);
+  const int total = (int)p.total_items;
+  for (int item = gw; item < total; item += warps_total) {
+    int it = item;
+    const A2ATensorDev* T = &p.t[0];
+#pragma unroll
+    for (int k = 1; k < AUTOSP_A2A_MAX_TENSORS; ++k)
+      if (k < p.n && it >= (int)T->items) { it -= (int)T->items; T = &p.t[k]; }
+    const int tile = it % T->tiles;
+    const int bh = it / T->tiles;
+    const int hh = bh % T->heads;
+    const int bi = bh / T->heads;
+    const int t0 = tile * kTileTokens;
+    const int eb = p.eb;
+    const char* src = T->src + ((int64_t)bi * T->ss_b + (int64_t)t0 * T->ss_s +
+                                (int64_t)hh * T->ss_h) * eb + voff;
+    const int64_t sstep = T->ss_s * eb;
+    const int64_t dstep = T->ds_s * eb;
+    const int last = min(t0 + kTileTokens, s_src) - 1;
+    uint4 v[PASSES];
+#pragma unroll
+    for (int ps = 0; ps < PASSES; ++ps) {
+      const int r = ps * RPP + r_in;
+      if (t0 + r <= last) v[ps] = __ldg(reinterpret_cast<const uint4*>(src + r * sstep));
+    }
+    if (s2h) {
+      const int hl = T->heads / p.P;
+      const int j = hh / hl;
+      char* dst = p.peer_base[j] + T->dst_off +
+                  ((int64_t)bi * T->ds_b + (int64_t)(p.rank * p.s_loc + t0) * T->ds_s +
+                   (int64_t)(hh - j * hl) * T->ds_h) * eb + voff;
+#pragma unroll
+      for (int ps = 0; ps < PASSES; ++ps) {
+        const int r = ps * RPP + r_in;
+        if (t0 + r <= last) *reinterpret_cast<uint4*>(dst + r * dstep) = v[ps];
+      }
+    } else {
+      const int dh = p.rank * T->heads + hh;
+      const int j0 = t0 / p.s_loc;
+      if (last / p.s_loc == j0) {  // tile inside one destination rank's token range
+        char* dst = p.peer_base[j0] + T->dst_off +
+                    ((int64_t)bi * T->ds_b + (int64_t)(t0 - j0 * p.s_loc) * T->ds_s +
+                     (int64_t)dh * T->ds_h) * eb + voff;
+#pragma unroll
+        for (int ps = 0; ps < PASSES; ++ps) {
+          const int r = ps * RPP + r_in;
+          if (t0 + r <= last) *reinterpret_cast<uint4*>(dst + r * dstep) = v[ps];
+        }
+      } else {
+#pragma unroll
+        for (int ps = 0; ps < PASSES; ++ps) {
+          const int t = t0 + ps * RPP + r_in;
+          if (t <= last) {
+            const int j = t / p.s_loc;
+            char* dst = p.peer_base[j] + T->dst_off +
+                        ((int64_t)bi * T->ds_b + (int64_t)(t - j * p.s_loc) * T->ds_s +
+                         (int64_t)dh * T->ds_h) * eb + voff;
+            *reinterpret_cast<uint4*>(dst) = v[ps];
+          }
+        }
+      }
+    }
+  }
+  push_complete(p);
+}
+
 // G = bytes moved per lane per row-chunk (16, 8, 4 or 2).
 template <typename V>
 __global__ void __launch_bounds__(kA2AThreads) a2a_push_kernel(const __grid_constant__ A2AParams p) {
@@ -127,23 +230,7 @@ __global__ void __launch_bounds__(kA2AThreads) a2a_push_kernel(const __grid_cons
     }
   }
 
-  // 1) completion: make this thread's (remote) stores visible system-wide, then the
-  //    last CTA publishes arrive[rank] = epoch in every peer's flag block.
-  __threadfence_system();
-  __syncthreads();
-  if (tid == 0) {
-    uint32_t* ctr = p.peer_flags[p.rank] + kCounterWord;
-    const uint32_t old = atom_add_acqrel_gpu(ctr, 1u);
-    if (old == gridDim.x - 1) {
-      *ctr = 0u;
-      __threadfence_system();
-      for (int j = 0; j < p.P; ++j)
-        if (j != p.rank) {
-          p.peer_flags[j][kCheckWord + p.rank] = p.check;
-          st_release_sys(p.peer_flags[j] + kArriveWord + p.rank, p.epoch);
-        }
-    }
-  }
+  push_complete(p);
 }
 
 // 0) publish "I reached epoch" and wait until every peer has reached it too.  One CTA:
@@ -279,7 +366,15 @@ extern "C" int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n
   if (blocks < 1) blocks = 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (world > 1) a2a_handshake_kernel<<<1, 32, 0, st>>>(p);
-  switch (align) {
+  const bool fast = align == 16 && (row == 64 || row == 128 || row == 256) &&
+                    p.total_items < (int64_t)INT32_MAX;
+  if (fast) {
+    switch (row) {
+      case 64: a2a_push_fast<64><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
+      case 128: a2a_push_fast<128><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
+      default: a2a_push_fast<256><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
+    }
+  } else switch (align) {
     case 16: a2a_push_kernel<uint4><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
     case 8: a2a_push_kernel<uint2><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
     case 4: a2a_push_kernel<uint32_t><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
@@ -331,6 +426,9 @@ extern "C" int autosp_a2a_mark_ready(uint32_t* const* flags, int world, uint32_t
 
 int autosp_preload_a2a() {
   cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, autosp::a2a_push_fast<64>);
+  cudaFuncGetAttributes(&a, autosp::a2a_push_fast<128>);
+  cudaFuncGetAttributes(&a, autosp::a2a_push_fast<256>);
   cudaFuncGetAttributes(&a, autosp::a2a_push_kernel<uint4>);
   cudaFuncGetAttributes(&a, autosp::a2a_push_kernel<uint2>);
   cudaFuncGetAttributes(&a, autosp::a2a_push_kernel<uint32_t>);
