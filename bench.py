@@ -210,7 +210,9 @@ def main():
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
-        tdist.init_process_group("nccl")
+        # NCCL for real multi-GPU runs; AUTOSP_BENCH_BACKEND=gloo lets several ranks share
+        # one GPU to exercise this path (the reshard itself never uses NCCL)
+        tdist.init_process_group(os.environ.get("AUTOSP_BENCH_BACKEND", "nccl"))
     rank = tdist.get_rank() if world > 1 else 0
     passes = ["auto_sp"] if args.no_sp_ac else ["auto_sp", "sp_ac"]
     autosp.reg_passes(passes, ac_mode=args.ac_mode)

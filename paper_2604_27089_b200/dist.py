@@ -183,7 +183,8 @@ def init(sp_group_size: int, pool_bytes: int | None = None, backend: str | None 
     if world % sp_group_size:
         raise ValidationError(f"world size {world} not divisible by SP group size {sp_group_size}")
     if torch.cuda.is_available():
-        local = int(os.environ.get("LOCAL_RANK", rank % max(torch.cuda.device_count(), 1)))
+        # (modulo: several ranks may share a device in single-GPU multi-process tests)
+        local = int(os.environ.get("LOCAL_RANK", rank)) % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local)
         device = torch.device("cuda", local)
     else:
