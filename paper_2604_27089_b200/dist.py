@@ -229,23 +229,55 @@ def register_state(st: SPState) -> None:
     _REGISTRY[st.name] = st
 
 
-def reduce_gradients(params, st: SPState | None = None) -> None:
+REDUCE_BUCKET_BYTES = 128 << 20
+
+
+def reduce_gradients(params, st: SPState | None = None,
+                     bucket_bytes: int = REDUCE_BUCKET_BYTES) -> None:
     """Sum the per-rank partial parameter gradients over the SP group (SURVEY §0 finding 6:
-    the reference's tests sum them, test_acceptance.py:89-96) and average over DP."""
+    the reference's tests sum them, test_acceptance.py:89-96) and average over DP.
+    Gradients are packed into buckets of at most ``bucket_bytes`` (one collective per
+    bucket; a gradient larger than a bucket is reduced in place), so the transient memory
+    is one bucket, not a flat copy of every gradient (16 GB for an 8B model)."""
     st = st or state()
     if not tdist.is_initialized():
         return
     grads = [p.grad for p in params if p.grad is not None]
     if not grads:
         return
-    flat = torch.cat([g.reshape(-1) for g in grads])
-    if st.group is not None and st.world > 1:
-        tdist.all_reduce(flat, group=st.group)
-    if st.dp_group is not None and tdist.get_world_size(st.dp_group) > 1:
-        tdist.all_reduce(flat, group=st.dp_group)
-        flat /= tdist.get_world_size(st.dp_group)
-    off = 0
+    sp = st.group if (st.group is not None and st.world > 1) else None
+    dp = st.dp_group if (st.dp_group is not None and tdist.get_world_size(st.dp_group) > 1) \
+        else None
+    if sp is None and dp is None:
+        return
+
+    def reduce(t):
+        if sp is not None:
+            tdist.all_reduce(t, group=sp)
+        if dp is not None:
+            tdist.all_reduce(t, group=dp)
+            t /= tdist.get_world_size(dp)
+
+    def flush(bucket):
+        if not bucket:
+            return
+        if len(bucket) == 1:
+            reduce(bucket[0])
+            return
+        flat = torch.cat([g.reshape(-1) for g in bucket])
+        reduce(flat)
+        off = 0
+        for g in bucket:
+            n = g.numel()
+            g.copy_(flat[off:off + n].view_as(g))
+            off += n
+
+    bucket, size = [], 0
     for g in grads:
-        n = g.numel()
-        g.copy_(flat[off:off + n].view_as(g))
-        off += n
+        nb = g.numel() * g.element_size()
+        if bucket and (size + nb > bucket_bytes or g.dtype != bucket[0].dtype):
+            flush(bucket)
+            bucket, size = [], 0
+        bucket.append(g)
+        size += nb
+    flush(bucket)
