@@ -137,6 +137,30 @@ AUTOSP_API int autosp_attn_fwd(autosp_attn_tensor q, autosp_attn_tensor k, autos
                     autosp_attn_tensor o, float* lse, int b, int hq, int hkv, int s, int d,
                     float scale, int causal, void* stream);
 
+/* Fused K3 + K2: the attention forward ALSO pushes every output row to the rank that owns
+ * its token (the head->seq all-to-all of O, reference executor.py:222-229) from the
+ * epilogue, over the same symmetric regions / epoch protocol as autosp_a2a, so the
+ * transfer overlaps the attention math tile by tile and no separate reshard kernel
+ * reads O back.  q/k/v/o/lse as in autosp_attn_fwd over the FULL sequence s on this
+ * rank's hq heads; row (b, h, t) lands in rank t / (s / world) at byte offset
+ * dst_offset + 2 * (b * dst_stride_b + (t mod s/world) * dst_stride_s
+ *                   + (rank * hq + h) * dst_stride_h)
+ * of its receive region.  Publishes arrive flags like autosp_a2a; the caller then runs
+ * autosp_a2a_wait.  Replaces the autosp_attn_fwd + autosp_a2a(head_to_seq) pair. */
+typedef struct autosp_push_spec {
+  int world, rank;
+  int64_t dst_offset;                          /* bytes, identical on every rank */
+  int64_t dst_stride_b, dst_stride_s, dst_stride_h;  /* elements */
+  void* const* peer_base;                      /* [world] receive regions */
+  uint32_t* const* peer_flags;                 /* [world] flag blocks */
+  uint32_t epoch;
+} autosp_push_spec;
+
+AUTOSP_API int autosp_attn_fwd_push(autosp_attn_tensor q, autosp_attn_tensor k,
+                    autosp_attn_tensor v, autosp_attn_tensor o, float* lse, int b, int hq,
+                    int hkv, int s, int d, float scale, int causal,
+                    const autosp_push_spec* push, void* stream);
+
 /* fp32 workspace the backward needs: dq accumulator [b, hq, s, d] + delta [b, hq, s] */
 AUTOSP_API size_t autosp_attn_bwd_workspace_bytes(int b, int hq, int s, int d);
 AUTOSP_API int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,

@@ -35,6 +35,13 @@ class AttnTensor(C.Structure):
                 ("stride_s", C.c_int64)]
 
 
+class PushSpec(C.Structure):
+    _fields_ = [("world", C.c_int), ("rank", C.c_int), ("dst_offset", C.c_int64),
+                ("dst_stride_b", C.c_int64), ("dst_stride_s", C.c_int64),
+                ("dst_stride_h", C.c_int64), ("peer_base", C.c_void_p),
+                ("peer_flags", C.c_void_p), ("epoch", C.c_uint32)]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -58,6 +65,8 @@ EXPORTS = {
                                         C.c_void_p]),
     "autosp_attn_fwd": (C.c_int, [AttnTensor] * 4 + [C.c_void_p] + [C.c_int] * 5 +
                         [C.c_float, C.c_int, C.c_void_p]),
+    "autosp_attn_fwd_push": (C.c_int, [AttnTensor] * 4 + [C.c_void_p] + [C.c_int] * 5 +
+                             [C.c_float, C.c_int, C.POINTER(PushSpec), C.c_void_p]),
     "autosp_swiglu_fwd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int64,
                                     C.c_int64, C.c_void_p]),
     "autosp_swiglu_bwd": (C.c_int, [C.c_void_p] * 3 + [C.c_int64, C.c_int] + [C.c_int64] * 3 +

@@ -20,14 +20,10 @@
 #include <cuda_runtime.h>
 
 #include "../../include/autosp.h"
+#include "flags.cuh"
 #include "ptx.cuh"
 
 namespace autosp {
-
-constexpr int kReadyWord = 0;
-constexpr int kArriveWord = 16;   // + src rank
-constexpr int kCheckWord = 32;    // + src rank: sender's view of the destination offset
-constexpr int kCounterWord = 48;  // CTA completion counter (local use only)
 constexpr int kTileTokens = 16;
 constexpr int kA2AThreads = 256;
 
@@ -65,25 +61,8 @@ AUTOSP_DEV void spin_until_epoch(const uint32_t* p, uint32_t e) {
   }
 }
 
-// Completion of one push launch: the CTA's (remote) stores are ordered before thread 0's
-// system-scope fence by the barrier (fences are cumulative), then the last CTA publishes
-// arrive[rank] = epoch (+ the offset check word) in every peer's flag block.
 AUTOSP_DEV void push_complete(const A2AParams& p) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    uint32_t* ctr = p.peer_flags[p.rank] + kCounterWord;
-    const uint32_t old = atom_add_acqrel_gpu(ctr, 1u);
-    if (old == gridDim.x - 1) {
-      *ctr = 0u;
-      __threadfence_system();
-      for (int j = 0; j < p.P; ++j)
-        if (j != p.rank) {
-          p.peer_flags[j][kCheckWord + p.rank] = p.check;
-          st_release_sys(p.peer_flags[j] + kArriveWord + p.rank, p.epoch);
-        }
-    }
-  }
+  publish_arrival(p.peer_flags, p.P, p.rank, p.epoch, p.check, gridDim.x);
 }
 
 // Fast path: 16-byte vectors, rows of ROWB = d * elem_bytes in {64, 128, 256} bytes.  A
@@ -240,6 +219,17 @@ __global__ void a2a_handshake_kernel(const __grid_constant__ A2AParams p) {
   const int tid = threadIdx.x;
   if (tid == 0) st_release_sys(p.peer_flags[p.rank] + kReadyWord, p.epoch);
   if (tid < p.P && tid != p.rank) spin_until_epoch(p.peer_flags[tid] + kReadyWord, p.epoch);
+}
+
+struct ShakeParams {
+  uint32_t* flags[AUTOSP_MAX_WORLD];
+  int P, rank;
+  uint32_t epoch;
+};
+__global__ void handshake_kernel(const __grid_constant__ ShakeParams s) {
+  const int tid = threadIdx.x;
+  if (tid == 0) st_release_sys(s.flags[s.rank] + kReadyWord, s.epoch);
+  if (tid < s.P && tid != s.rank) spin_until_epoch(s.flags[tid] + kReadyWord, s.epoch);
 }
 
 __global__ void a2a_wait_kernel(uint32_t* flags, int P, int rank, uint32_t epoch,
@@ -424,7 +414,21 @@ extern "C" int autosp_a2a_mark_ready(uint32_t* const* flags, int world, uint32_t
   return AUTOSP_OK;
 }
 
+// Ready handshake before a fused compute+push kernel (same protocol as the a2a calls).
+int autosp_internal_handshake(uint32_t* const* flags, int world, int rank, uint32_t epoch,
+                              cudaStream_t stream) {
+  autosp::ShakeParams s{};
+  for (int j = 0; j < world; ++j) s.flags[j] = flags[j];
+  s.P = world;
+  s.rank = rank;
+  s.epoch = epoch;
+  autosp::handshake_kernel<<<1, 32, 0, stream>>>(s);
+  return cudaGetLastError() == cudaSuccess ? AUTOSP_OK : AUTOSP_ERR_CUDA;
+}
+
 int autosp_preload_a2a() {
+  cudaFuncAttributes h;
+  cudaFuncGetAttributes(&h, autosp::handshake_kernel);
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, autosp::a2a_push_fast<64>);
   cudaFuncGetAttributes(&a, autosp::a2a_push_fast<128>);

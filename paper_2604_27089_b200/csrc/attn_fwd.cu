@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/autosp.h"
+#include "flags.cuh"
 #include "ptx.cuh"
 #include "tma.cuh"
 
@@ -80,6 +81,12 @@ struct Params {
   int causal;
   int n_qblk;
   long long* trace;  // debug timeline of the heaviest CTA (nullptr in production)
+  // fused head->seq all-to-all of O (autosp_attn_fwd_push); push == 0: local O only
+  int push, P, rank, s_loc;
+  int64_t dst_off, d_sb, d_ss, d_sh;  // bytes / elements
+  char* peer_base[AUTOSP_MAX_WORLD];
+  uint32_t* peer_flags[AUTOSP_MAX_WORLD];
+  uint32_t epoch, check;
 };
 constexpr int kTraceSteps = 64;
 #define FWD_TRACE(ev, t)                                                                   \
@@ -434,6 +441,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
       __nv_bfloat16* orow = p.o + (int64_t)batch * p.o_sb + (int64_t)head * p.o_sh +
                             (int64_t)qi * p.o_ss;
+      // fused K2: the same row goes to the rank owning token qi (token-major, global head
+      // rank * Hq + head), written while the other tiles of this CTA are still computing
+      uint4* prow = nullptr;
+      if (p.push && qi < p.S) {
+        const int j = qi / p.s_loc;
+        prow = reinterpret_cast<uint4*>(
+            p.peer_base[j] + p.dst_off +
+            ((int64_t)batch * p.d_sb + (int64_t)(qi - j * p.s_loc) * p.d_ss +
+             (int64_t)(p.rank * p.Hq + head) * p.d_sh) * 2);
+      }
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t orr[32];
@@ -453,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             v.w = pack_bf16(__uint_as_float(orr[8 * t + 6]) * inv_l,
                             __uint_as_float(orr[8 * t + 7]) * inv_l);
             dst[t] = v;
+            if (prow) prow[c / 8 + t] = v;
           }
         }
       }
@@ -464,14 +482,32 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   tc_fence_before();
   __syncthreads();
   if (warp == kAllocWarp) tmem_dealloc<C::TMEM_COLS>(tmem);
+  if (p.push) publish_arrival(p.peer_flags, p.P, p.rank, p.epoch, p.check,
+                              gridDim.x * gridDim.y * gridDim.z);
 }
 
 template <int D>
 int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autosp_attn_tensor& v,
            const autosp_attn_tensor& o, float* lse, int B, int Hq, int Hkv, int S, float scale,
-           int causal, cudaStream_t stream) {
+           int causal, const autosp_push_spec* push, cudaStream_t stream) {
   using C = Cfg<D>;
   Params p{};
+  if (push) {
+    p.push = 1;
+    p.P = push->world;
+    p.rank = push->rank;
+    p.s_loc = S / push->world;
+    p.dst_off = push->dst_offset;
+    p.d_sb = push->dst_stride_b;
+    p.d_ss = push->dst_stride_s;
+    p.d_sh = push->dst_stride_h;
+    for (int j = 0; j < push->world; ++j) {
+      p.peer_base[j] = static_cast<char*>(push->peer_base[j]);
+      p.peer_flags[j] = push->peer_flags[j];
+    }
+    p.epoch = push->epoch;
+    p.check = (uint32_t)((uint64_t)push->dst_offset >> 4);
+  }
   if (!make_map_bhsd(&p.tm_q, q.ptr, B, Hq, S, D, q.stride_b, q.stride_h, q.stride_s, C::CE, BM,
                      C::SW) ||
       !make_map_bhsd(&p.tm_k, k.ptr, B, Hkv, S, D, k.stride_b, k.stride_h, k.stride_s, C::CE, BN,
@@ -525,9 +561,57 @@ int autosp_check_attn_tensor(const autosp_attn_tensor& t, const char* name) {
   return AUTOSP_OK;
 }
 
+int autosp_internal_handshake(uint32_t* const* flags, int world, int rank, uint32_t epoch,
+                              cudaStream_t stream);
+
+static int attn_fwd_impl(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
+                         autosp_attn_tensor o, float* lse, int b, int hq, int hkv, int s, int d,
+                         float scale, int causal, const autosp_push_spec* push, void* stream);
+
 extern "C" int autosp_attn_fwd(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
                                autosp_attn_tensor o, float* lse, int b, int hq, int hkv, int s,
                                int d, float scale, int causal, void* stream) {
+  return attn_fwd_impl(q, k, v, o, lse, b, hq, hkv, s, d, scale, causal, nullptr, stream);
+}
+
+extern "C" int autosp_attn_fwd_push(autosp_attn_tensor q, autosp_attn_tensor k,
+                                    autosp_attn_tensor v, autosp_attn_tensor o, float* lse, int b,
+                                    int hq, int hkv, int s, int d, float scale, int causal,
+                                    const autosp_push_spec* push, void* stream) {
+  if (!push || push->world < 1 || push->world > AUTOSP_MAX_WORLD || push->rank < 0 ||
+      push->rank >= push->world || !push->peer_base || !push->peer_flags) {
+    autosp_set_error("attn_fwd_push: bad push spec");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (s % push->world) {
+    autosp_set_error("attn_fwd_push: sequence %d not divisible by world size %d", s, push->world);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (push->dst_offset % 16 || push->dst_stride_b % 8 || push->dst_stride_s % 8 ||
+      push->dst_stride_h % 8) {
+    autosp_set_error("attn_fwd_push: destination offset/strides must be 16-byte multiples");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  for (int j = 0; j < push->world; ++j)
+    if (!push->peer_base[j] || !push->peer_flags[j] ||
+        (reinterpret_cast<uintptr_t>(push->peer_base[j]) & 15)) {
+      autosp_set_error("attn_fwd_push: peer %d base/flags null or misaligned", j);
+      return AUTOSP_ERR_VALIDATION;
+    }
+  if (push->world > 1) {
+    int rc = autosp_internal_handshake(push->peer_flags, push->world, push->rank, push->epoch,
+                                       static_cast<cudaStream_t>(stream));
+    if (rc) {
+      autosp_set_error("attn_fwd_push: handshake launch failed");
+      return rc;
+    }
+  }
+  return attn_fwd_impl(q, k, v, o, lse, b, hq, hkv, s, d, scale, causal, push, stream);
+}
+
+static int attn_fwd_impl(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
+                         autosp_attn_tensor o, float* lse, int b, int hq, int hkv, int s, int d,
+                         float scale, int causal, const autosp_push_spec* push, void* stream) {
   if (b < 1 || hq < 1 || hkv < 1 || s < 1 || hq % hkv) {
     autosp_set_error("attn_fwd: bad shape b=%d hq=%d hkv=%d s=%d", b, hq, hkv, s);
     return AUTOSP_ERR_VALIDATION;
@@ -542,9 +626,9 @@ extern "C" int autosp_attn_fwd(autosp_attn_tensor q, autosp_attn_tensor k, autos
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (d) {
-    case 32: return autosp::fwd::launch<32>(q, k, v, o, lse, b, hq, hkv, s, scale, causal, st);
-    case 64: return autosp::fwd::launch<64>(q, k, v, o, lse, b, hq, hkv, s, scale, causal, st);
-    case 128: return autosp::fwd::launch<128>(q, k, v, o, lse, b, hq, hkv, s, scale, causal, st);
+    case 32: return autosp::fwd::launch<32>(q, k, v, o, lse, b, hq, hkv, s, scale, causal, push, st);
+    case 64: return autosp::fwd::launch<64>(q, k, v, o, lse, b, hq, hkv, s, scale, causal, push, st);
+    case 128: return autosp::fwd::launch<128>(q, k, v, o, lse, b, hq, hkv, s, scale, causal, push, st);
     default:
       autosp_set_error("attn_fwd: head_dim %d unsupported (32, 64, 128)", d);
       return AUTOSP_ERR_UNSUPPORTED;

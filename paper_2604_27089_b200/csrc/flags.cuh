@@ -1,0 +1,39 @@
+// Flag block of a rank's symmetric allocation (dist.py FLAG_BYTES) shared by every kernel
+// that writes into peers' receive regions: the a2a push kernels (a2a.cu) and the fused
+// attention-forward + head->seq push (attn_fwd.cu).  Words are uint32.
+#pragma once
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace autosp {
+
+constexpr int kReadyWord = 0;     // "this rank reached epoch e" (its older readers are done)
+constexpr int kArriveWord = 16;   // + src rank: src finished writing call e into me
+constexpr int kCheckWord = 32;    // + src rank: sender's view of the destination offset
+constexpr int kCounterWord = 48;  // CTA completion counter (local use only)
+
+// Completion of a launch that pushed into peers: every thread's (remote) stores are
+// ordered before thread 0's system-scope fence by the CTA barrier (fences are
+// cumulative); the last CTA to finish publishes arrive[rank] = epoch (+ check word) in
+// every peer's flag block.  Must be called by all threads of every CTA.
+AUTOSP_DEV void publish_arrival(uint32_t* const* peer_flags, int P, int rank, uint32_t epoch,
+                                uint32_t check, uint32_t n_ctas) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    uint32_t* ctr = peer_flags[rank] + kCounterWord;
+    const uint32_t old = atom_add_acqrel_gpu(ctr, 1u);
+    if (old == n_ctas - 1) {
+      *ctr = 0u;
+      __threadfence_system();
+      for (int j = 0; j < P; ++j)
+        if (j != rank) {
+          peer_flags[j][kCheckWord + rank] = check;
+          st_release_sys(peer_flags[j] + kArriveWord + rank, epoch);
+        }
+    }
+  }
+}
+
+}  // namespace autosp

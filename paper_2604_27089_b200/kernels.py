@@ -112,6 +112,29 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool = T
     return o, lse
 
 
+def attn_fwd_push(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
+                  lse: torch.Tensor, scale: float, causal: bool, world: int, rank: int,
+                  dst_offset: int, dst_strides: tuple[int, int, int], peer_base: list[int],
+                  peer_flags: list[int], epoch: int) -> None:
+    """Fused K3 + K2 (autosp_attn_fwd_push): attention into o/lse AND every output row
+    pushed to its token owner's receive region (head->seq all-to-all from the epilogue).
+    dst_strides are the (b, s, h) element strides of the token-major destination."""
+    lib = _lib.load()
+    b, hq, s, d = q.shape
+    hkv = k.shape[1]
+    pb = (C.c_void_p * world)(*peer_base)
+    pf = (C.c_void_p * world)(*peer_flags)
+    spec = _lib.PushSpec(world, rank, dst_offset, dst_strides[0], dst_strides[1], dst_strides[2],
+                         C.cast(pb, C.c_void_p), C.cast(pf, C.c_void_p), epoch & 0xFFFFFFFF)
+    ev = LOG.begin("attn_fwd")
+    rc = lib.autosp_attn_fwd_push(_attn_tensor(q, "q"), _attn_tensor(k, "k"),
+                                  _attn_tensor(v, "v"), _attn_tensor(o, "o"), lse.data_ptr(), b,
+                                  hq, hkv, s, d, float(scale), int(causal), C.byref(spec),
+                                  _stream())
+    _lib.check(rc, "attn_fwd_push")
+    LOG.end("attn_fwd", ev, 2 if world > 1 else 1, causal_attn_flops(b, hq, s, d, causal))
+
+
 def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = None,
              dq=None, dk=None, dv=None):
     """Flash attention backward recomputing P from the saved LSE.

@@ -3,6 +3,8 @@
     autosp::attention(q, k, v, scale, causal) -> (o, lse)          K3 (attn_fwd.cu)
     autosp::attention_backward(do, q, k, v, o, lse, ...) -> dq,dk,dv K4 (attn_bwd.cu)
     autosp::all_to_all(xs, direction, group) -> ys                 K1/K2 (a2a.cu)
+    autosp::attention_a2a(q, k, v, scale, causal, group)           K3 + K2 fused
+        -> (o_tokens, o_heads, lse)                                (attn_fwd.cu push epilogue)
 
 All tensors use the SDPA logical layout ``[b, h, s, d]`` (head_dim contiguous, any
 other strides).  ``all_to_all`` is the reference's AllToAll node
@@ -175,6 +177,60 @@ def _a2a_setup_shapes(ctx, inputs, output):
 all_to_all.register_autograd(_a2a_bwd, setup_context=_a2a_setup)
 
 
+# ----------------------------------------------------------------------------- fused K3 + K2
+@torch.library.custom_op("autosp::attention_a2a", mutates_args=(), device_types="cuda")
+def attention_a2a(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: float, causal: bool,
+                  group: str) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Attention over the full sequence on the local heads whose epilogue pushes every
+    output row to its token owner (the head->seq all-to-all, sp_pass.py:172-195, fused
+    into the producing kernel).  Returns (o_tokens [b, H, s/P, d] token-major = the
+    all-to-all output, o_heads [b, h/P, s, d] (kept for the backward), lse)."""
+    st = sp_dist.lookup(group)
+    P, pool = st.world, st.pool
+    b, hl, S, d = q.shape
+    o_head = torch.empty((b, hl, S, d), dtype=q.dtype, device=q.device)
+    lse = torch.empty((b, hl, S), dtype=torch.float32, device=q.device)
+    shape, strides = _out_geometry(o_head, HEAD_TO_SEQ_DIR, P)
+    off, base = pool.alloc(math.prod(shape) * q.element_size())
+    o_tok = base.view(q.dtype).as_strided(shape, strides)
+    epoch = pool.next_epoch()
+    kernels.attn_fwd_push(q, k, v, o_head, lse, scale, causal, P, st.rank, off,
+                          (strides[0], strides[2], strides[1]), pool.region_ptrs,
+                          pool.flag_ptrs, epoch)
+    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, off)
+    return o_tok, o_head, lse
+
+
+@attention_a2a.register_fake
+def _attention_a2a_fake(q, k, v, scale, causal, group):
+    P = sp_dist.lookup(group).world
+    b, hl, S, d = q.shape
+    shape, strides = _out_geometry(q, HEAD_TO_SEQ_DIR, P)
+    return (q.new_empty_strided(shape, strides), q.new_empty((b, hl, S, d)),
+            q.new_empty((b, hl, S), dtype=torch.float32))
+
+
+def _attn_a2a_setup(ctx, inputs, output):
+    q, k, v, scale, causal, group = inputs
+    _, o_head, lse = output
+    ctx.save_for_backward(q, k, v, o_head, lse)
+    ctx.scale, ctx.causal, ctx.group = scale, causal, group
+
+
+def _attn_a2a_bwd(ctx, d_otok, d_ohead, d_lse):
+    q, k, v, o_head, lse = ctx.saved_tensors
+    (do,) = all_to_all([d_otok], SEQ_TO_HEAD_DIR, ctx.group)  # gradient of the fused a2a
+    if d_ohead is not None:
+        do = do + d_ohead
+    dq, dk, dv = attention_backward(do, q, k, v, o_head, lse, ctx.scale, ctx.causal)
+    return dq, dk, dv, None, None, None
+
+
+attention_a2a.register_autograd(_attn_a2a_bwd, setup_context=_attn_a2a_setup)
+
+FUSE_OUTPUT_A2A = True  # attention epilogue pushes O (K3 + K2 in one kernel)
+
+
 def ulysses_attention(q, k, v, group: str, is_causal=True, scale=None):
     """The Ulysses attention block the auto_sp pass substitutes for SDPA
     (sp_pass.py:172-195): a2a seq->head of (q, k, v) in one launch, causal attention over
@@ -187,8 +243,14 @@ def ulysses_attention(q, k, v, group: str, is_causal=True, scale=None):
         vh = kh
     else:
         qh, kh, vh = all_to_all([q, k, v], SEQ_TO_HEAD_DIR, group)
-    oh = _sdpa(qh, kh, vh, is_causal, scale)
-    (o,) = all_to_all([oh], HEAD_TO_SEQ_DIR, group)
+    if FUSE_OUTPUT_A2A:
+        if not is_causal:
+            raise ValidationError("auto_sp attention is causal (reference mask, executor.py:62-65)")
+        sc = 1.0 / math.sqrt(qh.shape[-1]) if scale is None else float(scale)
+        o = attention_a2a(qh, kh, vh, sc, True, group)[0]
+    else:
+        oh = _sdpa(qh, kh, vh, is_causal, scale)
+        (o,) = all_to_all([oh], HEAD_TO_SEQ_DIR, group)
     return o if dt is None else o.to(dt)
 
 

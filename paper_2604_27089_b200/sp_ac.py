@@ -60,11 +60,13 @@ def _opname(n: fx.Node) -> str:
 
 
 def is_autosp_collective(n: fx.Node) -> bool:
-    return n.op == "call_function" and _opname(n) == "autosp::all_to_all"
+    return n.op == "call_function" and _opname(n) in ("autosp::all_to_all",
+                                                      "autosp::attention_a2a")
 
 
 def is_autosp_attention(n: fx.Node) -> bool:
-    return n.op == "call_function" and _opname(n) == "autosp::attention"
+    return n.op == "call_function" and _opname(n) in ("autosp::attention",
+                                                      "autosp::attention_a2a")
 
 
 def _is_matmul(n: fx.Node) -> bool:

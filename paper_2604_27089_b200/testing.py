@@ -76,6 +76,12 @@ def enable_cpu_lowering() -> None:
             outs.append(out)
         return outs
 
+    @torch.library.register_kernel("autosp::attention_a2a", "cpu")
+    def _attention_a2a_cpu(q, k, v, scale, causal, group):
+        o, lse = _attention_cpu(q, k, v, scale, causal)
+        (ot,) = _all_to_all_cpu([o], ops.HEAD_TO_SEQ_DIR, group)
+        return ot, o, lse
+
     _ENABLED = True
 
 
