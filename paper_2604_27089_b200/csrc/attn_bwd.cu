@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
             wait_q(t + 1);
             if (lane == 0) BWD_TRACE(11, t);
             issue_s(t + 1);
+            if (lane == 0) BWD_TRACE(13, t);
           }
         } else {
           // dQ(t-1) lives in the dP columns: dP(t) waits for its drain
@@ -394,6 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       const bool masked = (p.causal && (q0 < k0 + BK)) || (k0 + BK > p.S) || (q0 + BQ > p.S);
       const int col_lo = p.causal ? key - q0 : -1;  // col < col_lo -> masked (q < key)
       const int col_hi = min(p.S - q0, BQ);          // col >= col_hi -> masked (q >= S)
+      if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(12, t);
       mbar_wait(s_full + (t % C::NSB), (t / C::NSB) & 1);
       if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(5, t);
       tc_fence_after();

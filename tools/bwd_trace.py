@@ -20,7 +20,7 @@ lib.autosp_debug_set_bwd_trace(None)
 t = buf.view(16, 64).cpu()
 names = ["mma:dq_empty", "mma:dP_issued", "mma:p_ready", "mma:ds_ready", "mma:dQ_issued",
          "sm:s_full", "sm:p_arrive", "sm:dp_full", "sm:ds_arrive", "dr:dq_full", "dr:dq_empty",
-         "mma:q_next"]
+         "mma:q_next", "sm:loop_top", "mma:s_issued"]
 base = int(t[1, 0])
 for step in range(8, 16):
     row = "  ".join(f"{n}={int(t[i, step]) - base:8d}" for i, n in enumerate(names) if int(t[i, step]) > 0)
