@@ -79,7 +79,8 @@ def _ulysses_rank(st, x_full, do_full, results, r, P, causal=True):
     results[r] = (o.detach(), q.grad, k.grad, v.grad)
 
 
-@pytest.mark.parametrize("P,hq,hkv,d", [(2, 4, 2, 64), (4, 8, 4, 128), (8, 8, 8, 32)])
+@pytest.mark.parametrize("P,hq,hkv,d", [(2, 4, 2, 64), (4, 8, 4, 128), (8, 8, 8, 32),
+                                       (8, 32, 8, 128)])  # last: BASELINE C5 heads (32/8), SP=8
 def test_ulysses_block_virtual_ranks_one_gpu(P, hq, hkv, d):
     """P virtual ranks (threads + streams) run the REAL push kernels, epoch flags and
     pool allocator concurrently on one GPU; forward and backward must equal the
