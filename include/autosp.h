@@ -161,7 +161,8 @@ AUTOSP_API int autosp_attn_fwd_push(autosp_attn_tensor q, autosp_attn_tensor k,
                     int hkv, int s, int d, float scale, int causal,
                     const autosp_push_spec* push, void* stream);
 
-/* fp32 workspace the backward needs: dq accumulator [b, hq, s, d] + delta [b, hq, s] */
+/* fp32 workspace the backward needs: dq accumulator [b, hq, s, d] + delta [b, hq, s]
+ * + -lse*log2(e) [b, hq, s] */
 AUTOSP_API size_t autosp_attn_bwd_workspace_bytes(int b, int hq, int s, int d);
 AUTOSP_API int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
                     autosp_attn_tensor o, autosp_attn_tensor d_o, const float* lse,

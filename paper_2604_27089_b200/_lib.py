@@ -5,13 +5,14 @@ missing every hot-path op raises ExtensionMissingError."""
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from .errors import (CudaError, ExtensionMissingError, SeqcompError, UnsupportedError,
                      ValidationError)
 
-LIB_PATH = Path(__file__).resolve().parent / "libautosp.so"
+LIB_PATH = Path(os.environ.get("AUTOSP_LIB") or Path(__file__).resolve().parent / "libautosp.so")
 ABI_VERSION = 1
 IPC_HANDLE_BYTES = 64
 MAX_WORLD = 8

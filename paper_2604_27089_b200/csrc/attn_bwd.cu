@@ -32,6 +32,10 @@
 extern "C" void autosp_set_error(const char* fmt, ...);
 int autosp_check_attn_tensor(const autosp_attn_tensor& t, const char* name);
 
+#ifndef AUTOSP_BWD_EMU
+#define AUTOSP_BWD_EMU 2  // exps per 8 on the FMA pipe for d <= 64 (tools/emu sweep)
+#endif
+
 namespace autosp {
 namespace bwd {
 long long* g_bwd_trace = nullptr;  // set by autosp_debug_set_bwd_trace (tools only)
@@ -72,7 +76,7 @@ struct Cfg {
   // S^T buffers in TMEM: two (S(t+1) overlaps the softmax of t) when d <= 64
   static constexpr int NSB = D == 128 ? 1 : 2;
   // exps per 8 done on the FMA pipe (part 1 is MUFU-bound at 16 exp/clk/SM)
-  static constexpr int kEmuPer8 = D == 128 ? 1 : 2;
+  static constexpr int kEmuPer8 = D == 128 ? 1 : AUTOSP_BWD_EMU;
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = TILE;
   static constexpr int Q_OFF = 2 * TILE;                       // Q[st]
@@ -98,7 +102,7 @@ struct Params {
   int lse_tma;         // lse/delta rows staged by TMA with Q/dO (needs S % 4 == 0)
   long long* trace;    // debug timeline (nullptr in production): [16 events][kTraceSteps]
   float* dqacc;        // [B, Hq, S, D] fp32 accumulator (red.global.add from the drain)
-  const float* lse;    // [B, Hq, S]
+  const float* lse;    // [B, Hq, S]  -lse * log2(e) (written by bwd_pre)
   const float* delta;  // [B, Hq, S]
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
@@ -370,9 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t dp_addr = tmem + lane_base + C::DP_COL;
     uint8_t* ds_row = smem + C::DS_OFF + half * (128 * 128) + row * 128;
-    const float LOG2E = 1.4426950408889634f;
     const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
-    const uint64_t nl2e = f2_pack(-LOG2E, -LOG2E);
     const bool row_dead = key >= p.S;
     for (int t = 0; t < T; ++t) {
       const int head = kvh * group + t / per_head;
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
               const uint64_t lz = h ? f2_pack(l.z, l.w) : f2_pack(l.x, l.y);
               const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(sr[2 * c]),
                                                  __uint_as_float(sr[2 * c + 1])),
-                                         sl2, f2_mul(lz, nl2e));
+                                         sl2, lz);  // lz = -lse*log2(e) (bwd_pre)
               float e0, e1;
               if (!decltype(kMasked)::value && (c & 7) >= 8 - C::kEmuPer8) {
                 f2_unpack(f2_exp2_poly(x2), e0, e1);  // FMA pipe (offloads MUFU)
@@ -489,8 +491,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int unit = cc * 4 + u;  // 16-byte unit within this half's 128 B row
-            *reinterpret_cast<uint4*>(ds_row + ((unit ^ (row & 7)) << 4)) =
-                make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+            sts128(ds_row + ((unit ^ (row & 7)) << 4),
+                   make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
           }
         }
       };
@@ -571,8 +573,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            *reinterpret_cast<uint4*>(srow + ((u ^ (row & 7)) << 4)) =
-                make_uint4(v[cc][4 * u], v[cc][4 * u + 1], v[cc][4 * u + 2], v[cc][4 * u + 3]);
+            sts128(srow + ((u ^ (row & 7)) << 4),
+                   make_uint4(v[cc][4 * u], v[cc][4 * u + 1], v[cc][4 * u + 2], v[cc][4 * u + 3]));
           fence_proxy_async_smem();
           named_bar_sync(2, 128);
           if (leader) {
@@ -811,9 +813,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
     const uint32_t s_addr = tmem + lane_base + TM::S;
     const uint32_t dp_addr = tmem + lane_base + TM::DP;
     uint8_t* ds_row = smem + C::DS_OFF + (g >> 1) * (128 * 128) + row * 128;
-    const float LOG2E = 1.4426950408889634f;
     const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
-    const uint64_t nl2e = f2_pack(-LOG2E, -LOG2E);
     const bool row_dead = key >= p.S;
     for (int t = 0; t < T; ++t) {
       const int head = kvh * group + t / per_head;
@@ -852,7 +852,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
               const uint64_t lz = h ? f2_pack(l.z, l.w) : f2_pack(l.x, l.y);
               const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(sr[2 * c]),
                                                  __uint_as_float(sr[2 * c + 1])),
-                                         sl2, f2_mul(lz, nl2e));
+                                         sl2, lz);  // lz = -lse*log2(e) (bwd_pre)
               float e0, e1;
               if (!decltype(kMasked)::value && (c & 7) >= 8 - C::kEmuPer8) {
                 f2_unpack(f2_exp2_poly(x2), e0, e1);
@@ -912,8 +912,8 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int unit = (g & 1) * 4 + u;
-          *reinterpret_cast<uint4*>(ds_row + ((unit ^ (row & 7)) << 4)) =
-              make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+          sts128(ds_row + ((unit ^ (row & 7)) << 4),
+                 make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
         }
       }
       if (threadIdx.x == 0) BWD_TRACE(13, t);
@@ -981,8 +981,8 @@ __global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __gr
         uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          *reinterpret_cast<uint4*>(srow + ((u ^ (row & 7)) << 4)) =
-              make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+          sts128(srow + ((u ^ (row & 7)) << 4),
+                 make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]));
         fence_proxy_async_smem();
         named_bar_sync(2, 128);
         if (leader) {
@@ -1007,12 +1007,15 @@ struct PrePost {
   int64_t o_sb, o_sh, o_ss, do_sb, do_sh, do_ss, dq_sb, dq_sh, dq_ss;
   float* dqacc;
   float* delta;
+  const float* lse;  // forward LSE (natural log)
+  float* nlse2;      // -lse * log2(e): the exp2 argument offset the softmax-grad warps use
   int Hq, S, D;
   int64_t rows;
   float scale;
 };
 
-// delta[row] = sum_d dO*O ; dqacc[row, :] = 0.  lanes_per_row = D/8 (one 16B vector each).
+// delta[row] = sum_d dO*O ; nlse2[row] = -lse[row] * log2(e) ; dqacc[row, :] = 0.
+// lanes_per_row = D/8 (one 16B vector each).
 __global__ void bwd_pre_kernel(const __grid_constant__ PrePost a) {
   const int lpr = a.D / 8;
   const int rpw = 32 / lpr;
@@ -1043,7 +1046,10 @@ __global__ void bwd_pre_kernel(const __grid_constant__ PrePost a) {
     z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   for (int off = lpr / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (row < a.rows && sub == 0) a.delta[row] = acc;
+  if (row < a.rows && sub == 0) {
+    a.delta[row] = acc;
+    a.nlse2[row] = -a.lse[row] * 1.4426950408889634f;
+  }
 }
 
 __global__ void bwd_post_kernel(const __grid_constant__ PrePost a) {
@@ -1103,6 +1109,7 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   using C = Cfg<D>;
   float* dqacc = static_cast<float*>(ws);
   float* delta = dqacc + (size_t)B * Hq * S * D;
+  float* nlse2 = delta + (size_t)B * Hq * S;
   PrePost a{};
   a.o = static_cast<const __nv_bfloat16*>(o.ptr);
   a.d_o = static_cast<const __nv_bfloat16*>(d_o.ptr);
@@ -1112,6 +1119,8 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   a.dq_sb = dq.stride_b; a.dq_sh = dq.stride_h; a.dq_ss = dq.stride_s;
   a.dqacc = dqacc;
   a.delta = delta;
+  a.lse = lse;
+  a.nlse2 = nlse2;
   a.Hq = Hq;
   a.S = S;
   a.D = D;
@@ -1133,13 +1142,13 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
             make_map_bhsd(&p.tm_v, v.ptr, B, Hkv, S, D, v.stride_b, v.stride_h, v.stride_s,
                           C::CE, 128, C::SW) &&
             make_map_f32_3d(&p.tm_dqacc, dqacc, B * Hq, S, D);
-  p.lse_tma = (S % 4 == 0) && make_map_rows_f32(&p.tm_lse, lse, B * Hq, S) &&
+  p.lse_tma = (S % 4 == 0) && make_map_rows_f32(&p.tm_lse, nlse2, B * Hq, S) &&
               make_map_rows_f32(&p.tm_dlt, delta, B * Hq, S);
   if (!ok) {
     autosp_set_error("attn_bwd: cuTensorMapEncodeTiled failed (alignment/strides?)");
     return AUTOSP_ERR_VALIDATION;
   }
-  p.lse = lse;
+  p.lse = nlse2;  // the softmax-grad warps read -lse*log2(e)
   p.delta = delta;
   p.dqacc = dqacc;
   p.trace = g_bwd_trace;
@@ -1188,7 +1197,7 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
 }  // namespace autosp
 
 extern "C" size_t autosp_attn_bwd_workspace_bytes(int b, int hq, int s, int d) {
-  return (size_t)b * hq * s * (d + 1) * sizeof(float);
+  return (size_t)b * hq * s * (d + 2) * sizeof(float);  // dQ acc + delta + -lse*log2(e)
 }
 
 extern "C" int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,

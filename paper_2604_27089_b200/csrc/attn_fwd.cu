@@ -26,6 +26,10 @@
 
 extern "C" void autosp_set_error(const char* fmt, ...);
 
+#ifndef AUTOSP_FWD_EMU
+#define AUTOSP_FWD_EMU 3  // exps per 8 on the FMA pipe for d <= 64
+#endif
+
 namespace autosp {
 namespace fwd {
 
@@ -50,7 +54,7 @@ struct Cfg {
   static constexpr int kStages = D == 128 ? 2 : (D == 64 ? 3 : 4);
   // exps per 8 computed by the FMA-pipe polynomial instead of MUFU (MUFU is the
   // bottleneck when the tile's MMA work is small: d = 32 / 64)
-  static constexpr int kEmuPer8 = D == 128 ? 2 : 3;
+  static constexpr int kEmuPer8 = D == 128 ? 2 : AUTOSP_FWD_EMU;
   static constexpr int LAYOUT = SW == 128 ? 2 : (SW == 64 ? 4 : 6);
   static constexpr int SBO = 8 * SW;  // 8-row swizzle atom
   // smem: Q[2] | K[kStages] | V[kStages] | barriers

@@ -46,6 +46,13 @@ AUTOSP_DEV void reg_dealloc() {  // whole warpgroup
 
 // explicit shared-memory vector load (a generic-pointer load of smem data compiles to a
 // generic LD with extra address-space resolution latency)
+// 16-byte shared store through an explicit .shared address (a generic pointer into smem
+// compiles to ST.E, the generic path)
+AUTOSP_DEV void sts128(const void* p, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 AUTOSP_DEV float4 lds128(const void* p) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
