@@ -186,6 +186,20 @@ AUTOSP_API int autosp_swiglu_bwd(const void* gu, const void* dout, void* dgu, in
 AUTOSP_API int autosp_rope(const void* x, void* y, int b, int s, int h, int d, int64_t xsb,
                            int64_t xss, int64_t xsh, int64_t ysb, int64_t yss, int64_t ysh,
                            const float* pos, float theta, int inverse, void* stream);
+/* Segmented RoPE (rotate-half, positions pos[s], theta; inverse = rotate by -angle):
+ * each segment maps a [b, s, heads, d] strided view src to dst, rotating when `rotate`
+ * and copying otherwise.  Forward: the packed QKV projection output -> q, k (rotated), v;
+ * backward: dq, dk (inverse rotation), dv -> the packed QKV gradient.  One launch. */
+typedef struct autosp_rope_segment {
+  const void* src;
+  void* dst;
+  int64_t src_stride_b, src_stride_s, src_stride_h;  /* elements */
+  int64_t dst_stride_b, dst_stride_s, dst_stride_h;
+  int heads, rotate;
+} autosp_rope_segment;
+AUTOSP_API int autosp_rope_segments(const autosp_rope_segment* segs, int nseg, int b, int s,
+                                    int d, const float* pos, float theta, int inverse,
+                                    void* stream);
 AUTOSP_API int autosp_ce_fwd(const void* logits, const int64_t* labels, float* lse, float* loss,
                              int64_t rows, int64_t vocab, int64_t ld, void* stream);
 AUTOSP_API int autosp_ce_bwd(void* logits, const int64_t* labels, const float* lse, float g,

@@ -36,6 +36,14 @@ class AttnTensor(C.Structure):
                 ("stride_s", C.c_int64)]
 
 
+class RopeSegment(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p),
+                ("src_stride_b", C.c_int64), ("src_stride_s", C.c_int64),
+                ("src_stride_h", C.c_int64), ("dst_stride_b", C.c_int64),
+                ("dst_stride_s", C.c_int64), ("dst_stride_h", C.c_int64),
+                ("heads", C.c_int), ("rotate", C.c_int)]
+
+
 class PushSpec(C.Structure):
     _fields_ = [("world", C.c_int), ("rank", C.c_int), ("dst_offset", C.c_int64),
                 ("dst_stride_b", C.c_int64), ("dst_stride_s", C.c_int64),
@@ -74,6 +82,8 @@ EXPORTS = {
                           [C.c_void_p]),
     "autosp_rope": (C.c_int, [C.c_void_p, C.c_void_p] + [C.c_int] * 4 + [C.c_int64] * 6 +
                     [C.c_void_p, C.c_float, C.c_int, C.c_void_p]),
+    "autosp_rope_segments": (C.c_int, [C.POINTER(RopeSegment), C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_void_p, C.c_float, C.c_int, C.c_void_p]),
     "autosp_ce_fwd": (C.c_int, [C.c_void_p] * 4 + [C.c_int64] * 3 + [C.c_void_p]),
     "autosp_ce_bwd": (C.c_int, [C.c_void_p] * 3 + [C.c_float] + [C.c_int64] * 3 + [C.c_void_p]),
     "autosp_debug_set_bwd_trace": (C.c_int, [C.c_void_p]),

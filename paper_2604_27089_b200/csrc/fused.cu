@@ -127,6 +127,74 @@ __global__ void rope_kernel(const __grid_constant__ RopeArgs a) {
   }
 }
 
+// Segmented RoPE: up to 3 segments (q, k rotated; v copied) in ONE launch -- the split
+// of the packed QKV projection output into the attention operands (forward) and the
+// assembly of the packed QKV gradient from dq/dk/dv (backward, inverse rotation), with
+// no zero-filled slice_backward buffers and no adds.  One thread = (token, 8 rotation
+// pairs) over every head of every segment; sincos once per (token, pair).
+struct RopeSeg {
+  const __nv_bfloat16* src;
+  __nv_bfloat16* dst;
+  int64_t ssb, sss, ssh, dsb, dss, dsh;
+  int heads, rotate;
+};
+struct RopeSegArgs {
+  RopeSeg seg[3];
+  int nseg;
+  const float* pos;
+  int b, s, d;
+  float log2_theta;
+  int inverse;
+};
+
+__global__ void rope_seg_kernel(const __grid_constant__ RopeSegArgs a) {
+  const int half = a.d / 2;
+  const int vpt = half / 8;
+  const int64_t total = (int64_t)a.b * a.s * vpt;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(i % vpt);
+    const int64_t bt = i / vpt;
+    const int t = (int)(bt % a.s);
+    const int bi = (int)(bt / a.s);
+    const float p = a.pos[t];
+    float cs[8], sn[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int j = v * 8 + k;
+      const float inv_freq = exp2f(-(2.f * j / a.d) * a.log2_theta);
+      sincosf(p * inv_freq, &sn[k], &cs[k]);
+      if (a.inverse) sn[k] = -sn[k];
+    }
+#pragma unroll
+    for (int g = 0; g < 3; ++g) {
+      if (g >= a.nseg) break;
+      const RopeSeg& S = a.seg[g];
+      for (int hh = 0; hh < S.heads; ++hh) {
+        const __nv_bfloat16* xr = S.src + (int64_t)bi * S.ssb + (int64_t)t * S.sss + (int64_t)hh * S.ssh;
+        __nv_bfloat16* yr = S.dst + (int64_t)bi * S.dsb + (int64_t)t * S.dss + (int64_t)hh * S.dsh;
+        const uint4 r1 = *reinterpret_cast<const uint4*>(xr + v * 8);
+        const uint4 r2 = *reinterpret_cast<const uint4*>(xr + half + v * 8);
+        if (!S.rotate) {
+          *reinterpret_cast<uint4*>(yr + v * 8) = r1;
+          *reinterpret_cast<uint4*>(yr + half + v * 8) = r2;
+          continue;
+        }
+        float x1[8], x2[8], y1[8], y2[8];
+        unpack8(r1, x1);
+        unpack8(r2, x2);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          y1[k] = x1[k] * cs[k] - x2[k] * sn[k];
+          y2[k] = x2[k] * cs[k] + x1[k] * sn[k];
+        }
+        *reinterpret_cast<uint4*>(yr + v * 8) = pack8(y1);
+        *reinterpret_cast<uint4*>(yr + half + v * 8) = pack8(y2);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- cross entropy
 // one CTA per row: online max/sum over the bf16 logits row, target logit gathered.
 constexpr int kCeThreads = 512;
@@ -272,6 +340,39 @@ extern "C" int autosp_rope(const void* x, void* y, int b, int s, int h, int d, i
   return launched("rope");
 }
 
+extern "C" int autosp_rope_segments(const autosp_rope_segment* segs, int nseg, int b, int s,
+                                    int d, const float* pos, float theta, int inverse,
+                                    void* stream) {
+  if (!segs || nseg < 1 || nseg > 3 || !pos || d % 16 || theta <= 1.f) {
+    autosp_set_error("rope_segments: 1-3 segments, d multiple of 16, theta > 1");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  RopeSegArgs a{};
+  for (int g = 0; g < nseg; ++g) {
+    const autosp_rope_segment& G = segs[g];
+    if (!G.src || !G.dst || !al16(G.src) || !al16(G.dst) || G.src_stride_b % 8 ||
+        G.src_stride_s % 8 || G.src_stride_h % 8 || G.dst_stride_b % 8 || G.dst_stride_s % 8 ||
+        G.dst_stride_h % 8 || G.heads < 0) {
+      autosp_set_error("rope_segments: segment %d needs 16B-aligned views", g);
+      return AUTOSP_ERR_VALIDATION;
+    }
+    a.seg[g] = RopeSeg{static_cast<const __nv_bfloat16*>(G.src), static_cast<__nv_bfloat16*>(G.dst),
+                       G.src_stride_b, G.src_stride_s, G.src_stride_h, G.dst_stride_b,
+                       G.dst_stride_s, G.dst_stride_h, G.heads, G.rotate};
+  }
+  if ((int64_t)b * s == 0) return AUTOSP_OK;
+  a.nseg = nseg;
+  a.pos = pos;
+  a.b = b;
+  a.s = s;
+  a.d = d;
+  a.log2_theta = log2f(theta);
+  a.inverse = inverse;
+  const int64_t work = (int64_t)b * s * (d / 16);
+  rope_seg_kernel<<<grid_for(work, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return launched("rope_segments");
+}
+
 extern "C" int autosp_ce_fwd(const void* logits, const int64_t* labels, float* lse, float* loss,
                              int64_t rows, int64_t vocab, int64_t ld, void* stream) {
   if (!logits || !labels || !lse || !loss || ld % 8 || !al16(logits) || vocab < 1) {
@@ -301,6 +402,7 @@ int autosp_preload_fused() {
   cudaFuncGetAttributes(&a, swiglu_fwd_kernel);
   cudaFuncGetAttributes(&a, swiglu_bwd_kernel);
   cudaFuncGetAttributes(&a, rope_kernel);
+  cudaFuncGetAttributes(&a, rope_seg_kernel);
   cudaFuncGetAttributes(&a, ce_fwd_kernel);
   cudaFuncGetAttributes(&a, ce_bwd_kernel);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;

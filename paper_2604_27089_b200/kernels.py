@@ -279,6 +279,29 @@ def rope(x: torch.Tensor, pos: torch.Tensor, theta: float, inverse: bool = False
     return y
 
 
+def rope_segments(pairs: list[tuple[torch.Tensor, torch.Tensor, bool]], pos: torch.Tensor,
+                  theta: float, inverse: bool = False) -> None:
+    """One launch over up to 3 (src, dst, rotate) [b, s, h, d] view pairs (d contiguous):
+    dst = RoPE(src) when rotate else src."""
+    segs = []
+    b, s, _, d = pairs[0][0].shape
+    for src, dst, rot in pairs:
+        for t, n in ((src, "src"), (dst, "dst")):
+            if t.stride(-1) != 1 or t.dtype != torch.bfloat16 or not t.is_cuda:
+                raise ValidationError(f"rope_segments: {n} must be a CUDA bf16 view, d contiguous")
+        if src.shape != dst.shape or src.shape[0] != b or src.shape[1] != s:
+            raise ValidationError("rope_segments: src/dst shape mismatch")
+        segs.append(_lib.RopeSegment(src.data_ptr(), dst.data_ptr(), src.stride(0), src.stride(1),
+                                     src.stride(2), dst.stride(0), dst.stride(1), dst.stride(2),
+                                     src.shape[2], int(rot)))
+    arr = (_lib.RopeSegment * len(segs))(*segs)
+    pos = pos.to(torch.float32).contiguous()
+    rc = _lib.load().autosp_rope_segments(arr, len(segs), b, s, d, pos.data_ptr(), float(theta),
+                                          int(inverse), _stream())
+    _lib.check(rc, "rope_segments")
+    LOG.end("rope", None, 1)
+
+
 def ce_fwd(logits: torch.Tensor, labels: torch.Tensor):
     """Row-wise (lse, loss) of bf16 logits [n, V] (leading dim may exceed V)."""
     n, V = logits.shape

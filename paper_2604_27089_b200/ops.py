@@ -38,13 +38,19 @@ ATTN_DTYPE: torch.dtype | None = torch.bfloat16
 @torch.library.custom_op("autosp::attention", mutates_args=(), device_types="cuda")
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: float,
               causal: bool) -> tuple[torch.Tensor, torch.Tensor]:
-    return kernels.attn_fwd(q, k, v, causal=causal, scale=scale)
+    # O is written token-major ([b, s, h, d] memory, returned as the [b, h, s, d] view):
+    # the caller's transpose(1, 2).reshape(b, s, h*d) before the O projection is then a
+    # free view instead of a copy of the whole output
+    b, h, s, d = q.shape
+    o = torch.empty((b, s, h, d), dtype=q.dtype, device=q.device).transpose(1, 2)
+    return kernels.attn_fwd(q, k, v, causal=causal, scale=scale, out=o)
 
 
 @attention.register_fake
 def _attention_fake(q, k, v, scale, causal):
     b, h, s, d = q.shape
-    return q.new_empty((b, h, s, d)), q.new_empty((b, h, s), dtype=torch.float32)
+    return (q.new_empty_strided((b, h, s, d), (s * h * d, d, h * d, 1)),
+            q.new_empty((b, h, s), dtype=torch.float32))
 
 
 @torch.library.custom_op("autosp::attention_backward", mutates_args=(), device_types="cuda")
@@ -313,3 +319,57 @@ def _rope_bwd(ctx, dy):
 
 
 rope.register_autograd(_rope_bwd, setup_context=_rope_setup)
+
+
+# QKV split + RoPE as one op: forward = one launch producing q, k (rotated) and v from the
+# packed projection output; backward = one launch assembling the packed QKV gradient
+# (replaces 2 rope launches + 3 zero-filled slice_backward buffers + 2 adds).
+@torch.library.custom_op("autosp::qkv_rope", mutates_args=(), device_types="cuda")
+def qkv_rope(qkv: torch.Tensor, pos: torch.Tensor, theta: float, hq: int,
+             hkv: int) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    b, s, _, d = qkv.shape
+    q = torch.empty((b, s, hq, d), dtype=qkv.dtype, device=qkv.device)
+    k = torch.empty((b, s, hkv, d), dtype=qkv.dtype, device=qkv.device)
+    v = torch.empty((b, s, hkv, d), dtype=qkv.dtype, device=qkv.device)
+    kernels.rope_segments([(qkv[:, :, :hq], q, True), (qkv[:, :, hq:hq + hkv], k, True),
+                           (qkv[:, :, hq + hkv:], v, False)], pos, theta, False)
+    return q, k, v
+
+
+@qkv_rope.register_fake
+def _qkv_rope_fake(qkv, pos, theta, hq, hkv):
+    b, s, _, d = qkv.shape
+    return (qkv.new_empty((b, s, hq, d)), qkv.new_empty((b, s, hkv, d)),
+            qkv.new_empty((b, s, hkv, d)))
+
+
+@torch.library.custom_op("autosp::qkv_rope_backward", mutates_args=(), device_types="cuda")
+def qkv_rope_backward(dq: torch.Tensor, dk: torch.Tensor, dv: torch.Tensor, pos: torch.Tensor,
+                      theta: float) -> torch.Tensor:
+    b, s, hq, d = dq.shape
+    hkv = dk.shape[2]
+    dqkv = torch.empty((b, s, hq + 2 * hkv, d), dtype=dq.dtype, device=dq.device)
+    kernels.rope_segments([(dq, dqkv[:, :, :hq], True), (dk, dqkv[:, :, hq:hq + hkv], True),
+                           (dv, dqkv[:, :, hq + hkv:], False)], pos, theta, True)
+    return dqkv
+
+
+@qkv_rope_backward.register_fake
+def _qkv_rope_backward_fake(dq, dk, dv, pos, theta):
+    b, s, hq, d = dq.shape
+    return dq.new_empty((b, s, hq + 2 * dk.shape[2], d))
+
+
+def _qkv_rope_setup(ctx, inputs, output):
+    _, pos, theta, _, _ = inputs
+    ctx.save_for_backward(pos)
+    ctx.theta = theta
+
+
+def _qkv_rope_bwd(ctx, dq, dk, dv):
+    (pos,) = ctx.saved_tensors
+    fix = lambda t: t if t.stride(-1) == 1 else t.contiguous()
+    return qkv_rope_backward(fix(dq), fix(dk), fix(dv), pos, ctx.theta), None, None, None, None
+
+
+qkv_rope.register_autograd(_qkv_rope_bwd, setup_context=_qkv_rope_setup)

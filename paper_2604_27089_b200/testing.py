@@ -39,7 +39,8 @@ def enable_cpu_lowering() -> None:
         sc, ke, ve = _attn_math(q, k, v, scale, causal)
         lse = torch.logsumexp(sc, dim=-1)
         o = torch.softmax(sc, dim=-1) @ ve
-        return o.contiguous(), lse.float()
+        # same memory layout as the CUDA op (token-major, see ops.attention)
+        return o.transpose(1, 2).contiguous().transpose(1, 2), lse.float()
 
     @torch.library.register_kernel("autosp::attention_backward", "cpu")
     def _attention_backward_cpu(do, q, k, v, o, lse, scale, causal):

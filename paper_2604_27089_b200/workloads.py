@@ -156,14 +156,13 @@ class LlamaBlock(nn.Module):
             from . import ops
             h = F.rms_norm(x, (cfg.d_model,), self.norm1, cfg.eps)
             qkv = (h @ self.wqkv.t()).view(b, s, cfg.hq + 2 * cfg.hkv, hd)
-            q = ops.rope(qkv[:, :, :cfg.hq], pos, cfg.rope_theta, False)
-            k = ops.rope(qkv[:, :, cfg.hq:cfg.hq + cfg.hkv], pos, cfg.rope_theta, False)
+            q, k, v = ops.qkv_rope(qkv, pos, cfg.rope_theta, cfg.hq, cfg.hkv)
         else:
             h = rmsnorm(x, self.norm1, cfg.eps)
             qkv = (h @ self.wqkv.t()).view(b, s, cfg.hq + 2 * cfg.hkv, hd)
             q = rope(qkv[:, :, :cfg.hq], cos, sin)
             k = rope(qkv[:, :, cfg.hq:cfg.hq + cfg.hkv], cos, sin)
-        v = qkv[:, :, cfg.hq + cfg.hkv:]
+            v = qkv[:, :, cfg.hq + cfg.hkv:]
         o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
                                            v.transpose(1, 2), is_causal=True, enable_gqa=True)
         x = x + o.transpose(1, 2).reshape(b, s, cfg.hq * hd) @ self.wo.t()

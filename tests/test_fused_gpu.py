@@ -123,3 +123,25 @@ def test_fused_llama_block_matches_unfused():
     assert _rel(xa.grad, xb.grad) < 5e-2
     for pa, pb in zip(a.parameters(), bblk.parameters()):
         assert _rel(pa.grad, pb.grad) < 5e-2
+
+
+@pytest.mark.parametrize("b,s,hq,hkv,d,off", [(1, 64, 4, 2, 64, 0), (2, 40, 8, 2, 128, 4096),
+                                               (1, 256, 32, 8, 64, 131072)])
+def test_qkv_rope_split_and_packed_gradient(b, s, hq, hkv, d, off):
+    """autosp::qkv_rope = split of the packed QKV projection + RoPE of q/k in one launch;
+    its backward assembles the packed gradient (inverse rotation of dq/dk, dv copied)."""
+    from paper_2604_27089_b200 import ops
+    theta = 500000.0
+    qkv = torch.randn(b, s, hq + 2 * hkv, d, device="cuda").bfloat16().requires_grad_(True)
+    pos = torch.arange(off, off + s, device="cuda").float()
+    q, k, v = ops.qkv_rope(qkv, pos, theta, hq, hkv)
+    x = qkv.detach()
+    assert _rel(q, _rope_ref(x[:, :, :hq], pos, theta)) < TOL
+    assert _rel(k, _rope_ref(x[:, :, hq:hq + hkv], pos, theta)) < TOL
+    assert torch.equal(v, x[:, :, hq + hkv:])
+    dq, dk, dv = (torch.randn_like(t) for t in (q, k, v))
+    torch.autograd.backward((q, k, v), (dq, dk, dv))
+    g = qkv.grad
+    assert _rel(g[:, :, :hq], _inv_rot(dq, pos, theta)) < TOL
+    assert _rel(g[:, :, hq:hq + hkv], _inv_rot(dk, pos, theta)) < TOL
+    assert torch.equal(g[:, :, hq + hkv:], dv)
