@@ -200,6 +200,17 @@ typedef struct autosp_rope_segment {
 AUTOSP_API int autosp_rope_segments(const autosp_rope_segment* segs, int nseg, int b, int s,
                                     int d, const float* pos, float theta, int inverse,
                                     void* stream);
+/* RMSNorm (reference executor.py:43-45, eps inside the sqrt): y = x * rstd * w over rows
+ * of d (bf16, leading dims in elements), rstd [rows] fp32.  Backward: dx and dw (bf16 [d])
+ * in one pass over (dy, x) plus a column sum of per-CTA partials (workspace). */
+AUTOSP_API int autosp_rms_norm_fwd(const void* x, const void* w, void* y, float* rstd,
+                                   int64_t rows, int d, int64_t ld_x, int64_t ld_y, float eps,
+                                   void* stream);
+AUTOSP_API size_t autosp_rms_norm_bwd_workspace_bytes(int d);
+AUTOSP_API int autosp_rms_norm_bwd(const void* dy, const void* x, const void* w,
+                                   const float* rstd, void* dx, void* dw, void* workspace,
+                                   int64_t rows, int d, int64_t ld_dy, int64_t ld_x,
+                                   int64_t ld_dx, void* stream);
 AUTOSP_API int autosp_ce_fwd(const void* logits, const int64_t* labels, float* lse, float* loss,
                              int64_t rows, int64_t vocab, int64_t ld, void* stream);
 AUTOSP_API int autosp_ce_bwd(void* logits, const int64_t* labels, const float* lse, float g,

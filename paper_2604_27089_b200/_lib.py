@@ -84,6 +84,11 @@ EXPORTS = {
                     [C.c_void_p, C.c_float, C.c_int, C.c_void_p]),
     "autosp_rope_segments": (C.c_int, [C.POINTER(RopeSegment), C.c_int, C.c_int, C.c_int,
                                        C.c_int, C.c_void_p, C.c_float, C.c_int, C.c_void_p]),
+    "autosp_rms_norm_fwd": (C.c_int, [C.c_void_p] * 3 + [C.c_void_p, C.c_int64, C.c_int,
+                                      C.c_int64, C.c_int64, C.c_float, C.c_void_p]),
+    "autosp_rms_norm_bwd_workspace_bytes": (C.c_size_t, [C.c_int]),
+    "autosp_rms_norm_bwd": (C.c_int, [C.c_void_p] * 7 + [C.c_int64, C.c_int, C.c_int64,
+                                      C.c_int64, C.c_int64, C.c_void_p]),
     "autosp_ce_fwd": (C.c_int, [C.c_void_p] * 4 + [C.c_int64] * 3 + [C.c_void_p]),
     "autosp_ce_bwd": (C.c_int, [C.c_void_p] * 3 + [C.c_float] + [C.c_int64] * 3 + [C.c_void_p]),
     "autosp_debug_set_bwd_trace": (C.c_int, [C.c_void_p]),

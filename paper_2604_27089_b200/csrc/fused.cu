@@ -5,6 +5,7 @@
 //   swiglu  out = silu(g) * u over gu = [g | u]        (+ backward)
 //   rope    rotate-half RoPE of q/k heads with positions (rank offset applied by auto_sp)
 //   ce      row-wise log-sum-exp cross entropy over bf16 logits (+ in-place gradient)
+//   rms     RMSNorm forward (+ rstd) and a one-pass backward (dx and the weight gradient)
 #include <cmath>
 #include <cstdint>
 #include <cuda_bf16.h>
@@ -195,6 +196,138 @@ __global__ void rope_seg_kernel(const __grid_constant__ RopeSegArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- RMSNorm
+// y = x * rstd * w, rstd = 1/sqrt(mean(x^2) + eps) (reference executor.py:43-45), one warp
+// per row, 16-byte vectors; the backward computes dx and the weight gradient in ONE pass
+// over (dy, x): per-CTA dw partials accumulated with shared-memory reductions, then a
+// small column-sum kernel (torch's path: two kernels, the weight-gradient one at ~1.6 TB/s).
+constexpr int kNormThreads = 256;
+
+__global__ void __launch_bounds__(kNormThreads) rms_fwd_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+    __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int64_t rows, int d, int64_t ldx,
+    int64_t ldy, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (kNormThreads / 32);
+  const int vpr = d / 8;
+  for (int64_t r = (int64_t)blockIdx.x * (kNormThreads / 32) + (threadIdx.x >> 5); r < rows;
+       r += nw) {
+    const __nv_bfloat16* xr = x + r * ldx;
+    float ss = 0.f;
+    for (int v = lane; v < vpr; v += 32) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(xr + v * 8), f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ss = fmaf(f[k], f[k], ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float rs = rsqrtf(ss / d + eps);
+    __nv_bfloat16* yr = y + r * ldy;
+    for (int v = lane; v < vpr; v += 32) {
+      float f[8], g[8];
+      unpack8(*reinterpret_cast<const uint4*>(xr + v * 8), f);
+      unpack8(*reinterpret_cast<const uint4*>(w + v * 8), g);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) f[k] = f[k] * rs * g[k];
+      *reinterpret_cast<uint4*>(yr + v * 8) = pack8(f);
+    }
+    if (lane == 0) rstd[r] = rs;
+  }
+}
+
+// Each lane owns VPL 16-byte column vectors (v = lane + 32 i) of every row its warp
+// processes and accumulates dy * xhat for them in REGISTERS across rows; the warps of a
+// CTA then combine through shared memory once (shared-memory atomics per element were
+// the bottleneck of the first version).
+template <int VPL>
+__global__ void __launch_bounds__(kNormThreads) rms_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+    const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
+    __nv_bfloat16* __restrict__ dx, float* __restrict__ partial, int64_t rows, int d,
+    int64_t lddy, int64_t ldx, int64_t lddx) {
+  extern __shared__ float dw_s[];  // [d]
+  for (int c = threadIdx.x; c < d; c += kNormThreads) dw_s[c] = 0.f;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t nw = (int64_t)gridDim.x * (kNormThreads / 32);
+  const int vpr = d / 8;
+  float acc[VPL][8];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[i][k] = 0.f;
+  for (int64_t r = (int64_t)blockIdx.x * (kNormThreads / 32) + warp; r < rows; r += nw) {
+    const __nv_bfloat16* xr = x + r * ldx;
+    const __nv_bfloat16* gr = dy + r * lddy;
+    const float rs = rstd[r];
+    float dot = 0.f;  // sum_c dy*w*xhat
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int v = lane + 32 * i;
+      if (v < vpr) {
+        float f[8], g[8], ww[8];
+        unpack8(*reinterpret_cast<const uint4*>(xr + v * 8), f);
+        unpack8(*reinterpret_cast<const uint4*>(gr + v * 8), g);
+        unpack8(*reinterpret_cast<const uint4*>(w + v * 8), ww);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dot = fmaf(g[k] * ww[k], f[k] * rs, dot);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    const float mdot = dot / d;
+    __nv_bfloat16* dxr = dx + r * lddx;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {  // second pass: the row is L1-resident
+      const int v = lane + 32 * i;
+      if (v < vpr) {
+        float f[8], g[8], ww[8], o8[8];
+        unpack8(*reinterpret_cast<const uint4*>(xr + v * 8), f);
+        unpack8(*reinterpret_cast<const uint4*>(gr + v * 8), g);
+        unpack8(*reinterpret_cast<const uint4*>(w + v * 8), ww);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float xh = f[k] * rs;
+          o8[k] = rs * (g[k] * ww[k] - xh * mdot);
+          acc[i][k] = fmaf(g[k], xh, acc[i][k]);
+        }
+        *reinterpret_cast<uint4*>(dxr + v * 8) = pack8(o8);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int v = lane + 32 * i;
+    if (v < vpr)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) atomicAdd(&dw_s[v * 8 + k], acc[i][k]);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += kNormThreads) partial[(int64_t)blockIdx.x * d + c] = dw_s[c];
+}
+
+__global__ void colsum_kernel(const float* __restrict__ partial, int nb, int d,
+                              __nv_bfloat16* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d) return;
+  float acc = 0.f;
+  for (int b = 0; b < nb; ++b) acc += partial[(int64_t)b * d + c];
+  out[c] = __float2bfloat16_rn(acc);
+}
+
+int norm_blocks() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return 2 * sms;
+}
+
 // ---------------------------------------------------------------- cross entropy
 // one CTA per row: online max/sum over the bf16 logits row, target logit gathered.
 constexpr int kCeThreads = 512;
@@ -373,6 +506,63 @@ extern "C" int autosp_rope_segments(const autosp_rope_segment* segs, int nseg, i
   return launched("rope_segments");
 }
 
+extern "C" int autosp_rms_norm_fwd(const void* x, const void* w, void* y, float* rstd,
+                                   int64_t rows, int d, int64_t ld_x, int64_t ld_y, float eps,
+                                   void* stream) {
+  if (!x || !w || !y || !rstd || d % 8 || d < 8 || !al16(x) || !al16(w) || !al16(y) ||
+      ld_x % 8 || ld_y % 8) {
+    autosp_set_error("rms_norm_fwd: d multiple of 8, 16B-aligned rows");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (rows == 0) return AUTOSP_OK;
+  const int64_t warps = rows;
+  rms_fwd_kernel<<<grid_for(warps * 32, kNormThreads), kNormThreads, 0,
+                   static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
+      static_cast<__nv_bfloat16*>(y), rstd, rows, d, ld_x, ld_y, eps);
+  return launched("rms_norm_fwd");
+}
+
+extern "C" size_t autosp_rms_norm_bwd_workspace_bytes(int d) {
+  return (size_t)norm_blocks() * d * sizeof(float);
+}
+
+extern "C" int autosp_rms_norm_bwd(const void* dy, const void* x, const void* w,
+                                   const float* rstd, void* dx, void* dw, void* workspace,
+                                   int64_t rows, int d, int64_t ld_dy, int64_t ld_x,
+                                   int64_t ld_dx, void* stream) {
+  if (!dy || !x || !w || !rstd || !dx || !dw || !workspace || d % 8 || d < 8 ||
+      d > 4096 || !al16(dy) || !al16(x) || !al16(w) || !al16(dx) ||
+      ld_dy % 8 || ld_x % 8 || ld_dx % 8) {
+    autosp_set_error("rms_norm_bwd: d multiple of 8 (<= 4096), 16B-aligned rows");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  const int nb = norm_blocks();
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t smem = (size_t)d * sizeof(float);
+  const int vpl = (d / 8 + 31) / 32;  // 16-byte vectors per lane
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<nb, kNormThreads, smem, st>>>(
+        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x),
+        static_cast<const __nv_bfloat16*>(w), rstd, static_cast<__nv_bfloat16*>(dx),
+        static_cast<float*>(workspace), rows, d, ld_dy, ld_x, ld_dx);
+  };
+  if (vpl <= 1) go(rms_bwd_kernel<1>);
+  else if (vpl <= 2) go(rms_bwd_kernel<2>);
+  else if (vpl <= 4) go(rms_bwd_kernel<4>);
+  else if (vpl <= 8) go(rms_bwd_kernel<8>);
+  else if (vpl <= 16) go(rms_bwd_kernel<16>);
+  else {
+    autosp_set_error("rms_norm_bwd: d = %d > 4096 unsupported", d);
+    return AUTOSP_ERR_UNSUPPORTED;
+  }
+  colsum_kernel<<<(d + 255) / 256, 256, 0, st>>>(static_cast<const float*>(workspace), nb, d,
+                                                 static_cast<__nv_bfloat16*>(dw));
+  return launched("rms_norm_bwd");
+}
+
 extern "C" int autosp_ce_fwd(const void* logits, const int64_t* labels, float* lse, float* loss,
                              int64_t rows, int64_t vocab, int64_t ld, void* stream) {
   if (!logits || !labels || !lse || !loss || ld % 8 || !al16(logits) || vocab < 1) {
@@ -403,6 +593,10 @@ int autosp_preload_fused() {
   cudaFuncGetAttributes(&a, swiglu_bwd_kernel);
   cudaFuncGetAttributes(&a, rope_kernel);
   cudaFuncGetAttributes(&a, rope_seg_kernel);
+  cudaFuncGetAttributes(&a, rms_fwd_kernel);
+  cudaFuncGetAttributes(&a, rms_bwd_kernel<8>);
+  cudaFuncGetAttributes(&a, rms_bwd_kernel<16>);
+  cudaFuncGetAttributes(&a, colsum_kernel);
   cudaFuncGetAttributes(&a, ce_fwd_kernel);
   cudaFuncGetAttributes(&a, ce_bwd_kernel);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;

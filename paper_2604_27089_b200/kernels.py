@@ -302,6 +302,48 @@ def rope_segments(pairs: list[tuple[torch.Tensor, torch.Tensor, bool]], pos: tor
     LOG.end("rope", None, 1)
 
 
+def _rows2d(t: torch.Tensor, name: str) -> torch.Tensor:
+    t2 = t.reshape(-1, t.shape[-1])
+    if not t2.is_cuda or t2.dtype != torch.bfloat16 or t2.stride(-1) != 1:
+        raise ValidationError(f"{name}: expected a CUDA bf16 tensor with contiguous last dim")
+    return t2
+
+
+def rms_norm_fwd(x: torch.Tensor, w: torch.Tensor, eps: float):
+    """RMSNorm over the last dim: (y bf16 like x, rstd fp32 [rows])."""
+    x2 = _rows2d(x, "x")
+    rows, d = x2.shape
+    y = torch.empty((rows, d), dtype=x.dtype, device=x.device)
+    rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+    w = w.contiguous()
+    rc = _lib.load().autosp_rms_norm_fwd(x2.data_ptr(), w.data_ptr(), y.data_ptr(),
+                                         rstd.data_ptr(), rows, d, x2.stride(0), d, float(eps),
+                                         _stream())
+    _lib.check(rc, "rms_norm_fwd")
+    LOG.end("rms_norm", None, 1)
+    return y.view(x.shape), rstd.view(x.shape[:-1])
+
+
+def rms_norm_bwd(dy: torch.Tensor, x: torch.Tensor, w: torch.Tensor, rstd: torch.Tensor):
+    """(dx like x, dw like w) in one pass over (dy, x)."""
+    lib = _lib.load()
+    d2 = _rows2d(dy if dy.stride(-1) == 1 else dy.contiguous(), "dy")
+    x2 = _rows2d(x, "x")
+    rows, d = x2.shape
+    dx = torch.empty((rows, d), dtype=x.dtype, device=x.device)
+    dw = torch.empty(d, dtype=w.dtype, device=w.device)
+    ws = torch.empty(lib.autosp_rms_norm_bwd_workspace_bytes(d), dtype=torch.uint8,
+                     device=x.device)
+    rs = rstd.reshape(-1).contiguous()
+    w = w.contiguous()
+    rc = lib.autosp_rms_norm_bwd(d2.data_ptr(), x2.data_ptr(), w.data_ptr(), rs.data_ptr(),
+                                 dx.data_ptr(), dw.data_ptr(), ws.data_ptr(), rows, d,
+                                 d2.stride(0), x2.stride(0), d, _stream())
+    _lib.check(rc, "rms_norm_bwd")
+    LOG.end("rms_norm", None, 2)
+    return dx.view(x.shape), dw
+
+
 def ce_fwd(logits: torch.Tensor, labels: torch.Tensor):
     """Row-wise (lse, loss) of bf16 logits [n, V] (leading dim may exceed V)."""
     n, V = logits.shape

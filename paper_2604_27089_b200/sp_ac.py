@@ -98,7 +98,8 @@ def _nbytes(n: fx.Node) -> int | None:
     return None  # tuples / lists: cannot be saved as a unit
 
 
-_NORMS = {"aten::_fused_rms_norm", "aten::rms_norm", "aten::native_layer_norm"}
+_NORMS = {"aten::_fused_rms_norm", "aten::rms_norm", "aten::native_layer_norm",
+          "autosp::rms_norm"}
 _CASTS = {"aten::_to_copy", "prims::convert_element_type"}
 
 

@@ -145,3 +145,23 @@ def test_qkv_rope_split_and_packed_gradient(b, s, hq, hkv, d, off):
     assert _rel(g[:, :, :hq], _inv_rot(dq, pos, theta)) < TOL
     assert _rel(g[:, :, hq:hq + hkv], _inv_rot(dk, pos, theta)) < TOL
     assert torch.equal(g[:, :, hq + hkv:], dv)
+
+
+@pytest.mark.parametrize("rows,d", [(1, 64), (37, 2048), (4096, 4096), (300, 1000)])
+def test_rms_norm_fwd_bwd(rows, d):
+    """autosp::rms_norm (reference executor.py:43-45) vs an fp32 torch reference, incl. the
+    one-pass weight gradient."""
+    from paper_2604_27089_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(d)
+    x = (torch.randn(rows, d, device="cuda", generator=g) * 3).bfloat16().requires_grad_(True)
+    w = (1 + 0.1 * torch.randn(d, device="cuda", generator=g)).bfloat16().requires_grad_(True)
+    dy = torch.randn(rows, d, device="cuda", generator=g).bfloat16()
+    y = ops.rms_norm(x, w, 1e-5)
+    y.backward(dy)
+    xr = x.detach().float().requires_grad_(True)
+    wr = w.detach().float().requires_grad_(True)
+    ref = xr * torch.rsqrt(xr.pow(2).mean(-1, keepdim=True) + 1e-5) * wr
+    ref.backward(dy.float())
+    assert _rel(y, ref) < TOL
+    assert _rel(x.grad, xr.grad) < TOL
+    assert _rel(w.grad, wr.grad) < TOL
