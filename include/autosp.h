@@ -95,7 +95,7 @@ typedef struct autosp_a2a_tensor {
   int64_t dst_offset;
   int64_t dst_stride_b, dst_stride_s, dst_stride_h;
   int32_t heads; /* h of the SOURCE logical tensor */
-  int32_t _pad;
+  int32_t rope;  /* autosp_a2a_rope only: 1 = rotate (RoPE) the rows while moving them */
 } autosp_a2a_tensor;
 
 #define AUTOSP_A2A_MAX_TENSORS 4
@@ -113,6 +113,14 @@ AUTOSP_API int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n
                int s_global, int d, int elem_bytes, int world, int rank,
                void* const* peer_base, uint32_t* const* peer_flags, uint32_t epoch,
                void* stream);
+/* autosp_a2a with RoPE folded into the reshard (seq_to_head, bf16, d in {32,64,128}):
+ * tensors with rope = 1 are rotated (rotate-half, pos[t] of the source token t, theta)
+ * on the way, so the projection output is read ONCE and arrives rotated and head-major
+ * at its owner -- no separate RoPE / split / transpose kernel.                        */
+AUTOSP_API int autosp_a2a_rope(int direction, const autosp_a2a_tensor* tensors, int n_tensors,
+               int b, int s_global, int d, int elem_bytes, int world, int rank,
+               void* const* peer_base, uint32_t* const* peer_flags, uint32_t epoch,
+               const float* pos, float theta, void* stream);
 /* Stream-ordered wait until every peer has published `epoch` into this rank's flag
  * block (the receive region then holds the complete a2a output).  `first_dst_offset` is
  * this rank's dst_offset of tensor 0 for the call: every sender records its own view of

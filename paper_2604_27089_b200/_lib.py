@@ -28,7 +28,7 @@ class A2ATensor(C.Structure):
                 ("dst_offset", C.c_int64),
                 ("dst_stride_b", C.c_int64), ("dst_stride_s", C.c_int64),
                 ("dst_stride_h", C.c_int64),
-                ("heads", C.c_int32), ("_pad", C.c_int32)]
+                ("heads", C.c_int32), ("rope", C.c_int32)]
 
 
 class AttnTensor(C.Structure):
@@ -68,6 +68,10 @@ EXPORTS = {
     "autosp_a2a": (C.c_int, [C.c_int, C.POINTER(A2ATensor), C.c_int, C.c_int, C.c_int, C.c_int,
                              C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p),
                              C.POINTER(C.c_void_p), C.c_uint32, C.c_void_p]),
+    "autosp_a2a_rope": (C.c_int, [C.c_int, C.POINTER(A2ATensor), C.c_int, C.c_int, C.c_int,
+                                  C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p),
+                                  C.POINTER(C.c_void_p), C.c_uint32, C.c_void_p, C.c_float,
+                                  C.c_void_p]),
     "autosp_a2a_wait": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_uint32, C.c_int64,
                                   C.c_void_p]),
     "autosp_a2a_mark_ready": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_uint32,

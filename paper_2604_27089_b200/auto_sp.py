@@ -23,6 +23,7 @@ lowered to the sm_100a kernel.
 
 from __future__ import annotations
 
+import operator
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -51,7 +52,39 @@ def positions(n: int, device=None) -> torch.Tensor:
 
 
 INDEX_OPS = (positions, torch.arange)
-_LOWERED = (ops.ulysses_attention, ops.sdpa)
+_LOWERED = (ops.ulysses_attention, ops.sdpa, ops.ulysses_qkv_block)
+FUSE_QKV_ROPE = True  # fold autosp::qkv_rope (RoPE + split + transpose) into the reshard
+
+
+def _transposed_item(node, idx):
+    """node == <x>.transpose(1, 2) with x == getitem(R, idx); returns R or None."""
+    if not isinstance(node, fx.Node) or len(node.users) != 1:
+        return None
+    is_t = (node.op == "call_method" and node.target == "transpose") or \
+        (node.op == "call_function" and node.target is torch.transpose)
+    if not is_t or tuple(node.args[1:3]) not in ((1, 2), (2, 1)):
+        return None
+    it = node.args[0]
+    if not (isinstance(it, fx.Node) and it.op == "call_function" and
+            it.target is operator.getitem and it.args[1] == idx and len(it.users) == 1):
+        return None
+    return it.args[0]
+
+
+def _match_qkv_rope(q, k, v):
+    """q, k, v = transpose(getitem(autosp::qkv_rope(qkv, pos, theta, hq, hkv), i), 1, 2)
+    for i = 0, 1, 2 of ONE qkv_rope node with no other users, bf16, d in {32, 64, 128}."""
+    rs = [_transposed_item(x, i) for i, x in enumerate((q, k, v))]
+    r = rs[0]
+    if r is None or any(x is not r for x in rs):
+        return None
+    if not (r.op == "call_function" and r.target is torch.ops.autosp.qkv_rope.default and
+            len(r.users) == 3):
+        return None
+    qkv = _val(r.args[0])
+    if qkv is None or qkv.dtype != torch.bfloat16 or qkv.shape[-1] not in (32, 64, 128):
+        return None
+    return r
 
 
 @dataclass
@@ -131,8 +164,14 @@ def auto_sp(gm: fx.GraphModule, example_inputs, st: SPState) -> tuple[fx.GraphMo
             hq, hkv = _val(q).shape[1], _val(k).shape[1]
             if hq % P or hkv % P:
                 raise ValidationError(f"head count {hq}/{hkv} not divisible by world size {P}")
+            rq = _match_qkv_rope(q, k, v) if (P > 1 and FUSE_QKV_ROPE) else None
             with g.inserting_before(n):
-                if P > 1:
+                if rq is not None:
+                    qkv, pos, theta, nq, nkv = rq.args[:5]
+                    new = g.call_function(ops.ulysses_qkv_block, (qkv, pos, theta, nq, nkv),
+                                          {"group": st.name, "scale": scale})
+                    info.provenance[new.name] = RewriteReason.INSERTED_COLLECTIVE
+                elif P > 1:
                     new = g.call_function(ops.ulysses_attention, (q, k, v),
                                           {"group": st.name, "is_causal": True, "scale": scale})
                     info.provenance[new.name] = RewriteReason.INSERTED_COLLECTIVE
@@ -142,6 +181,12 @@ def auto_sp(gm: fx.GraphModule, example_inputs, st: SPState) -> tuple[fx.GraphMo
             new.meta.update(n.meta)
             n.replace_all_uses_with(new)
             g.erase_node(n)
+            if rq is not None:  # the transposes, getitems and qkv_rope are now dead
+                for x in (q, k, v):
+                    it = x.args[0]
+                    g.erase_node(x)
+                    g.erase_node(it)
+                g.erase_node(rq)
         elif n.target in INDEX_OPS and P > 1:
             if n.target is positions:
                 length = n.args[0]

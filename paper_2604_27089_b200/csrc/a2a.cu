@@ -16,12 +16,16 @@
 //    "ready" (I have reached call e: my readers of older data are stream-ordered
 //    before me) and "arrive[src]" (src finished writing call e into me).  All spins are
 //    bounded by %globaltimer and trap instead of hanging the GPU.
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "../../include/autosp.h"
+#include <cuda_bf16.h>
+
 #include "flags.cuh"
 #include "ptx.cuh"
+#include "rope.cuh"
 
 namespace autosp {
 constexpr int kTileTokens = 16;
@@ -35,6 +39,7 @@ struct A2ATensorDev {
   int heads;
   int tiles;                 // token tiles of the source
   int64_t items;             // b * heads * tiles
+  int rope;                  // 1: apply RoPE (bf16 rows) at the source token's position
 };
 
 struct A2AParams {
@@ -48,6 +53,8 @@ struct A2AParams {
   uint32_t epoch;
   uint32_t check;
   int64_t total_items;
+  const float* pos;  // RoPE positions of the SOURCE tokens (seq_to_head: the local shard)
+  float log2_theta;
 };
 
 AUTOSP_DEV bool epoch_reached(uint32_t v, uint32_t e) { return (int32_t)(v - e) >= 0; }
@@ -70,6 +77,8 @@ AUTOSP_DEV void push_complete(const A2AParams& p) {
 // hoisted out of the row loop (the generic kernel below recomputed 64-bit strided
 // addresses and integer divisions for all 16 possible row passes, predicated, and was
 // instruction-bound at ~0.5 TB/s).
+AUTOSP_DEV float p_pos(const float* pos, int t) { return __ldg(pos + t); }
+
 template <int ROWB>
 __global__ void __launch_bounds__(kA2AThreads) a2a_push_fast(const __grid_constant__ A2AParams p) {
   constexpr int VPR = ROWB / 16;          // vectors per row
@@ -105,6 +114,42 @@ __global__ void __launch_bounds__(kA2AThreads) a2a_push_fast(const __grid_consta
     for (int ps = 0; ps < PASSES; ++ps) {
       const int r = ps * RPP + r_in;
       if (t0 + r <= last) v[ps] = __ldg(reinterpret_cast<const uint4*>(src + r * sstep));
+    }
+    if (T->rope) {
+      // RoPE folded into the reshard (bf16 rows): the rotation partner of this lane's 8
+      // elements is the lane holding the other half of the row (lane ^ VPR/2, same row)
+      const int vin = lane % VPR;
+      const bool hi = vin >= VPR / 2;
+      const int d = ROWB / 2;
+#pragma unroll
+      for (int ps = 0; ps < PASSES; ++ps) {
+        const int r = ps * RPP + r_in;
+        uint4 o;
+        o.x = __shfl_xor_sync(0xffffffffu, v[ps].x, VPR / 2);
+        o.y = __shfl_xor_sync(0xffffffffu, v[ps].y, VPR / 2);
+        o.z = __shfl_xor_sync(0xffffffffu, v[ps].z, VPR / 2);
+        o.w = __shfl_xor_sync(0xffffffffu, v[ps].w, VPR / 2);
+        if (t0 + r <= last) {
+          const float tp = p_pos(p.pos, t0 + r);
+          const __nv_bfloat162* mine = reinterpret_cast<const __nv_bfloat162*>(&v[ps]);
+          const __nv_bfloat162* other = reinterpret_cast<const __nv_bfloat162*>(&o);
+          uint4 res;
+          __nv_bfloat162* out = reinterpret_cast<__nv_bfloat162*>(&res);
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            const float2 m2 = __bfloat1622float2(mine[k2]);
+            const float2 o2 = __bfloat1622float2(other[k2]);
+            float s0, c0, s1, c1;
+            const int j0 = (vin % (VPR / 2)) * 8 + 2 * k2;
+            rope_sincos(tp, j0, d, p.log2_theta, &s0, &c0);
+            rope_sincos(tp, j0 + 1, d, p.log2_theta, &s1, &c1);
+            const float y0 = hi ? rope_hi(o2.x, m2.x, c0, s0) : rope_lo(m2.x, o2.x, c0, s0);
+            const float y1 = hi ? rope_hi(o2.y, m2.y, c1, s1) : rope_lo(m2.y, o2.y, c1, s1);
+            out[k2] = __floats2bfloat162_rn(y0, y1);
+          }
+          v[ps] = res;
+        }
+      }
     }
     if (s2h) {
       const int hl = T->heads / p.P;
@@ -259,10 +304,42 @@ __global__ void a2a_mark_ready_kernel(const __grid_constant__ MarkParams m) {
 // ---------------------------------------------------------------------------- C ABI
 extern "C" void autosp_set_error(const char* fmt, ...);
 
+static int a2a_impl(int direction, const autosp_a2a_tensor* tensors, int n_tensors, int b,
+                    int s_global, int d, int elem_bytes, int world, int rank,
+                    void* const* peer_base, uint32_t* const* peer_flags, uint32_t epoch,
+                    const float* pos, float theta, void* stream);
+
 extern "C" int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n_tensors, int b,
                           int s_global, int d, int elem_bytes, int world, int rank,
                           void* const* peer_base, uint32_t* const* peer_flags, uint32_t epoch,
                           void* stream) {
+  for (int i = 0; tensors && i < n_tensors && i < AUTOSP_A2A_MAX_TENSORS; ++i)
+    if (tensors[i].rope) {
+      autosp_set_error("autosp_a2a: tensor %d requests RoPE; use autosp_a2a_rope", i);
+      return AUTOSP_ERR_VALIDATION;
+    }
+  return a2a_impl(direction, tensors, n_tensors, b, s_global, d, elem_bytes, world, rank,
+                  peer_base, peer_flags, epoch, nullptr, 0.f, stream);
+}
+
+extern "C" int autosp_a2a_rope(int direction, const autosp_a2a_tensor* tensors, int n_tensors,
+                               int b, int s_global, int d, int elem_bytes, int world, int rank,
+                               void* const* peer_base, uint32_t* const* peer_flags,
+                               uint32_t epoch, const float* pos, float theta, void* stream) {
+  if (direction != AUTOSP_SEQ_TO_HEAD || elem_bytes != 2 || !pos || theta <= 1.f ||
+      (d != 32 && d != 64 && d != 128)) {
+    autosp_set_error("autosp_a2a_rope: seq_to_head of bf16 rows with d in {32, 64, 128}, "
+                     "positions and theta > 1 required");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  return a2a_impl(direction, tensors, n_tensors, b, s_global, d, elem_bytes, world, rank,
+                  peer_base, peer_flags, epoch, pos, theta, stream);
+}
+
+static int a2a_impl(int direction, const autosp_a2a_tensor* tensors, int n_tensors, int b,
+                    int s_global, int d, int elem_bytes, int world, int rank,
+                    void* const* peer_base, uint32_t* const* peer_flags, uint32_t epoch,
+                    const float* pos, float theta, void* stream) {
   using namespace autosp;
   if (direction != AUTOSP_SEQ_TO_HEAD && direction != AUTOSP_HEAD_TO_SEQ) {
     autosp_set_error("unknown all-to-all direction %d", direction);
@@ -332,6 +409,7 @@ extern "C" int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n
     D.dst_off = T.dst_offset;
     D.ds_b = T.dst_stride_b; D.ds_s = T.dst_stride_s; D.ds_h = T.dst_stride_h;
     D.heads = T.heads;
+    D.rope = T.rope ? 1 : 0;
     D.tiles = (s_src + kTileTokens - 1) / kTileTokens;
     D.items = (int64_t)b * T.heads * D.tiles;
     p.total_items += D.items;
@@ -358,6 +436,12 @@ extern "C" int autosp_a2a(int direction, const autosp_a2a_tensor* tensors, int n
   if (world > 1) a2a_handshake_kernel<<<1, 32, 0, st>>>(p);
   const bool fast = align == 16 && (row == 64 || row == 128 || row == 256) &&
                     p.total_items < (int64_t)INT32_MAX;
+  p.pos = pos;
+  p.log2_theta = pos ? log2f(theta) : 0.f;
+  if (pos && !fast) {
+    autosp_set_error("a2a with RoPE needs 16-byte aligned rows of 64/128/256 bytes");
+    return AUTOSP_ERR_UNSUPPORTED;
+  }
   if (fast) {
     switch (row) {
       case 64: a2a_push_fast<64><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;

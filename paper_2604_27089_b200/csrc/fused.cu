@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/autosp.h"
+#include "rope.cuh"
 
 extern "C" void autosp_set_error(const char* fmt, ...);
 
@@ -162,9 +163,7 @@ __global__ void rope_seg_kernel(const __grid_constant__ RopeSegArgs a) {
     float cs[8], sn[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int j = v * 8 + k;
-      const float inv_freq = exp2f(-(2.f * j / a.d) * a.log2_theta);
-      sincosf(p * inv_freq, &sn[k], &cs[k]);
+      rope_sincos(p, v * 8 + k, a.d, a.log2_theta, &sn[k], &cs[k]);
       if (a.inverse) sn[k] = -sn[k];
     }
 #pragma unroll
@@ -186,8 +185,8 @@ __global__ void rope_seg_kernel(const __grid_constant__ RopeSegArgs a) {
         unpack8(r2, x2);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          y1[k] = x1[k] * cs[k] - x2[k] * sn[k];
-          y2[k] = x2[k] * cs[k] + x1[k] * sn[k];
+          y1[k] = rope_lo(x1[k], x2[k], cs[k], sn[k]);
+          y2[k] = rope_hi(x1[k], x2[k], cs[k], sn[k]);
         }
         *reinterpret_cast<uint4*>(yr + v * 8) = pack8(y1);
         *reinterpret_cast<uint4*>(yr + half + v * 8) = pack8(y2);

@@ -164,25 +164,34 @@ def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = Non
 
 # ----------------------------------------------------------------------------- all-to-all
 def a2a_tensor_desc(src: torch.Tensor, heads: int, dst_offset: int,
-                    dst_strides: tuple[int, int, int]) -> _lib.A2ATensor:
+                    dst_strides: tuple[int, int, int], rope: bool = False) -> _lib.A2ATensor:
     """src is a logical [b, s, h, d] view with d contiguous."""
     if src.dim() != 4 or src.stride(3) != 1:
         raise ValidationError("a2a source must be a [b, s, h, d] view with contiguous head_dim")
     sb, ss, sh, _ = src.stride()
     db, ds, dh = dst_strides
-    return _lib.A2ATensor(src.data_ptr(), sb, ss, sh, dst_offset, db, ds, dh, heads, 0)
+    return _lib.A2ATensor(src.data_ptr(), sb, ss, sh, dst_offset, db, ds, dh, heads, int(rope))
 
 
 def a2a_launch(direction: int, descs: list, b: int, s_global: int, d: int, elem_bytes: int,
                world: int, rank: int, peer_base: list[int], peer_flags: list[int],
-               epoch: int) -> None:
+               epoch: int, pos: torch.Tensor | None = None, theta: float = 0.0) -> None:
+    """K1/K2.  With `pos` (fp32 positions of the source tokens) the descriptors flagged
+    rope are rotated on the way (autosp_a2a_rope)."""
     lib = _lib.load()
     arr = (_lib.A2ATensor * len(descs))(*descs)
     pb = (C.c_void_p * world)(*peer_base)
     pf = (C.c_void_p * world)(*peer_flags)
     ev = LOG.begin("a2a")
-    rc = lib.autosp_a2a(direction, arr, len(descs), b, s_global, d, elem_bytes, world, rank,
-                        pb, pf, epoch & 0xFFFFFFFF, _stream())
+    if pos is None:
+        rc = lib.autosp_a2a(direction, arr, len(descs), b, s_global, d, elem_bytes, world, rank,
+                            pb, pf, epoch & 0xFFFFFFFF, _stream())
+    else:
+        if pos.dtype != torch.float32 or not pos.is_contiguous() or not pos.is_cuda:
+            raise ValidationError("a2a rope positions must be a contiguous CUDA fp32 tensor")
+        rc = lib.autosp_a2a_rope(direction, arr, len(descs), b, s_global, d, elem_bytes, world,
+                                 rank, pb, pf, epoch & 0xFFFFFFFF, pos.data_ptr(), float(theta),
+                                 _stream())
     _lib.check(rc, "a2a")
     LOG.end("a2a", ev, 2 if world > 1 else 1)
 

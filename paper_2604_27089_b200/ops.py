@@ -234,6 +234,125 @@ def _attn_a2a_bwd(ctx, d_otok, d_ohead, d_lse):
 
 attention_a2a.register_autograd(_attn_a2a_bwd, setup_context=_attn_a2a_setup)
 
+# ----------------------------------------------------------------------------- Ulysses block
+# from the PACKED QKV projection output: RoPE + split + transpose folded into the reshard
+@torch.library.custom_op("autosp::ulysses_qkv_attention", mutates_args=(), device_types="cuda")
+def ulysses_qkv_attention(qkv: torch.Tensor, pos: torch.Tensor, theta: float, hq: int, hkv: int,
+                          scale: float, group: str) -> tuple[torch.Tensor, torch.Tensor,
+                                                             torch.Tensor, torch.Tensor,
+                                                             torch.Tensor, torch.Tensor]:
+    """The whole Ulysses attention block (sp_pass.py:172-195) fed by the packed projection
+    output qkv [b, s/P, hq+2hkv, d] of this rank's tokens:
+      K1 (a2a_rope): q/k rotated and v moved straight from the packed rows into the head
+         owners' receive regions, head-major [b, h/P, s, d] -- the projection output is
+         read once, no RoPE / split / transpose kernel;
+      K3+K2: causal attention on the local heads, the epilogue pushing O to the token
+         owners (token-major [b, H, s/P, d] = the O-projection input).
+    Returns (o_tokens, q_heads, k_heads, v_heads, o_heads, lse); everything after o_tokens
+    is what the backward needs (the a2a outputs sp_ac keeps)."""
+    st = sp_dist.lookup(group)
+    P, pool = st.world, st.pool
+    b, sl, H3, d = qkv.shape
+    S = sl * P
+    if H3 != hq + 2 * hkv or hq % P or hkv % P:
+        raise ValidationError(f"qkv heads {H3} != {hq}+2*{hkv} or not divisible by {P}")
+    srcs = (qkv[:, :, :hq], qkv[:, :, hq:hq + hkv], qkv[:, :, hq + hkv:])
+    outs, descs, first = [], [], None
+    for x, rot in zip(srcs, (True, True, False)):
+        h = x.shape[2]
+        shape = (b, h // P, S, d)
+        strides = ((h // P) * S * d, S * d, d, 1)
+        off, base = pool.alloc(math.prod(shape) * qkv.element_size())
+        first = off if first is None else first
+        outs.append(base.view(qkv.dtype).as_strided(shape, strides))
+        descs.append(kernels.a2a_tensor_desc(x, h, off, (strides[0], strides[2], strides[1]),
+                                             rope=rot))
+    epoch = pool.next_epoch()
+    kernels.a2a_launch(SEQ_TO_HEAD_DIR, descs, b, S, d, qkv.element_size(), P, st.rank,
+                       pool.region_ptrs, pool.flag_ptrs, epoch,
+                       pos=pos.to(torch.float32).contiguous(), theta=theta)
+    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, first)
+    qh, kh, vh = outs
+    o_tok, o_head, lse = attention_a2a(qh, kh, vh, scale, True, group)
+    return o_tok, qh, kh, vh, o_head, lse
+
+
+@ulysses_qkv_attention.register_fake
+def _ulysses_qkv_attention_fake(qkv, pos, theta, hq, hkv, scale, group):
+    P = sp_dist.lookup(group).world
+    b, sl, H3, d = qkv.shape
+    S = sl * P
+    H = hq
+    heads = lambda h: qkv.new_empty_strided((b, h // P, S, d), ((h // P) * S * d, S * d, d, 1))
+    return (qkv.new_empty_strided((b, H, sl, d), (sl * H * d, d, H * d, 1)), heads(hq),
+            heads(hkv), heads(hkv), qkv.new_empty((b, hq // P, S, d)),
+            qkv.new_empty((b, hq // P, S), dtype=torch.float32))
+
+
+def _uqa_setup(ctx, inputs, output):
+    qkv, pos, theta, hq, hkv, scale, group = inputs
+    _, qh, kh, vh, o_head, lse = output
+    ctx.save_for_backward(pos, qh, kh, vh, o_head, lse)
+    ctx.theta, ctx.hq, ctx.hkv, ctx.scale, ctx.group = theta, hq, hkv, scale, group
+    ctx.qkv_shape = tuple(qkv.shape)
+
+
+def _uqa_bwd(ctx, d_otok, *unused):
+    pos, qh, kh, vh, o_head, lse = ctx.saved_tensors
+    (do,) = all_to_all([d_otok], SEQ_TO_HEAD_DIR, ctx.group)
+    dq, dk, dv = attention_backward(do, qh, kh, vh, o_head, lse, ctx.scale, True)
+    dqkv = qkv_grad_gather(dq, dk, dv, pos, ctx.theta, ctx.group)
+    return dqkv, None, None, None, None, None, None
+
+
+ulysses_qkv_attention.register_autograd(_uqa_bwd, setup_context=_uqa_setup)
+
+
+@torch.library.custom_op("autosp::qkv_grad_gather", mutates_args=(), device_types="cuda")
+def qkv_grad_gather(dq: torch.Tensor, dk: torch.Tensor, dv: torch.Tensor, pos: torch.Tensor,
+                    theta: float, group: str) -> torch.Tensor:
+    """Backward of the RoPE-fused seq->head reshard: dq/dk/dv (head-sharded [b, h/P, s, d])
+    pushed head->seq straight into ONE packed [b, s/P, hq+2hkv, d] gradient on each token
+    owner, then the inverse rotation of its q/k heads in place (one segmented-RoPE launch)."""
+    st = sp_dist.lookup(group)
+    P, pool = st.world, st.pool
+    b, hql, S, d = dq.shape
+    hkvl = dk.shape[1]
+    hq, hkv, sl = hql * P, hkvl * P, S // P
+    H3 = hq + 2 * hkv
+    es = dq.element_size()
+    off, base = pool.alloc(b * sl * H3 * d * es)
+    dqkv = base.view(dq.dtype).as_strided((b, sl, H3, d), (sl * H3 * d, H3 * d, d, 1))
+    descs = []
+    for x, h0 in ((dq, 0), (dk, hq), (dv, hq + hkv)):
+        if x.stride(-1) != 1:
+            x = x.contiguous()
+        descs.append(kernels.a2a_tensor_desc(x.permute(0, 2, 1, 3), x.shape[1], off + h0 * d * es,
+                                             (sl * H3 * d, H3 * d, d)))
+    epoch = pool.next_epoch()
+    kernels.a2a_launch(HEAD_TO_SEQ_DIR, descs, b, S, d, es, P, st.rank, pool.region_ptrs,
+                       pool.flag_ptrs, epoch)
+    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, off)
+    kernels.rope_segments([(dqkv[:, :, :hq], dqkv[:, :, :hq], True),
+                           (dqkv[:, :, hq:hq + hkv], dqkv[:, :, hq:hq + hkv], True)],
+                          pos, theta, inverse=True)
+    return dqkv
+
+
+@qkv_grad_gather.register_fake
+def _qkv_grad_gather_fake(dq, dk, dv, pos, theta, group):
+    P = sp_dist.lookup(group).world
+    b, hql, S, d = dq.shape
+    H3 = (hql + 2 * dk.shape[1]) * P
+    return dq.new_empty((b, S // P, H3, d))
+
+
+def ulysses_qkv_block(qkv, pos, theta: float, hq: int, hkv: int, group: str, scale=None):
+    """What auto_sp substitutes for qkv_rope -> transpose -> SDPA at P > 1 (bf16)."""
+    sc = 1.0 / math.sqrt(qkv.shape[-1]) if scale is None else float(scale)
+    return ulysses_qkv_attention(qkv, pos, theta, hq, hkv, sc, group)[0]
+
+
 FUSE_OUTPUT_A2A = True  # attention epilogue pushes O (K3 + K2 in one kernel)
 
 

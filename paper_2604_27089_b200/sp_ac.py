@@ -61,12 +61,15 @@ def _opname(n: fx.Node) -> str:
 
 def is_autosp_collective(n: fx.Node) -> bool:
     return n.op == "call_function" and _opname(n) in ("autosp::all_to_all",
-                                                      "autosp::attention_a2a")
+                                                      "autosp::attention_a2a",
+                                                      "autosp::ulysses_qkv_attention",
+                                                      "autosp::qkv_grad_gather")
 
 
 def is_autosp_attention(n: fx.Node) -> bool:
     return n.op == "call_function" and _opname(n) in ("autosp::attention",
-                                                      "autosp::attention_a2a")
+                                                      "autosp::attention_a2a",
+                                                      "autosp::ulysses_qkv_attention")
 
 
 def _is_matmul(n: fx.Node) -> bool:
