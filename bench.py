@@ -194,6 +194,8 @@ def main():
                          "seq-aware, conservative, seq-aware-all")
     ap.add_argument("--no-sp-ac", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-zero1", action="store_true",
+                    help="N > 1: all-reduce gradients + replicated AdamW instead of ZeRO-1")
     ap.add_argument("--layers", type=int, default=None, help="override (debug only; invalid bench)")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -230,7 +232,12 @@ def main():
 
     torch.manual_seed(0)
     model = LlamaDecoder(cfg, dtype=torch.bfloat16, device=dev)
-    opt = torch.optim.AdamW(model.parameters(), lr=1e-4, fused=True)
+    zero1 = P > 1 and not args.no_zero1
+    if zero1:  # ZeRO-1 over the SP group: reduce-scatter + sharded AdamW + all-gather
+        from paper_2604_27089_b200.zero import ShardedAdamW
+        opt = ShardedAdamW(model.parameters(), st, lr=1e-4)
+    else:
+        opt = torch.optim.AdamW(model.parameters(), lr=1e-4, fused=True)
     cm = autosp.compile(model)
     g = torch.Generator(device="cpu").manual_seed(1234)
     ids_full = torch.randint(0, cfg.vocab, (b, S + 1), generator=g)
@@ -244,9 +251,9 @@ def main():
         hidden = cm(ids_)
         loss = lm_loss(hidden, model.lm_head, labels_)
         loss.backward()
-        if P > 1:
+        if P > 1 and not zero1:
             autosp.dist.reduce_gradients(params, st)
-        opt.step()
+        opt.step()  # (ShardedAdamW reduces the SP-partial gradients itself)
         opt.zero_grad(set_to_none=True)
         return loss
 
@@ -329,7 +336,8 @@ def main():
         "config": {"workload": f"{cfg.name} synthetic, global seq {S}, batch {b} "
                                f"(BASELINE.json configs[1]; at N=1 the single-GPU case)",
                    "model": cfg.name, "global_batch": b, "seq_len": S,
-                   "parallelism": f"sp{P}", "passes": passes, "ac_mode": args.ac_mode,
+                   "parallelism": f"sp{P}" + ("+zero1" if zero1 else ""), "passes": passes,
+                   "ac_mode": args.ac_mode,
                    "ac_applied": sp_ac.LAST_PLAN.get("mode_applied"),
                    "l2": "working set (weights 2.5 GB + activations) >> 126 MB L2; no flush"},
         "e2e": e2e,
