@@ -34,45 +34,67 @@ namespace autosp {
 namespace fwd {
 
 constexpr int BM = 128;  // query rows per tile
-constexpr int BN = 128;  // keys per tile
-constexpr int kThreads = 384;
-// Warp roles.  The issue arbiter favours HIGHER warp ids, so the latency-critical
-// single-thread producers (TMA, MMA) get the top ids and are never starved by the
-// instruction-heavy softmax warpgroups (which must be whole, aligned warpgroups for
-// TMEM lane access).
-constexpr int kSoftmaxWarp0 = 0;   // warps 0-3: Q tile 0, 4-7: Q tile 1
-constexpr int kAllocWarp = 8;
-constexpr int kTmaWarp = 10;
-constexpr int kMmaWarp = 11;
+constexpr int kSoftmaxWarp0 = 0;   // warps 4i..4i+3: softmax of Q tile i
+// Tile shape (build-time, swept with tools/attn_bench.py): 64-key tiles (3 x 64 for
+// d <= 64, or 2 x 64 with separate P buffers for d = 128) measured 25 % slower than
+// 2 Q tiles x 128 keys -- the per-tile hand-off chain (S -> softmax -> P -> PV) is paid
+// twice as often -- so 2 x 128 is the default.
+#ifndef AUTOSP_FWD_NQ64
+#define AUTOSP_FWD_NQ64 2     // Q tiles per CTA for d <= 64
+#endif
+#ifndef AUTOSP_FWD_BN64
+#define AUTOSP_FWD_BN64 128   // keys per KV tile for d <= 64
+#endif
+#ifndef AUTOSP_FWD_BN128
+#define AUTOSP_FWD_BN128 128  // keys per KV tile for d = 128
+#endif
 
 template <int D>
 struct Cfg {
+  // NQ Q tiles of 128 rows per CTA ping-pong on the tensor core, one softmax warpgroup
+  // each; KV tiles of BN keys (see the tile-shape note above).
+  static constexpr int NQ = D == 128 ? 2 : AUTOSP_FWD_NQ64;
+  static constexpr int BN = D == 128 ? AUTOSP_FWD_BN128 : AUTOSP_FWD_BN64;
+  static constexpr int NH = BN / 64;                        // 64-column score chunks
+  static constexpr int kThreads = 32 * (4 * NQ + 4);
+  // Warp roles.  The issue arbiter favours HIGHER warp ids, so the latency-critical
+  // single-thread producers (TMA, MMA) get the top ids and are never starved by the
+  // instruction-heavy softmax warpgroups (whole, aligned warpgroups for TMEM lanes).
+  static constexpr int kAllocWarp = 4 * NQ;
+  static constexpr int kTmaWarp = 4 * NQ + 2;
+  static constexpr int kMmaWarp = 4 * NQ + 3;
   static constexpr int SW = (D * 2 >= 128) ? 128 : D * 2;  // swizzle bytes
   static constexpr int CE = SW / 2;                         // elements per swizzle chunk
   static constexpr int NCH = D / CE;                        // chunks per row
-  static constexpr int TILE_BYTES = BM * D * 2;             // 128 x D bf16
-  static constexpr int kStages = D == 128 ? 2 : (D == 64 ? 3 : 4);
+  static constexpr int TILE_BYTES = BM * D * 2;             // Q tile: 128 x D bf16
+  static constexpr int KTILE = BN * D * 2;                  // K / V tile: BN x D bf16
+  static constexpr int KV_RING = D == 128 ? 131072 : 98304;  // bytes of K + V stages
+  static constexpr int kStagesRaw = KV_RING / (2 * KTILE);
+  static constexpr int kStages = kStagesRaw < 2 ? 2 : (kStagesRaw > 8 ? 8 : kStagesRaw);
   // exps per 8 computed by the FMA-pipe polynomial instead of MUFU (MUFU is the
   // bottleneck when the tile's MMA work is small: d = 32 / 64)
   static constexpr int kEmuPer8 = D == 128 ? 2 : AUTOSP_FWD_EMU;
   static constexpr int LAYOUT = SW == 128 ? 2 : (SW == 64 ? 4 : 6);
   static constexpr int SBO = 8 * SW;  // 8-row swizzle atom
-  // smem: Q[2] | K[kStages] | V[kStages] | barriers
+  // smem: Q[NQ] | K[kStages] | V[kStages] | barriers
   static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = 2 * TILE_BYTES;
-  static constexpr int V_OFF = K_OFF + kStages * TILE_BYTES;
-  static constexpr int BAR_OFF = V_OFF + kStages * TILE_BYTES;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;  // + alignment slack
+  static constexpr int K_OFF = NQ * TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + kStages * KTILE;
+  static constexpr int BAR_OFF = V_OFF + kStages * KTILE;
+  static constexpr int SMEM = BAR_OFF + 512 + 1024;  // + alignment slack
+  static_assert(SMEM <= 232448, "shared memory budget");
   static constexpr uint32_t TMEM_COLS = 512;
-  // d <= 64: separate bf16 P buffers so S_i(j+1) = Q_i K^T can be issued as soon as the
-  // softmax has READ S_i(j), overlapping the rest of the softmax and PV_i(j):
-  //   S0 | S1 | P0 | P1 (64 cols each) | O0 | O1.     d = 128: S0 | S1 | O0 | O1, P aliases S.
-  static constexpr bool SEP_P = D <= 64;
-  static constexpr uint32_t S_COL = 0;                    // S_i at i*128
-  static constexpr uint32_t P_COL = SEP_P ? 256 : 0;      // P_i at P_COL + i*(SEP_P ? 64 : 128)
-  static constexpr uint32_t P_STRIDE = SEP_P ? 64 : 128;
-  static constexpr uint32_t O_COL = SEP_P ? 384 : 256;    // O_i at O_COL + i*D
-  static_assert(O_COL + 2 * D <= TMEM_COLS, "TMEM budget");
+  // TMEM: S_0..S_{NQ-1} (BN fp32 cols each) | P_i (bf16, BN/2 cols) | O_i (D cols).
+  // Separate P buffers (SEP_P) let S_i(j+1) = Q_i K^T be issued as soon as the softmax
+  // has READ S_i(j), overlapping the rest of the softmax and PV_i(j); without room for
+  // them P aliases S (only the old 128-key d = 128 layout).
+  static constexpr bool SEP_P = NQ * (BN + BN / 2 + D) <= (int)TMEM_COLS;
+  static constexpr uint32_t S_COL = 0;                         // S_i at i*BN
+  static constexpr uint32_t P_COL = SEP_P ? NQ * BN : 0;       // P_i at P_COL + i*P_STRIDE
+  static constexpr uint32_t P_STRIDE = SEP_P ? BN / 2 : BN;
+  static constexpr uint32_t O_COL = SEP_P ? NQ * (BN + BN / 2) : NQ * BN;  // O_i at O_COL + i*D
+  static_assert(O_COL + NQ * D <= TMEM_COLS, "TMEM budget");
+  static_assert(BN == 64 || BN == 128, "KV tile");
 };
 
 struct Params {
@@ -100,30 +122,18 @@ constexpr int kTraceSteps = 64;
   } while (0)
 long long* g_fwd_trace = nullptr;
 
-// K-major operand tile [128 rows x D] stored as NCH swizzled chunks of [128 x SW bytes].
-template <int D>
-AUTOSP_DEV uint64_t desc_kmajor(uint32_t tile_saddr, int kk) {
-  using C = Cfg<D>;
-  const int e = kk * 16;  // element offset along K
-  const uint32_t addr = tile_saddr + (e / C::CE) * (BM * C::SW) + (e % C::CE) * 2;
-  return make_smem_desc(addr, 16, C::SBO, C::LAYOUT);
-}
-// byte offset >> 4 of K-step kk inside a K-major tile (added to the descriptor's address)
-template <int D>
+// byte offset >> 4 of K-step kk inside a K-major tile of ROWS rows stored as NCH swizzled
+// chunks of [ROWS x SW bytes] (added to the descriptor's start address)
+template <int D, int ROWS>
 __host__ __device__ constexpr uint64_t kmajor_off(int kk) {
-  return (uint64_t)((((kk * 16) / Cfg<D>::CE) * (BM * Cfg<D>::SW) + ((kk * 16) % Cfg<D>::CE) * 2) >> 4);
-}
-// MN-major B operand V [128 keys x D] (N = D contiguous), K-step kk covers 16 keys.
-template <int D>
-AUTOSP_DEV uint64_t desc_v(uint32_t tile_saddr, int kk) {
-  using C = Cfg<D>;
-  const uint32_t addr = tile_saddr + kk * 16 * C::SW;
-  return make_smem_desc(addr, BN * C::SW /*LBO: next D chunk*/, C::SBO, C::LAYOUT);
+  return (uint64_t)((((kk * 16) / Cfg<D>::CE) * (ROWS * Cfg<D>::SW) + ((kk * 16) % Cfg<D>::CE) * 2) >> 4);
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
+  constexpr int NQ = C::NQ, BN = C::BN;
+  constexpr int kAllocWarp = C::kAllocWarp, kTmaWarp = C::kTmaWarp, kMmaWarp = C::kMmaWarp;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -133,11 +143,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   uint64_t* k_empty = k_full + C::kStages;
   uint64_t* v_full = k_empty + C::kStages;
   uint64_t* v_empty = v_full + C::kStages;
-  uint64_t* s_full = v_empty + C::kStages;  // [2]
-  uint64_t* p_full = s_full + 2;            // [2]
-  uint64_t* o_done = p_full + 2;            // [2]
-  uint64_t* s_free = o_done + 2;            // [2] softmax finished reading S_i (SEP_P)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_free + 2);
+  uint64_t* s_full = v_empty + C::kStages;  // [NQ]
+  uint64_t* p_full = s_full + NQ;           // [NQ]
+  uint64_t* o_done = p_full + NQ;           // [NQ]
+  uint64_t* s_free = o_done + NQ;           // [NQ] softmax finished reading S_i (SEP_P)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_free + NQ);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -145,16 +155,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   const int head = blockIdx.y;
   const int batch = blockIdx.z;
   const int kvhead = head / (p.Hq / p.Hkv);
-  const int q0 = qblk * 2 * BM;
+  const int q0 = qblk * NQ * BM;
   const int n_kv_total = (p.S + BN - 1) / BN;
-  int n_tiles[2];
+  int n_tiles[NQ];
+  int n_max = 0;
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < NQ; ++i) {
     const int last_row = min(q0 + (i + 1) * BM, p.S) - 1;
     n_tiles[i] = p.causal ? min(last_row / BN + 1, n_kv_total) : n_kv_total;
     if (q0 + i * BM >= p.S) n_tiles[i] = 0;
+    n_max = max(n_max, n_tiles[i]);
   }
-  const int n_max = max(n_tiles[0], n_tiles[1]);
 
   if (warp == kTmaWarp && lane == 0) {
     mbar_init(q_full, 1);
@@ -164,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       mbar_init(v_full + s, 1);
       mbar_init(v_empty + s, 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NQ; ++i) {
       mbar_init(s_full + i, 1);
       mbar_init(p_full + i, 4);   // one arrival per softmax warp
       mbar_init(o_done + i, 1);
@@ -189,8 +200,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     if (lane == 0 && n_max > 0) {
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
-      mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
-      for (int i = 0; i < 2; ++i)
+      int nq_live = 0;
+      for (int i = 0; i < NQ; ++i) nq_live += (q0 + i * BM < p.S) ? 1 : 0;
+      mbar_arrive_expect_tx(q_full, nq_live * C::TILE_BYTES);
+      for (int i = 0; i < nq_live; ++i)
         for (int c = 0; c < C::NCH; ++c)
           tma_load_4d(smem + C::Q_OFF + i * C::TILE_BYTES + c * BM * C::SW, &p.tm_q, q_full,
                       c * C::CE, q0 + i * BM, head, batch, pol_q);
@@ -198,14 +211,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         const int st = j % C::kStages;
         const uint32_t ph = (j / C::kStages) & 1;
         mbar_wait(k_empty + st, ph ^ 1);
-        mbar_arrive_expect_tx(k_full + st, C::TILE_BYTES);
+        mbar_arrive_expect_tx(k_full + st, C::KTILE);
         for (int c = 0; c < C::NCH; ++c)
-          tma_load_4d(smem + C::K_OFF + st * C::TILE_BYTES + c * BN * C::SW, &p.tm_k,
+          tma_load_4d(smem + C::K_OFF + st * C::KTILE + c * BN * C::SW, &p.tm_k,
                       k_full + st, c * C::CE, j * BN, kvhead, batch, pol_kv);
         mbar_wait(v_empty + st, ph ^ 1);
-        mbar_arrive_expect_tx(v_full + st, C::TILE_BYTES);
+        mbar_arrive_expect_tx(v_full + st, C::KTILE);
         for (int c = 0; c < C::NCH; ++c)
-          tma_load_4d(smem + C::V_OFF + st * C::TILE_BYTES + c * BN * C::SW, &p.tm_v,
+          tma_load_4d(smem + C::V_OFF + st * C::KTILE + c * BN * C::SW, &p.tm_v,
                       v_full + st, c * C::CE, j * BN, kvhead, batch, pol_kv);
       }
     }
@@ -220,19 +233,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       auto issue_qk = [&](int i, int j) {
         const int st = j % C::kStages;
         const uint64_t da = make_smem_desc(sq + i * C::TILE_BYTES, 16, C::SBO, C::LAYOUT);
-        const uint64_t db = make_smem_desc(sk + st * C::TILE_BYTES, 16, C::SBO, C::LAYOUT);
+        const uint64_t db = make_smem_desc(sk + st * C::KTILE, 16, C::SBO, C::LAYOUT);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
-            mma_ss(tmem + C::S_COL + i * BN, da + kmajor_off<D>(kk), db + kmajor_off<D>(kk),
-                   idesc_qk, kk > 0);
+            mma_ss(tmem + C::S_COL + i * BN, da + kmajor_off<D, BM>(kk),
+                   db + kmajor_off<D, BN>(kk), idesc_qk, kk > 0);
           tc_commit(s_full + i);
         }
         __syncwarp();
       };
       auto issue_pv = [&](int i, int j) {
         const int st = j % C::kStages;
-        const uint64_t dv = make_smem_desc(sv + st * C::TILE_BYTES, BN * C::SW, C::SBO, C::LAYOUT);
+        const uint64_t dv = make_smem_desc(sv + st * C::KTILE, BN * C::SW, C::SBO, C::LAYOUT);
         const uint32_t pa = tmem + C::P_COL + i * C::P_STRIDE;
         const uint32_t oa = tmem + C::O_COL + i * D;
         const uint32_t acc0 = j > 0 ? 1u : 0u;
@@ -252,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       mbar_wait(q_full, 0);
       mbar_wait(k_full + 0, 0);
       tc_fence_after();
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < NQ; ++i)
         if (n_tiles[i] > 0) issue_qk(i, 0);
       commit(k_empty + 0);
       for (int j = 0; j < n_max; ++j) {
@@ -271,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             k_next_ready = true;
           }
         };
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NQ; ++i) {
           if (j >= n_tiles[i]) continue;
           if (C::SEP_P && j + 1 < n_tiles[i]) {
             // S_i(j+1) as soon as the softmax has read S_i(j)
@@ -298,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         }
       }
     }
-  } else if (warp >= kSoftmaxWarp0 && warp < kSoftmaxWarp0 + 8) {
+  } else if (warp >= kSoftmaxWarp0 && warp < kSoftmaxWarp0 + 4 * NQ) {
     // ------------------------------------------------------------ softmax warpgroups
     const int i = (warp - kSoftmaxWarp0) / 4;  // Q tile
     const int quarter = warp & 3;              // TMEM lane quarter
@@ -331,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 #pragma unroll
         for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < C::NH; ++h) {
           uint32_t sr[64];
           tmem_ld32(s_addr + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
           tmem_ld32(s_addr + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
@@ -384,12 +397,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         uint64_t rs2[4] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f),
                            f2_pack(0.f, 0.f)};
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < C::NH; ++h) {
           uint32_t sr[64];
           tmem_ld32(s_addr + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
           tmem_ld32(s_addr + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
           tmem_wait_ld();
-          if (C::SEP_P && h == 1) {  // S_i fully read: the MMA may overwrite it with S_i(j+1)
+          if (C::SEP_P && h == C::NH - 1) {  // S_i fully read: the MMA may overwrite it with S_i(j+1)
             tc_fence_before();
             mbar_arrive_warp(s_free + i);
             if (lane == 0 && warp == 0) FWD_TRACE(15, j);
@@ -514,9 +527,9 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   }
   if (!make_map_bhsd(&p.tm_q, q.ptr, B, Hq, S, D, q.stride_b, q.stride_h, q.stride_s, C::CE, BM,
                      C::SW) ||
-      !make_map_bhsd(&p.tm_k, k.ptr, B, Hkv, S, D, k.stride_b, k.stride_h, k.stride_s, C::CE, BN,
+      !make_map_bhsd(&p.tm_k, k.ptr, B, Hkv, S, D, k.stride_b, k.stride_h, k.stride_s, C::CE, C::BN,
                      C::SW) ||
-      !make_map_bhsd(&p.tm_v, v.ptr, B, Hkv, S, D, v.stride_b, v.stride_h, v.stride_s, C::CE, BN,
+      !make_map_bhsd(&p.tm_v, v.ptr, B, Hkv, S, D, v.stride_b, v.stride_h, v.stride_s, C::CE, C::BN,
                      C::SW)) {
     autosp_set_error("attn_fwd: cuTensorMapEncodeTiled failed (alignment/strides?)");
     return AUTOSP_ERR_VALIDATION;
@@ -532,7 +545,7 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   p.S = S;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.causal = causal;
-  p.n_qblk = (S + 2 * BM - 1) / (2 * BM);
+  p.n_qblk = (S + C::NQ * BM - 1) / (C::NQ * BM);
   p.trace = g_fwd_trace;
   static bool attr_set = false;
   if (!attr_set) {
@@ -540,7 +553,7 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
     attr_set = true;
   }
   dim3 grid(p.n_qblk, Hq, B);
-  attn_fwd_kernel<D><<<grid, kThreads, C::SMEM, stream>>>(p);
+  attn_fwd_kernel<D><<<grid, C::kThreads, C::SMEM, stream>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     autosp_set_error("attn_fwd launch failed: %s", cudaGetErrorString(e));
