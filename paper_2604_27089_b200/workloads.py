@@ -135,6 +135,9 @@ def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
     return torch.cat((x1 * c - x2 * s_, x2 * c + x1 * s_), dim=-1)
 
 
+MLP_CHUNK = 32768  # tokens per MLP chunk above which the MLP runs chunked (memory only)
+
+
 class LlamaBlock(nn.Module):
     def __init__(self, cfg: LlamaConfig, dtype, device, fused: bool = True):
         super().__init__()
@@ -170,7 +173,12 @@ class LlamaBlock(nn.Module):
         if self.fused:
             from . import ops
             h = ops.rms_norm(x, self.norm2, cfg.eps)
-            return x + ops.swiglu(h @ self.w13.t()) @ self.w2.t()
+            if s <= MLP_CHUNK:
+                return x + ops.swiglu(h @ self.w13.t()) @ self.w2.t()
+            # long contexts: the MLP in sequence chunks, so its [s, 2*d_ffn] intermediate
+            # (and, under sp_ac, its recomputation in backward) is live one chunk at a time
+            return x + torch.cat([ops.swiglu(hc @ self.w13.t()) @ self.w2.t()
+                                  for hc in h.split(MLP_CHUNK, dim=1)], dim=1)
         h = rmsnorm(x, self.norm2, cfg.eps)
         g, u = (h @ self.w13.t()).chunk(2, dim=-1)
         return x + (F.silu(g) * u) @ self.w2.t()
