@@ -14,6 +14,7 @@ auto_sp pass finds their ``scaled_dot_product_attention`` calls and position ind
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -136,6 +137,7 @@ def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
 
 
 MLP_CHUNK = 32768  # tokens per MLP chunk above which the MLP runs chunked (memory only)
+FUSE_RESIDUAL = os.environ.get("AUTOSP_FUSE_RESIDUAL", "1") == "1"  # addmm epilogue adds
 
 
 class LlamaBlock(nn.Module):
@@ -169,10 +171,18 @@ class LlamaBlock(nn.Module):
             v = qkv[:, :, cfg.hq + cfg.hkv:]
         o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
                                            v.transpose(1, 2), is_causal=True, enable_gqa=True)
-        x = x + o.transpose(1, 2).reshape(b, s, cfg.hq * hd) @ self.wo.t()
+        if self.fused and FUSE_RESIDUAL:  # residual adds in the GEMM epilogue (beta = 1)
+            d = cfg.d_model
+            x = torch.addmm(x.reshape(b * s, d), o.transpose(1, 2).reshape(b * s, cfg.hq * hd),
+                            self.wo.t()).view(b, s, d)
+        else:
+            x = x + o.transpose(1, 2).reshape(b, s, cfg.hq * hd) @ self.wo.t()
         if self.fused:
             from . import ops
             h = ops.rms_norm(x, self.norm2, cfg.eps)
+            if s <= MLP_CHUNK and FUSE_RESIDUAL:
+                return torch.addmm(x.reshape(b * s, d), ops.swiglu(h @ self.w13.t()).view(b * s, -1),
+                                   self.w2.t()).view(b, s, d)
             if s <= MLP_CHUNK:
                 return x + ops.swiglu(h @ self.w13.t()) @ self.w2.t()
             # long contexts: the MLP in sequence chunks, so its [s, 2*d_ffn] intermediate
