@@ -45,8 +45,8 @@ constexpr int BQ = 128;  // queries per step
 constexpr int kThreads = 512;
 // Warp roles (the issue arbiter favours higher warp ids: the single-thread TMA / MMA
 // producers sit on top, the dQ drain above the instruction-heavy softmax warpgroups).
-constexpr int kSoftWarp0 = 0;   // warps 0-3: query columns [0,64), 4-7: [64,128)
-constexpr int kDrainWarp0 = 8;  // warps 8-11
+constexpr int kSoftWarp0 = 4;   // warps 4-7: query columns [0,64), 8-11: [64,128)
+constexpr int kDrainWarp0 = 0;  // warps 0-3 (lowest priority: the drain has a step of slack)
 constexpr int kAllocWarp = 12;
 constexpr int kTmaWarp = 14;
 constexpr int kMmaWarp = 15;
