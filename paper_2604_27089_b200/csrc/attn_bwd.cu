@@ -35,6 +35,9 @@ int autosp_check_attn_tensor(const autosp_attn_tensor& t, const char* name);
 #ifndef AUTOSP_BWD_EMU
 #define AUTOSP_BWD_EMU 2  // exps per 8 on the FMA pipe for d <= 64 (tools/emu sweep)
 #endif
+#ifndef AUTOSP_BWD_EMU128
+#define AUTOSP_BWD_EMU128 1  // exps per 8 on the FMA pipe for d = 128
+#endif
 
 namespace autosp {
 namespace bwd {
@@ -76,7 +79,7 @@ struct Cfg {
   // S^T buffers in TMEM: two (S(t+1) overlaps the softmax of t) when d <= 64
   static constexpr int NSB = D == 128 ? 1 : 2;
   // exps per 8 done on the FMA pipe (part 1 is MUFU-bound at 16 exp/clk/SM)
-  static constexpr int kEmuPer8 = D == 128 ? 1 : AUTOSP_BWD_EMU;
+  static constexpr int kEmuPer8 = D == 128 ? AUTOSP_BWD_EMU128 : AUTOSP_BWD_EMU;
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = TILE;
   static constexpr int Q_OFF = 2 * TILE;                       // Q[st]

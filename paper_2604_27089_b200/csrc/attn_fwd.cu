@@ -29,6 +29,9 @@ extern "C" void autosp_set_error(const char* fmt, ...);
 #ifndef AUTOSP_FWD_EMU
 #define AUTOSP_FWD_EMU 3  // exps per 8 on the FMA pipe for d <= 64
 #endif
+#ifndef AUTOSP_FWD_EMU128
+#define AUTOSP_FWD_EMU128 2  // exps per 8 on the FMA pipe for d = 128
+#endif
 
 namespace autosp {
 namespace fwd {
@@ -73,7 +76,7 @@ struct Cfg {
   static constexpr int kStages = kStagesRaw < 2 ? 2 : (kStagesRaw > 8 ? 8 : kStagesRaw);
   // exps per 8 computed by the FMA-pipe polynomial instead of MUFU (MUFU is the
   // bottleneck when the tile's MMA work is small: d = 32 / 64)
-  static constexpr int kEmuPer8 = D == 128 ? 2 : AUTOSP_FWD_EMU;
+  static constexpr int kEmuPer8 = D == 128 ? AUTOSP_FWD_EMU128 : AUTOSP_FWD_EMU;
   static constexpr int LAYOUT = SW == 128 ? 2 : (SW == 64 ? 4 : 6);
   static constexpr int SBO = 8 * SW;  // 8-row swizzle atom
   // smem: Q[NQ] | K[kStages] | V[kStages] | barriers
