@@ -595,412 +595,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   if (warp == kAllocWarp) tmem_dealloc<512>(tmem);
 }
 
-// ---------------------------------------------------------------------------- v4 (d <= 64)
-// Same math, more softmax parallelism for the small head dims where the per-step MMA work
-// is short: FOUR softmax-grad warpgroups (each owns 32 query columns) instead of two, a
-// single S^T buffer (S^T(t+1) is issued right after dV(t) and overlaps the dS math of t),
-// and a dedicated dQ TMEM region.  Each group writes its bf16 P^T / dS^T into the first 16
-// columns of the 32 it read itself, so no group overwrites scores another still reads.
-namespace v4 {
-constexpr int kSoftWarps = 16;   // warps 0-15: group g = warp / 4 owns query cols [32g, 32g+32)
-constexpr int kDrainWarp0 = 16;  // warps 16-19
-constexpr int kTmaWarp = 20;     // also allocates TMEM
-constexpr int kMmaWarp = 21;
-constexpr int kThreads = 22 * 32;
-template <int D>
-struct Tm {
-  static constexpr uint32_t S = 0, DP = 128, DV = 256, DK = 256 + D, DQ = 256 + 2 * D;
-  static_assert(DQ + D <= 512, "TMEM budget");
-};
-__device__ __forceinline__ uint32_t pk_col(int kk) { return 32 * (kk >> 1) + 8 * (kk & 1); }
-}  // namespace v4
-
-template <int D>
-__global__ void __launch_bounds__(v4::kThreads, 1) attn_bwd_kernel_v4(const __grid_constant__ Params p) {
-  using C = Cfg<D>;
-  using TM = v4::Tm<D>;
-  static_assert(D <= 64, "v4 is the small-head-dim variant");
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
-  uint64_t* kv_full = bars + 0;
-  uint64_t* q_full = bars + 1;                  // [kQStages]
-  uint64_t* q_empty = q_full + C::kQStages;     // [kQStages]
-  uint64_t* s_full = q_empty + C::kQStages;
-  uint64_t* dp_full = s_full + 1;
-  uint64_t* p_ready = dp_full + 1;              // 512 arrivals
-  uint64_t* ds_ready = p_ready + 1;             // 512 arrivals
-  uint64_t* dq_full = ds_ready + 1;
-  uint64_t* dq_empty = dq_full + 1;             // 128 arrivals
-  uint64_t* acc_full = dq_empty + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_full + 1);
-  float* lse_s = reinterpret_cast<float*>(smem + C::LSE_OFF);  // [kQStages][128]
-  float* dlt_s = lse_s + C::kQStages * 128;
-
-  const int warp = warp_id();
-  const int lane = lane_id();
-  const int kvh = blockIdx.y;
-  const int batch = blockIdx.z;
-  const int group = p.Hq / p.Hkv;
-  const int k0 = blockIdx.x * BK;
-  const int n_qtiles = (p.S + BQ - 1) / BQ;
-  const int m_first = p.causal ? (k0 / BQ) : 0;
-  const int per_head = n_qtiles - m_first;
-  const int T = per_head * group;
-
-  if (warp == v4::kTmaWarp) {
-    if (lane == 0) {
-      mbar_init(kv_full, 1);
-      for (int s = 0; s < C::kQStages; ++s) {
-        mbar_init(q_full + s, 1);
-        mbar_init(q_empty + s, 1);
-      }
-      mbar_init(s_full, 1);
-      mbar_init(dp_full, 1);
-      mbar_init(p_ready, 16);
-      mbar_init(ds_ready, 16);
-      mbar_init(dq_full, 1);
-      mbar_init(dq_empty, 4);
-      mbar_init(acc_full, 1);
-      fence_mbar_init();
-      tma_prefetch_desc(&p.tm_q);
-      tma_prefetch_desc(&p.tm_k);
-      tma_prefetch_desc(&p.tm_v);
-      tma_prefetch_desc(&p.tm_do);
-      tma_prefetch_desc(&p.tm_dqacc);
-      if (p.lse_tma) {
-        tma_prefetch_desc(&p.tm_lse);
-        tma_prefetch_desc(&p.tm_dlt);
-      }
-    }
-    __syncwarp();
-    tmem_alloc<512>(tmem_holder);
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
-  const uint32_t s_k = smem_u32(smem + C::K_OFF);
-  const uint32_t s_v = smem_u32(smem + C::V_OFF);
-  const uint32_t s_q = smem_u32(smem + C::Q_OFF);
-  const uint32_t s_do = smem_u32(smem + C::DO_OFF);
-  const uint32_t s_ds = smem_u32(smem + C::DS_OFF);
-
-  if (warp == v4::kTmaWarp) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && T > 0) {
-      const uint64_t pol_last = policy_evict_last();
-      mbar_arrive_expect_tx(kv_full, 2 * C::TILE);
-      for (int c = 0; c < C::NCH; ++c) {
-        tma_load_4d(smem + C::K_OFF + c * 128 * C::SW, &p.tm_k, kv_full, c * C::CE, k0, kvh,
-                    batch, pol_last);
-        tma_load_4d(smem + C::V_OFF + c * 128 * C::SW, &p.tm_v, kv_full, c * C::CE, k0, kvh,
-                    batch, pol_last);
-      }
-      for (int t = 0; t < T; ++t) {
-        const int st = t % C::kQStages;
-        const uint32_t ph = (t / C::kQStages) & 1;
-        const int head = kvh * group + t / per_head;
-        const int q0 = (m_first + t % per_head) * BQ;
-        mbar_wait(q_empty + st, ph ^ 1);
-        mbar_arrive_expect_tx(q_full + st, 2 * C::TILE + (p.lse_tma ? 2 * 128 * 4 : 0));
-        if (p.lse_tma) {
-          tma_load_2d(lse_s + st * 128, &p.tm_lse, q_full + st, q0, batch * p.Hq + head);
-          tma_load_2d(dlt_s + st * 128, &p.tm_dlt, q_full + st, q0, batch * p.Hq + head);
-        }
-        for (int c = 0; c < C::NCH; ++c) {
-          tma_load_4d(smem + C::Q_OFF + st * C::TILE + c * 128 * C::SW, &p.tm_q, q_full + st,
-                      c * C::CE, q0, head, batch, pol_last);
-          tma_load_4d(smem + C::DO_OFF + st * C::TILE + c * 128 * C::SW, &p.tm_do, q_full + st,
-                      c * C::CE, q0, head, batch, pol_last);
-        }
-      }
-    }
-  } else if (warp == v4::kMmaWarp) {
-    // ------------------------------------------------------------ MMA issuer (whole warp)
-    if (T > 0) {
-      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t idesc_g = make_idesc_bf16(128, D, 0, 1);
-      constexpr uint32_t idesc_q = make_idesc_bf16(128, D, 1, 1);
-      const uint64_t dk_k = make_smem_desc(s_k, 16, C::SBO, C::LAYOUT);
-      const uint64_t dv_k = make_smem_desc(s_v, 16, C::SBO, C::LAYOUT);
-      const uint64_t dk_mn = make_smem_desc(s_k, 128 * C::SW, C::SBO, C::LAYOUT);
-      const uint64_t dds = make_smem_desc(s_ds, 128 * 128, 1024, 2);
-      auto wait_q = [&](int t) {
-        mbar_wait(q_full + (t % C::kQStages), (t / C::kQStages) & 1);
-        tc_fence_after();
-      };
-      auto issue_s = [&](int t) {
-        const uint64_t dq = make_smem_desc(s_q + (t % C::kQStages) * C::TILE, 16, C::SBO, C::LAYOUT);
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            mma_ss(tmem + TM::S, dk_k + kmajor_off<D>(kk), dq + kmajor_off<D>(kk), idesc_s, kk > 0);
-          tc_commit(s_full);
-        }
-        __syncwarp();
-      };
-      mbar_wait(kv_full, 0);
-      wait_q(0);
-      issue_s(0);
-      for (int t = 0; t < T; ++t) {
-        const int st = t % C::kQStages;
-        const uint64_t ddo = make_smem_desc(s_do + st * C::TILE, 16, C::SBO, C::LAYOUT);
-        const uint64_t dq_mn = make_smem_desc(s_q + st * C::TILE, 128 * C::SW, C::SBO, C::LAYOUT);
-        const uint64_t ddo_mn = make_smem_desc(s_do + st * C::TILE, 128 * C::SW, C::SBO, C::LAYOUT);
-        const uint32_t acc0 = t > 0 ? 1u : 0u;
-        // dP^T(t) = V dO(t)^T  (dP region: previous dS consumed by dK(t-1), in-order)
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            mma_ss(tmem + TM::DP, dv_k + kmajor_off<D>(kk), ddo + kmajor_off<D>(kk), idesc_s, kk > 0);
-          tc_commit(dp_full);
-        }
-        __syncwarp();
-        if (lane == 0) BWD_TRACE(1, t);
-        // dV += P^T dO
-        mbar_wait(p_ready, t & 1);
-        if (lane == 0) BWD_TRACE(2, t);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk)
-            mma_ts(tmem + TM::DV, tmem + TM::S + v4::pk_col(kk),
-                   ddo_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_g, kk > 0 ? 1u : acc0);
-        }
-        __syncwarp();
-        // S^T(t+1) right behind dV(t) (which read P(t) from the S columns): it overlaps the
-        // dS math of t on the softmax warps
-        if (t + 1 < T) {
-          wait_q(t + 1);
-          issue_s(t + 1);
-        }
-        // dK += dS^T Q ; dQ(t) = dS K
-        mbar_wait(ds_ready, t & 1);
-        if (lane == 0) BWD_TRACE(3, t);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk)
-            mma_ts(tmem + TM::DK, tmem + TM::DP + v4::pk_col(kk),
-                   dq_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_g, kk > 0 ? 1u : acc0);
-          tc_commit(q_empty + st);
-        }
-        __syncwarp();
-        if (t > 0) {
-          mbar_wait(dq_empty, (t - 1) & 1);
-          if (lane == 0) BWD_TRACE(0, t);
-          tc_fence_after();
-        }
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            mma_ss(tmem + TM::DQ, dds + (uint64_t)((kk * 16 * 128) >> 4),
-                   dk_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_q, kk > 0);
-          tc_commit(dq_full);
-        }
-        __syncwarp();
-        if (lane == 0) BWD_TRACE(4, t);
-      }
-      if (elect_one()) tc_commit(acc_full);
-      __syncwarp();
-    }
-  } else if (warp < v4::kSoftWarps) {
-    // ------------------------------------------------------------ softmax-grad groups
-    const int g = warp >> 2;         // query-column group: cols [32g, 32g+32)
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const int key = k0 + row;
-    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t s_addr = tmem + lane_base + TM::S;
-    const uint32_t dp_addr = tmem + lane_base + TM::DP;
-    uint8_t* ds_row = smem + C::DS_OFF + (g >> 1) * (128 * 128) + row * 128;
-    const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
-    const bool row_dead = key >= p.S;
-    for (int t = 0; t < T; ++t) {
-      const int head = kvh * group + t / per_head;
-      const int q0 = (m_first + t % per_head) * BQ;
-      const int st = t % C::kQStages;
-      const float* lse_b = lse_s + st * 128 + 32 * g;
-      const float* dlt_b = dlt_s + st * 128 + 32 * g;
-      if (!p.lse_tma) {  // S % 4 != 0: stage lse/delta through registers (slow path)
-        if (t >= C::kQStages) named_bar_sync(1, 512);
-        if (g == 0) {
-          const int q = q0 + row;
-          const int64_t idx = ((int64_t)batch * p.Hq + head) * p.S + q;
-          lse_s[st * 128 + row] = q < p.S ? p.lse[idx] : 0.f;
-          dlt_s[st * 128 + row] = q < p.S ? p.delta[idx] : 0.f;
-        }
-        named_bar_sync(1, 512);
-      }
-      const bool masked = (p.causal && (q0 < k0 + BK)) || (k0 + BK > p.S) || (q0 + BQ > p.S);
-      const int col_lo = (p.causal ? key - q0 : -1) - 32 * g;  // relative to this group
-      const int col_hi = min(p.S - q0, BQ) - 32 * g;
-      mbar_wait(s_full, t & 1);
-      if (threadIdx.x == 0) BWD_TRACE(5, t);
-      tc_fence_after();
-      uint32_t pk[16];
-      {
-        uint32_t sr[32];
-        tmem_ld32(s_addr + 32 * g, sr);
-        tmem_wait_ld();
-        auto body = [&](auto kMasked) {
-#pragma unroll
-          for (int c8 = 0; c8 < 8; ++c8) {
-            const float4 l = lds128(reinterpret_cast<const float4*>(lse_b) + c8);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int c = c8 * 2 + h;
-              const uint64_t lz = h ? f2_pack(l.z, l.w) : f2_pack(l.x, l.y);
-              const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(sr[2 * c]),
-                                                 __uint_as_float(sr[2 * c + 1])),
-                                         sl2, lz);  // lz = -lse*log2(e) (bwd_pre)
-              float e0, e1;
-              if (!decltype(kMasked)::value && (c & 7) >= 8 - C::kEmuPer8) {
-                f2_unpack(f2_exp2_poly(x2), e0, e1);
-              } else {
-                float x0, x1;
-                f2_unpack(x2, x0, x1);
-                e0 = fast_exp2(x0);
-                e1 = fast_exp2(x1);
-              }
-              if constexpr (decltype(kMasked)::value) {
-                const int col = 2 * c;
-                e0 = (row_dead || col < col_lo || col >= col_hi) ? 0.f : e0;
-                e1 = (row_dead || col + 1 < col_lo || col + 1 >= col_hi) ? 0.f : e1;
-              }
-              pk[c] = pack_bf16(e0, e1);
-            }
-          }
-        };
-        if (masked) body(std::true_type{});
-        else body(std::false_type{});
-      }
-      tmem_st16(s_addr + 32 * g, pk);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive_warp(p_ready);
-      if (threadIdx.x == 0) BWD_TRACE(6, t);
-      mbar_wait(dp_full, t & 1);  // also: dQ(t-1) finished reading the smem dS tile
-      if (threadIdx.x == 0) BWD_TRACE(7, t);
-      tc_fence_after();
-      {
-        uint32_t dr[32], dk[16];
-        tmem_ld32(dp_addr + 32 * g, dr);
-        tmem_wait_ld();
-        if (threadIdx.x == 0) BWD_TRACE(11, t);
-#pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) {
-          float4 dl = lds128(reinterpret_cast<const float4*>(dlt_b) + c8);
-          if (masked) {
-            const int col = 4 * c8;
-            dl.x = col + 0 < col_hi ? dl.x : 0.f;
-            dl.y = col + 1 < col_hi ? dl.y : 0.f;
-            dl.z = col + 2 < col_hi ? dl.z : 0.f;
-            dl.w = col + 3 < col_hi ? dl.w : 0.f;
-          }
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = c8 * 2 + h;
-            const uint64_t dd = f2_add(f2_pack(__uint_as_float(dr[2 * c]), __uint_as_float(dr[2 * c + 1])),
-                                       h ? f2_pack(-dl.z, -dl.w) : f2_pack(-dl.x, -dl.y));
-            float a, b;
-            f2_unpack(dd, a, b);
-            dk[c] = bf16x2_mul(pk[c], pack_bf16(a, b));
-          }
-        }
-        tmem_st16(dp_addr + 32 * g, dk);
-        if (threadIdx.x == 0) BWD_TRACE(12, t);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int unit = (g & 1) * 4 + u;
-          sts128(ds_row + ((unit ^ (row & 7)) << 4),
-                 make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
-        }
-      }
-      if (threadIdx.x == 0) BWD_TRACE(13, t);
-      tmem_wait_st();
-      if (threadIdx.x == 0) BWD_TRACE(14, t);
-      fence_proxy_async_smem();
-      if (threadIdx.x == 0) BWD_TRACE(15, t);
-      tc_fence_before();
-      mbar_arrive_warp(ds_ready);
-      if (threadIdx.x == 0) BWD_TRACE(8, t);
-    }
-    // ---- epilogue: group 0 writes dV, group 1 writes dK (scaled)
-    if (T > 0 && g < 2) {
-      mbar_wait(acc_full, 0);
-      tc_fence_after();
-      const uint32_t src = tmem + lane_base + (g ? TM::DK : TM::DV);
-      const float sc = g ? p.scale : 1.f;
-      __nv_bfloat16* dst =
-          g ? p.dk + (int64_t)batch * p.dk_sb + (int64_t)kvh * p.dk_sh + (int64_t)key * p.dk_ss
-            : p.dv + (int64_t)batch * p.dv_sb + (int64_t)kvh * p.dv_sh + (int64_t)key * p.dv_ss;
-#pragma unroll
-      for (int c = 0; c < D; c += 32) {
-        uint32_t a[32];
-        tmem_ld32(src + c, a);
-        tmem_wait_ld();
-        if (key < p.S) {
-#pragma unroll
-          for (int t4 = 0; t4 < 4; ++t4) {
-            uint4 va;
-            va.x = pack_bf16(__uint_as_float(a[8 * t4 + 0]) * sc, __uint_as_float(a[8 * t4 + 1]) * sc);
-            va.y = pack_bf16(__uint_as_float(a[8 * t4 + 2]) * sc, __uint_as_float(a[8 * t4 + 3]) * sc);
-            va.z = pack_bf16(__uint_as_float(a[8 * t4 + 4]) * sc, __uint_as_float(a[8 * t4 + 5]) * sc);
-            va.w = pack_bf16(__uint_as_float(a[8 * t4 + 6]) * sc, __uint_as_float(a[8 * t4 + 7]) * sc);
-            reinterpret_cast<uint4*>(dst + c)[t4] = va;
-          }
-        }
-      }
-    }
-  } else if (warp >= v4::kDrainWarp0 && warp < v4::kDrainWarp0 + 4) {
-    // ------------------------------------------------------------ dQ drain warpgroup
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const bool leader = (warp == v4::kDrainWarp0 && lane == 0);
-    const uint32_t dq_addr = tmem + lane_base + TM::DQ;
-    for (int t = 0; t < T; ++t) {
-      const int head = kvh * group + t / per_head;
-      const int q0 = (m_first + t % per_head) * BQ;
-      mbar_wait(dq_full, t & 1);
-      if (threadIdx.x == v4::kDrainWarp0 * 32) BWD_TRACE(9, t);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        const int chunk_id = t * (D / 32) + c;
-        float* slot = reinterpret_cast<float*>(smem + C::DQ_OFF) + (chunk_id & 1) * (128 * 32);
-        uint32_t v[32];
-        tmem_ld32(dq_addr + c * 32, v);
-        if (leader) bulk_wait_read1();
-        named_bar_sync(2, 128);
-        tmem_wait_ld();
-        if (c == D / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive_warp(dq_empty);
-        }
-        uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          sts128(srow + ((u ^ (row & 7)) << 4),
-                 make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]));
-        fence_proxy_async_smem();
-        named_bar_sync(2, 128);
-        if (leader) {
-          tma_reduce_add_3d(&p.tm_dqacc, slot, c * 32, q0, batch * p.Hq + head);
-          bulk_commit();
-        }
-      }
-      if (threadIdx.x == v4::kDrainWarp0 * 32) BWD_TRACE(10, t);
-    }
-    if (leader) bulk_wait0();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == v4::kTmaWarp) tmem_dealloc<512>(tmem);
-}
 
 // ---------------------------------------------------------------------------- pre / post
 struct PrePost {
@@ -1168,22 +762,11 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   p.causal = causal;
   p.n_ktiles = (S + BK - 1) / BK;
   static bool attr_set = false;
-  static const bool use_v4 = getenv("AUTOSP_BWD_V4") && getenv("AUTOSP_BWD_V4")[0] == '1';
-  if (D <= 64 && use_v4) {  // experimental 4-group variant (tools/attn_bench.py A/B)
-    if (!attr_set) {
-      cudaFuncSetAttribute(attn_bwd_kernel_v4<(D <= 64 ? D : 64)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           C::SMEM);
-      attr_set = true;
-    }
-    attn_bwd_kernel_v4<(D <= 64 ? D : 64)><<<dim3(p.n_ktiles, Hkv, B), v4::kThreads, C::SMEM, stream>>>(p);
-  } else {
-    if (!attr_set) {
-      cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           C::SMEM);
-      attr_set = true;
-    }
-    attn_bwd_kernel<D><<<dim3(p.n_ktiles, Hkv, B), kThreads, C::SMEM, stream>>>(p);
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr_set = true;
   }
+  attn_bwd_kernel<D><<<dim3(p.n_ktiles, Hkv, B), kThreads, C::SMEM, stream>>>(p);
   {
     const int64_t threads = a.rows * (D / 8);
     bwd_post_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(a);
@@ -1249,8 +832,6 @@ int autosp_preload_bwd() {
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<32>);
   cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<64>);
-  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel_v4<32>);
-  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel_v4<64>);
   cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<128>);
   cudaFuncGetAttributes(&a, autosp::bwd::bwd_pre_kernel);
   cudaFuncGetAttributes(&a, autosp::bwd::bwd_post_kernel);
