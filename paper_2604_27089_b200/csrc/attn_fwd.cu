@@ -365,6 +365,75 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
         return fmaxf(fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]), mx8[6]),
                      mx8[7]);
       };
+      if (C::SEP_P && j > 0 && !need_mask) {
+        // Optimistic single pass (the common case): exps against the RUNNING max m, the
+        // row max tracked in the same pass -- no separate max pass re-reading S from TMEM.
+        // Only if some row's max grew by more than 2^8 (exp2 arguments beyond +8) is the
+        // tile redone exactly like the two-pass path below (warp-uniform decision).
+        mbar_wait(o_done + i, (j - 1) & 1);  // PV_i(j-1) done with the P_i buffer
+        tc_fence_after();
+        const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
+        const uint64_t nm2 = f2_pack(-m, -m);
+        uint64_t rs2[4] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f),
+                           f2_pack(0.f, 0.f)};
+        float mx4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mx4[k] = -INFINITY;
+        bool redo = false;
+#pragma unroll
+        for (int h = 0; h < C::NH; ++h) {
+          uint32_t sr[64];
+          tmem_ld32(s_addr + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+          tmem_ld32(s_addr + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 64; c += 2)
+            mx4[(c >> 1) & 3] = fmax3(mx4[(c >> 1) & 3], __uint_as_float(sr[c]),
+                                      __uint_as_float(sr[c + 1]));
+          if (h == C::NH - 1) {  // whole row seen: decide, then release S_i
+            const float mxr = fmaxf(fmax3(mx4[0], mx4[1], mx4[2]), mx4[3]);
+            redo = __any_sync(0xffffffffu, mxr * p.scale_log2 > m + 8.f);
+            if (redo) break;  // S_i stays: the two-pass path re-reads it
+            tc_fence_before();
+            mbar_arrive_warp(s_free + i);
+            if (lane == 0 && warp == 0) FWD_TRACE(15, j);
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(sr[q * 32 + 2 * c]),
+                                                 __uint_as_float(sr[q * 32 + 2 * c + 1])),
+                                         sl2, nm2);
+              uint64_t e2;
+              if ((c & 7) >= 8 - C::kEmuPer8) {
+                e2 = f2_exp2_poly(x2);  // FMA pipe
+              } else {
+                float x0, x1;
+                f2_unpack(x2, x0, x1);
+                e2 = f2_pack(fast_exp2(x0), fast_exp2(x1));  // MUFU
+              }
+              rs2[c & 3] = f2_add(rs2[c & 3], e2);
+              float ea, eb;
+              f2_unpack(e2, ea, eb);
+              pk[c] = pack_bf16(ea, eb);
+            }
+            tmem_st16(p_addr + (h * 2 + q) * 16, pk);
+          }
+        }
+        if (!redo) {
+          float r0, r1;
+          f2_unpack(f2_add(f2_add(rs2[0], rs2[1]), f2_add(rs2[2], rs2[3])), r0, r1);
+          l += r0 + r1;
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive_warp(p_full + i);
+          if (lane == 0 && (warp & 3) == 0) FWD_TRACE(6 + i, j);
+          if (lane == 0 && i == 0) FWD_TRACE(8 + (warp & 3), j);
+          continue;
+        }
+      }
       const float mx = need_mask ? pass1(std::true_type{}) : pass1(std::false_type{});
       const float m_cand = mx * p.scale_log2;
       if (m_cand > m + 8.f) {  // lazy rescale (also taken on the first tile)
