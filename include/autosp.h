@@ -154,7 +154,8 @@ AUTOSP_API int autosp_attn_fwd(autosp_attn_tensor q, autosp_attn_tensor k, autos
  * dst_offset + 2 * (b * dst_stride_b + (t mod s/world) * dst_stride_s
  *                   + (rank * hq + h) * dst_stride_h)
  * of its receive region.  Publishes arrive flags like autosp_a2a; the caller then runs
- * autosp_a2a_wait.  Replaces the autosp_attn_fwd + autosp_a2a(head_to_seq) pair. */
+ * autosp_a2a_wait.  Replaces the autosp_attn_fwd + autosp_a2a(head_to_seq) pair.
+ * o.ptr may be NULL: only the pushed (token-major) copy is written. */
 typedef struct autosp_push_spec {
   int world, rank;
   int64_t dst_offset;                          /* bytes, identical on every rank */
@@ -177,6 +178,16 @@ AUTOSP_API int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autos
                     autosp_attn_tensor dq, autosp_attn_tensor dk, autosp_attn_tensor dv,
                     void* workspace, int b, int hq, int hkv, int s, int d, float scale,
                     int causal, void* stream);
+
+/* autosp_attn_bwd with delta[b, hq, s] = rowsum(dO * O) (fp32, contiguous) supplied by the
+ * caller instead of O: the Ulysses backward forms delta on the token owner from the
+ * token-major output it keeps anyway and reshards it with dO, so the head-major O need
+ * not be kept for the backward. */
+AUTOSP_API int autosp_attn_bwd_delta(autosp_attn_tensor q, autosp_attn_tensor k,
+                    autosp_attn_tensor v, const float* delta, autosp_attn_tensor d_o,
+                    const float* lse, autosp_attn_tensor dq, autosp_attn_tensor dk,
+                    autosp_attn_tensor dv, void* workspace, int b, int hq, int hkv, int s, int d,
+                    float scale, int causal, void* stream);
 
 /* ------------------------------------------------------------------ fused elementwise
  * HBM-bound bf16 kernels for the layer around the Ulysses path (fp32 math):

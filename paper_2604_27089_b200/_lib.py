@@ -100,6 +100,9 @@ EXPORTS = {
     "autosp_attn_bwd_workspace_bytes": (C.c_size_t, [C.c_int] * 4),
     "autosp_attn_bwd": (C.c_int, [AttnTensor] * 5 + [C.c_void_p] + [AttnTensor] * 3 +
                         [C.c_void_p] + [C.c_int] * 5 + [C.c_float, C.c_int, C.c_void_p]),
+    "autosp_attn_bwd_delta": (C.c_int, [AttnTensor] * 3 + [C.c_void_p, AttnTensor, C.c_void_p] +
+                              [AttnTensor] * 3 + [C.c_void_p] + [C.c_int] * 5 +
+                              [C.c_float, C.c_int, C.c_void_p]),
 }
 
 

@@ -606,6 +606,7 @@ struct PrePost {
   float* delta;
   const float* lse;  // forward LSE (natural log)
   float* nlse2;      // -lse * log2(e): the exp2 argument offset the softmax-grad warps use
+  int delta_given;   // 1: delta supplied by the caller (no O needed), only dQacc / nlse2
   int Hq, S, D;
   int64_t rows;
   float scale;
@@ -621,7 +622,7 @@ __global__ void bwd_pre_kernel(const __grid_constant__ PrePost a) {
   const int64_t row = warp * rpw + lane / lpr;
   const int sub = lane % lpr;
   float acc = 0.f;
-  if (row < a.rows) {
+  if (row < a.rows && !a.delta_given) {
     const int64_t bh = row / a.S;
     const int q = (int)(row % a.S);
     const int h = (int)(bh % a.Hq);
@@ -638,13 +639,15 @@ __global__ void bwd_pre_kernel(const __grid_constant__ PrePost a) {
       const float2 y = __bfloat1622float2(g2[i]);
       acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
     }
+  }
+  if (row < a.rows) {
     float4* z = reinterpret_cast<float4*>(a.dqacc + row * a.D + sub * 8);
     z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
     z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   for (int off = lpr / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (row < a.rows && sub == 0) {
-    a.delta[row] = acc;
+    if (!a.delta_given) a.delta[row] = acc;
     a.nlse2[row] = -a.lse[row] * 1.4426950408889634f;
   }
 }
@@ -702,11 +705,11 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
            const autosp_attn_tensor& o, const autosp_attn_tensor& d_o, const float* lse,
            const autosp_attn_tensor& dq, const autosp_attn_tensor& dk,
            const autosp_attn_tensor& dv, void* ws, int B, int Hq, int Hkv, int S, float scale,
-           int causal, cudaStream_t stream) {
+           int causal, const float* delta_in, cudaStream_t stream) {
   using C = Cfg<D>;
   float* dqacc = static_cast<float*>(ws);
-  float* delta = dqacc + (size_t)B * Hq * S * D;
-  float* nlse2 = delta + (size_t)B * Hq * S;
+  float* delta = delta_in ? const_cast<float*>(delta_in) : dqacc + (size_t)B * Hq * S * D;
+  float* nlse2 = dqacc + (size_t)B * Hq * S * D + (size_t)B * Hq * S;
   PrePost a{};
   a.o = static_cast<const __nv_bfloat16*>(o.ptr);
   a.d_o = static_cast<const __nv_bfloat16*>(d_o.ptr);
@@ -718,6 +721,7 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   a.delta = delta;
   a.lse = lse;
   a.nlse2 = nlse2;
+  a.delta_given = delta_in ? 1 : 0;
   a.Hq = Hq;
   a.S = S;
   a.D = D;
@@ -786,18 +790,50 @@ extern "C" size_t autosp_attn_bwd_workspace_bytes(int b, int hq, int s, int d) {
   return (size_t)b * hq * s * (d + 2) * sizeof(float);  // dQ acc + delta + -lse*log2(e)
 }
 
+static int attn_bwd_impl(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
+                         autosp_attn_tensor o, const float* delta, autosp_attn_tensor d_o,
+                         const float* lse, autosp_attn_tensor dq, autosp_attn_tensor dk,
+                         autosp_attn_tensor dv, void* workspace, int b, int hq, int hkv, int s,
+                         int d, float scale, int causal, void* stream);
+
 extern "C" int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
                                autosp_attn_tensor o, autosp_attn_tensor d_o, const float* lse,
                                autosp_attn_tensor dq, autosp_attn_tensor dk,
                                autosp_attn_tensor dv, void* workspace, int b, int hq, int hkv,
                                int s, int d, float scale, int causal, void* stream) {
+  int rc;
+  if ((rc = autosp_check_attn_tensor(o, "o"))) return rc;
+  return attn_bwd_impl(q, k, v, o, nullptr, d_o, lse, dq, dk, dv, workspace, b, hq, hkv, s, d,
+                       scale, causal, stream);
+}
+
+extern "C" int autosp_attn_bwd_delta(autosp_attn_tensor q, autosp_attn_tensor k,
+                                     autosp_attn_tensor v, const float* delta,
+                                     autosp_attn_tensor d_o, const float* lse,
+                                     autosp_attn_tensor dq, autosp_attn_tensor dk,
+                                     autosp_attn_tensor dv, void* workspace, int b, int hq,
+                                     int hkv, int s, int d, float scale, int causal,
+                                     void* stream) {
+  if (!delta || (reinterpret_cast<uintptr_t>(delta) & 15)) {
+    autosp_set_error("attn_bwd_delta: delta must be non-null and 16-byte aligned");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  return attn_bwd_impl(q, k, v, q /* unused */, delta, d_o, lse, dq, dk, dv, workspace, b, hq,
+                       hkv, s, d, scale, causal, stream);
+}
+
+static int attn_bwd_impl(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
+                         autosp_attn_tensor o, const float* delta, autosp_attn_tensor d_o,
+                         const float* lse, autosp_attn_tensor dq, autosp_attn_tensor dk,
+                         autosp_attn_tensor dv, void* workspace, int b, int hq, int hkv, int s,
+                         int d, float scale, int causal, void* stream) {
   if (b < 1 || hq < 1 || hkv < 1 || s < 1 || hq % hkv) {
     autosp_set_error("attn_bwd: bad shape b=%d hq=%d hkv=%d s=%d", b, hq, hkv, s);
     return AUTOSP_ERR_VALIDATION;
   }
   int rc;
   if ((rc = autosp_check_attn_tensor(q, "q")) || (rc = autosp_check_attn_tensor(k, "k")) ||
-      (rc = autosp_check_attn_tensor(v, "v")) || (rc = autosp_check_attn_tensor(o, "o")) ||
+      (rc = autosp_check_attn_tensor(v, "v")) ||
       (rc = autosp_check_attn_tensor(d_o, "do")) || (rc = autosp_check_attn_tensor(dq, "dq")) ||
       (rc = autosp_check_attn_tensor(dk, "dk")) || (rc = autosp_check_attn_tensor(dv, "dv")))
     return rc;
@@ -809,13 +845,13 @@ extern "C" int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autos
   switch (d) {
     case 32:
       return autosp::bwd::launch<32>(q, k, v, o, d_o, lse, dq, dk, dv, workspace, b, hq, hkv, s,
-                                     scale, causal, st);
+                                     scale, causal, delta, st);
     case 64:
       return autosp::bwd::launch<64>(q, k, v, o, d_o, lse, dq, dk, dv, workspace, b, hq, hkv, s,
-                                     scale, causal, st);
+                                     scale, causal, delta, st);
     case 128:
       return autosp::bwd::launch<128>(q, k, v, o, d_o, lse, dq, dk, dv, workspace, b, hq, hkv, s,
-                                      scale, causal, st);
+                                      scale, causal, delta, st);
     default:
       autosp_set_error("attn_bwd: head_dim %d unsupported (32, 64, 128)", d);
       return AUTOSP_ERR_UNSUPPORTED;

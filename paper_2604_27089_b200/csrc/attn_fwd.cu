@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
                             __uint_as_float(orr[8 * t + 5]) * inv_l);
             v.w = pack_bf16(__uint_as_float(orr[8 * t + 6]) * inv_l,
                             __uint_as_float(orr[8 * t + 7]) * inv_l);
-            dst[t] = v;
+            if (p.o) dst[t] = v;  // (push without a local copy: o == nullptr)
             if (prow) prow[c / 8 + t] = v;
           }
         }
@@ -707,7 +707,8 @@ static int attn_fwd_impl(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn
   }
   int rc;
   if ((rc = autosp_check_attn_tensor(q, "q")) || (rc = autosp_check_attn_tensor(k, "k")) ||
-      (rc = autosp_check_attn_tensor(v, "v")) || (rc = autosp_check_attn_tensor(o, "o")))
+      (rc = autosp_check_attn_tensor(v, "v")) ||
+      ((o.ptr || !push) && (rc = autosp_check_attn_tensor(o, "o"))))
     return rc;
   if (!lse) {
     autosp_set_error("attn_fwd: lse must be non-null");

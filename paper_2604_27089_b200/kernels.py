@@ -112,7 +112,7 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool = T
     return o, lse
 
 
-def attn_fwd_push(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor,
+def attn_fwd_push(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor | None,
                   lse: torch.Tensor, scale: float, causal: bool, world: int, rank: int,
                   dst_offset: int, dst_strides: tuple[int, int, int], peer_base: list[int],
                   peer_flags: list[int], epoch: int) -> None:
@@ -127,8 +127,9 @@ def attn_fwd_push(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Te
     spec = _lib.PushSpec(world, rank, dst_offset, dst_strides[0], dst_strides[1], dst_strides[2],
                          C.cast(pb, C.c_void_p), C.cast(pf, C.c_void_p), epoch & 0xFFFFFFFF)
     ev = LOG.begin("attn_fwd")
+    o_t = _attn_tensor(o, "o") if o is not None else _lib.AttnTensor(None, 0, 0, 0)
     rc = lib.autosp_attn_fwd_push(_attn_tensor(q, "q"), _attn_tensor(k, "k"),
-                                  _attn_tensor(v, "v"), _attn_tensor(o, "o"), lse.data_ptr(), b,
+                                  _attn_tensor(v, "v"), o_t, lse.data_ptr(), b,
                                   hq, hkv, s, d, float(scale), int(causal), C.byref(spec),
                                   _stream())
     _lib.check(rc, "attn_fwd_push")
@@ -136,9 +137,10 @@ def attn_fwd_push(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Te
 
 
 def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = None,
-             dq=None, dk=None, dv=None):
+             dq=None, dk=None, dv=None, delta: torch.Tensor | None = None):
     """Flash attention backward recomputing P from the saved LSE.
-    Returns (dq, dk, dv) in bf16 ([b, h, s, d])."""
+    Returns (dq, dk, dv) in bf16 ([b, h, s, d]).  With `delta` ([b, hq, s] fp32 =
+    rowsum(dO * O)) `o` is not read and may be None (autosp_attn_bwd_delta)."""
     lib = _lib.load()
     b, hq, s, d = q.shape
     hkv = k.shape[1]
@@ -152,11 +154,22 @@ def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = Non
     if not lse.is_contiguous() or lse.dtype != torch.float32:
         raise ValidationError("attn_bwd: lse must be contiguous fp32 [b, hq, s]")
     ev = LOG.begin("attn_bwd")
-    rc = lib.autosp_attn_bwd(_attn_tensor(q, "q"), _attn_tensor(k, "k"), _attn_tensor(v, "v"),
-                             _attn_tensor(o, "o"), _attn_tensor(do, "do"), lse.data_ptr(),
-                             _attn_tensor(dq, "dq"), _attn_tensor(dk, "dk"),
-                             _attn_tensor(dv, "dv"), ws.data_ptr(), b, hq, hkv, s, d,
-                             float(scale), int(causal), _stream())
+    if delta is None:
+        rc = lib.autosp_attn_bwd(_attn_tensor(q, "q"), _attn_tensor(k, "k"), _attn_tensor(v, "v"),
+                                 _attn_tensor(o, "o"), _attn_tensor(do, "do"), lse.data_ptr(),
+                                 _attn_tensor(dq, "dq"), _attn_tensor(dk, "dk"),
+                                 _attn_tensor(dv, "dv"), ws.data_ptr(), b, hq, hkv, s, d,
+                                 float(scale), int(causal), _stream())
+    else:
+        if delta.dtype != torch.float32 or not delta.is_contiguous() or \
+                tuple(delta.shape) != (b, hq, s):
+            raise ValidationError("attn_bwd: delta must be contiguous fp32 [b, hq, s]")
+        rc = lib.autosp_attn_bwd_delta(_attn_tensor(q, "q"), _attn_tensor(k, "k"),
+                                       _attn_tensor(v, "v"), delta.data_ptr(),
+                                       _attn_tensor(do, "do"), lse.data_ptr(),
+                                       _attn_tensor(dq, "dq"), _attn_tensor(dk, "dk"),
+                                       _attn_tensor(dv, "dv"), ws.data_ptr(), b, hq, hkv, s, d,
+                                       float(scale), int(causal), _stream())
     _lib.check(rc, "attn_bwd")
     LOG.end("attn_bwd", ev, 3, 2.5 * causal_attn_flops(b, hq, s, d, causal))
     return dq, dk, dv

@@ -67,6 +67,22 @@ def _attention_backward_fake(do, q, k, v, o, lse, scale, causal):
     return (q.new_empty(q.shape), k.new_empty(k.shape), v.new_empty(v.shape))
 
 
+@torch.library.custom_op("autosp::attention_backward_delta", mutates_args=(), device_types="cuda")
+def attention_backward_delta(do: torch.Tensor, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                             delta: torch.Tensor, lse: torch.Tensor, scale: float,
+                             causal: bool) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """attention_backward with delta = rowsum(dO * O) supplied (no O needed)."""
+    if do.stride(-1) != 1:
+        do = do.contiguous()
+    return kernels.attn_bwd(q, k, v, None, do, lse, causal=causal, scale=scale,
+                            delta=delta.float().contiguous())
+
+
+@attention_backward_delta.register_fake
+def _attention_backward_delta_fake(do, q, k, v, delta, lse, scale, causal):
+    return (q.new_empty(q.shape), k.new_empty(k.shape), v.new_empty(v.shape))
+
+
 def _attn_setup(ctx, inputs, output):
     q, k, v, scale, causal = inputs
     o, lse = output
@@ -186,25 +202,25 @@ all_to_all.register_autograd(_a2a_bwd, setup_context=_a2a_setup)
 # ----------------------------------------------------------------------------- fused K3 + K2
 @torch.library.custom_op("autosp::attention_a2a", mutates_args=(), device_types="cuda")
 def attention_a2a(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: float, causal: bool,
-                  group: str) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+                  group: str) -> tuple[torch.Tensor, torch.Tensor]:
     """Attention over the full sequence on the local heads whose epilogue pushes every
     output row to its token owner (the head->seq all-to-all, sp_pass.py:172-195, fused
     into the producing kernel).  Returns (o_tokens [b, H, s/P, d] token-major = the
-    all-to-all output, o_heads [b, h/P, s, d] (kept for the backward), lse)."""
+    all-to-all output, lse [b, h/P, s]).  No head-major copy of O is kept: the backward
+    forms delta = rowsum(dO * O) on the token owner (see _attn_a2a_bwd)."""
     st = sp_dist.lookup(group)
     P, pool = st.world, st.pool
     b, hl, S, d = q.shape
-    o_head = torch.empty((b, hl, S, d), dtype=q.dtype, device=q.device)
     lse = torch.empty((b, hl, S), dtype=torch.float32, device=q.device)
-    shape, strides = _out_geometry(o_head, HEAD_TO_SEQ_DIR, P)
+    shape, strides = _out_geometry(q, HEAD_TO_SEQ_DIR, P)  # (O has q's shape)
     off, base = pool.alloc(math.prod(shape) * q.element_size())
     o_tok = base.view(q.dtype).as_strided(shape, strides)
     epoch = pool.next_epoch()
-    kernels.attn_fwd_push(q, k, v, o_head, lse, scale, causal, P, st.rank, off,
+    kernels.attn_fwd_push(q, k, v, None, lse, scale, causal, P, st.rank, off,
                           (strides[0], strides[2], strides[1]), pool.region_ptrs,
                           pool.flag_ptrs, epoch)
     kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, off)
-    return o_tok, o_head, lse
+    return o_tok, lse
 
 
 @attention_a2a.register_fake
@@ -212,23 +228,32 @@ def _attention_a2a_fake(q, k, v, scale, causal, group):
     P = sp_dist.lookup(group).world
     b, hl, S, d = q.shape
     shape, strides = _out_geometry(q, HEAD_TO_SEQ_DIR, P)
-    return (q.new_empty_strided(shape, strides), q.new_empty((b, hl, S, d)),
-            q.new_empty((b, hl, S), dtype=torch.float32))
+    return (q.new_empty_strided(shape, strides), q.new_empty((b, hl, S), dtype=torch.float32))
 
 
 def _attn_a2a_setup(ctx, inputs, output):
     q, k, v, scale, causal, group = inputs
-    _, o_head, lse = output
-    ctx.save_for_backward(q, k, v, o_head, lse)
+    o_tok, lse = output
+    ctx.save_for_backward(q, k, v, o_tok, lse)
     ctx.scale, ctx.causal, ctx.group = scale, causal, group
 
 
-def _attn_a2a_bwd(ctx, d_otok, d_ohead, d_lse):
-    q, k, v, o_head, lse = ctx.saved_tensors
-    (do,) = all_to_all([d_otok], SEQ_TO_HEAD_DIR, ctx.group)  # gradient of the fused a2a
-    if d_ohead is not None:
-        do = do + d_ohead
-    dq, dk, dv = attention_backward(do, q, k, v, o_head, lse, ctx.scale, ctx.causal)
+def ulysses_attention_grad(d_otok, o_tok, q, k, v, lse, scale, causal, group):
+    """Backward of the fused attention + head->seq reshard: delta = rowsum(dO * O) is
+    formed on the token owner from the token-major output (kept anyway for the
+    O-projection weight gradient) and resharded with dO (the inverse all-to-all of the
+    fused one, autodiff.py:252-262)."""
+    acc = torch.promote_types(d_otok.dtype, torch.float32)             # fp32 (fp64 on CPU tests)
+    delta_tok = (d_otok.to(acc) * o_tok.to(acc)).sum(-1, keepdim=True)   # [b, H, s/P, 1]
+    (do,) = all_to_all([d_otok], SEQ_TO_HEAD_DIR, group)
+    (delta,) = all_to_all([delta_tok], SEQ_TO_HEAD_DIR, group)          # [b, h/P, s, 1]
+    return attention_backward_delta(do, q, k, v, delta.squeeze(-1), lse, scale, causal)
+
+
+def _attn_a2a_bwd(ctx, d_otok, d_lse):
+    q, k, v, o_tok, lse = ctx.saved_tensors
+    dq, dk, dv = ulysses_attention_grad(d_otok, o_tok, q, k, v, lse, ctx.scale, ctx.causal,
+                                        ctx.group)
     return dq, dk, dv, None, None, None
 
 
@@ -240,7 +265,7 @@ attention_a2a.register_autograd(_attn_a2a_bwd, setup_context=_attn_a2a_setup)
 def ulysses_qkv_attention(qkv: torch.Tensor, pos: torch.Tensor, theta: float, hq: int, hkv: int,
                           scale: float, group: str) -> tuple[torch.Tensor, torch.Tensor,
                                                              torch.Tensor, torch.Tensor,
-                                                             torch.Tensor, torch.Tensor]:
+                                                             torch.Tensor]:
     """The whole Ulysses attention block (sp_pass.py:172-195) fed by the packed projection
     output qkv [b, s/P, hq+2hkv, d] of this rank's tokens:
       K1 (a2a_rope): q/k rotated and v moved straight from the packed rows into the head
@@ -248,8 +273,8 @@ def ulysses_qkv_attention(qkv: torch.Tensor, pos: torch.Tensor, theta: float, hq
          read once, no RoPE / split / transpose kernel;
       K3+K2: causal attention on the local heads, the epilogue pushing O to the token
          owners (token-major [b, H, s/P, d] = the O-projection input).
-    Returns (o_tokens, q_heads, k_heads, v_heads, o_heads, lse); everything after o_tokens
-    is what the backward needs (the a2a outputs sp_ac keeps)."""
+    Returns (o_tokens, q_heads, k_heads, v_heads, lse); with o_tokens these are what the
+    backward needs (the a2a outputs sp_ac keeps; no head-major O)."""
     st = sp_dist.lookup(group)
     P, pool = st.world, st.pool
     b, sl, H3, d = qkv.shape
@@ -273,8 +298,8 @@ def ulysses_qkv_attention(qkv: torch.Tensor, pos: torch.Tensor, theta: float, hq
                        pos=pos.to(torch.float32).contiguous(), theta=theta)
     kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, first)
     qh, kh, vh = outs
-    o_tok, o_head, lse = attention_a2a(qh, kh, vh, scale, True, group)
-    return o_tok, qh, kh, vh, o_head, lse
+    o_tok, lse = attention_a2a(qh, kh, vh, scale, True, group)
+    return o_tok, qh, kh, vh, lse
 
 
 @ulysses_qkv_attention.register_fake
@@ -285,22 +310,21 @@ def _ulysses_qkv_attention_fake(qkv, pos, theta, hq, hkv, scale, group):
     H = hq
     heads = lambda h: qkv.new_empty_strided((b, h // P, S, d), ((h // P) * S * d, S * d, d, 1))
     return (qkv.new_empty_strided((b, H, sl, d), (sl * H * d, d, H * d, 1)), heads(hq),
-            heads(hkv), heads(hkv), qkv.new_empty((b, hq // P, S, d)),
-            qkv.new_empty((b, hq // P, S), dtype=torch.float32))
+            heads(hkv), heads(hkv), qkv.new_empty((b, hq // P, S), dtype=torch.float32))
 
 
 def _uqa_setup(ctx, inputs, output):
     qkv, pos, theta, hq, hkv, scale, group = inputs
-    _, qh, kh, vh, o_head, lse = output
-    ctx.save_for_backward(pos, qh, kh, vh, o_head, lse)
+    o_tok, qh, kh, vh, lse = output
+    ctx.save_for_backward(pos, qh, kh, vh, o_tok, lse)
     ctx.theta, ctx.hq, ctx.hkv, ctx.scale, ctx.group = theta, hq, hkv, scale, group
     ctx.qkv_shape = tuple(qkv.shape)
 
 
 def _uqa_bwd(ctx, d_otok, *unused):
-    pos, qh, kh, vh, o_head, lse = ctx.saved_tensors
-    (do,) = all_to_all([d_otok], SEQ_TO_HEAD_DIR, ctx.group)
-    dq, dk, dv = attention_backward(do, qh, kh, vh, o_head, lse, ctx.scale, True)
+    pos, qh, kh, vh, o_tok, lse = ctx.saved_tensors
+    dq, dk, dv = ulysses_attention_grad(d_otok, o_tok, qh, kh, vh, lse, ctx.scale, True,
+                                        ctx.group)
     dqkv = qkv_grad_gather(dq, dk, dv, pos, ctx.theta, ctx.group)
     return dqkv, None, None, None, None, None, None
 

@@ -11,8 +11,8 @@ Per rank, with S the global sequence, P the SP size, e = 2 (bf16), L layers:
   saved      what sp_ac keeps per layer:
                P == 1: x_in [S, d] + O [S, hq*hd] + LSE / rstd
                P  > 1: x_in [S/P, d] + the fused op's outputs: o_tokens [S/P, hq*hd],
-                       q/k/v head shards [S, (hq + 2 hkv)/P * hd], o_heads [S, hq/P * hd]
-                       + LSE [hq/P, S] fp32
+                       q/k/v head shards [S, (hq + 2 hkv)/P * hd] + LSE [hq/P, S] fp32
+                       (no head-major O: delta = rowsum(dO*O) is formed token-side)
   transient  the largest backward working set of one layer: the recomputed MLP chunk
              (gate/up and their gradients, chunked at MLP_CHUNK tokens), the attention
              backward's fp32 dQ accumulator and bf16 dq/dk/dv, the recomputed projections,
@@ -55,7 +55,6 @@ def step_memory(cfg: LlamaConfig, S: int, P: int = 1, zero1: bool = True,
     else:
         per_layer = (e * sl * (d + hq * hd)                              # x_in, o_tokens
                      + e * S * (hq + 2 * hkv) // P * hd                  # q/k/v head shards
-                     + e * S * hq // P * hd                              # o_heads
                      + 4 * S * hq // P + 4 * sl * 2)                     # LSE, rstd
     saved = L * per_layer + e * sl * d                                   # + final hidden
     chunk = min(sl, MLP_CHUNK)

@@ -81,7 +81,19 @@ def enable_cpu_lowering() -> None:
     def _attention_a2a_cpu(q, k, v, scale, causal, group):
         o, lse = _attention_cpu(q, k, v, scale, causal)
         (ot,) = _all_to_all_cpu([o], ops.HEAD_TO_SEQ_DIR, group)
-        return ot, o, lse
+        return ot, lse
+
+    @torch.library.register_kernel("autosp::attention_backward_delta", "cpu")
+    def _attention_backward_delta_cpu(do, q, k, v, delta, lse, scale, causal):
+        sc, ke, ve = _attn_math(q, k, v, scale, causal)
+        p = torch.softmax(sc, dim=-1)
+        dp = do @ ve.transpose(-1, -2)
+        ds = p * (dp - delta.to(dp.dtype).unsqueeze(-1)) * scale
+        dq = ds @ ke
+        g = q.shape[1] // k.shape[1]
+        dk = (ds.transpose(-1, -2) @ q).unflatten(1, (k.shape[1], g)).sum(2)
+        dv = (p.transpose(-1, -2) @ do).unflatten(1, (k.shape[1], g)).sum(2)
+        return dq, dk, dv
 
     _ENABLED = True
 

@@ -293,3 +293,23 @@ def test_a2a_full_size_round_trip_bit_exact():
     # spot-check the global-slicing identity on one destination
     full = torch.cat(shards, dim=1)
     assert torch.equal(heads[3].view(torch.int16), full[:, :, 3 * 4:4 * 4].view(torch.int16))
+
+
+@pytest.mark.parametrize("hq,hkv,s,d", [(4, 1, 1024, 64), (2, 2, 300, 128)])
+def test_attn_bwd_with_supplied_delta_equals_o_path(hq, hkv, s, d):
+    """autosp_attn_bwd_delta (delta = rowsum(dO*O) from the caller, no O) produces exactly
+    the gradients of the O-reading entry point."""
+    K = _k()
+    g = torch.Generator(device="cuda").manual_seed(s + d)
+    q = torch.randn(1, hq, s, d, device="cuda", generator=g).bfloat16()
+    k = torch.randn(1, hkv, s, d, device="cuda", generator=g).bfloat16()
+    v = torch.randn(1, hkv, s, d, device="cuda", generator=g).bfloat16()
+    do = torch.randn(1, hq, s, d, device="cuda", generator=g).bfloat16()
+    o, lse = K.attn_fwd(q, k, v)
+    ref = K.attn_bwd(q, k, v, o, do, lse)
+    delta = (do.float() * o.float()).sum(-1).contiguous()
+    got = K.attn_bwd(q, k, v, None, do, lse, delta=delta)
+    torch.cuda.synchronize()
+    for a, b in zip(got, ref):
+        err = float((a.float() - b.float()).abs().max() / b.float().abs().max())
+        assert err < 1e-2, err  # same math; dQ's fp32 reduce order is not deterministic

@@ -102,8 +102,8 @@ def test_two_processes_ipc_match_unsharded(mode):
     for rank, loss, grads, n_fw, n_bw in out:
         assert abs(loss - ref_loss) / abs(ref_loss) < 1e-3, (loss, ref_loss)
         # forward: ONE collective op per layer (RoPE-fused q/k/v reshard + attention whose
-        # epilogue pushes O); backward: dO reshard + packed-gradient gather per layer
-        assert n_fw == CFG["layers"] and n_bw == 2 * CFG["layers"]
+        # epilogue pushes O); backward: dO and delta reshards + packed-gradient gather
+        assert n_fw == CFG["layers"] and n_bw == 3 * CFG["layers"]
         for n, gr in ref_grads.items():
             err = float(abs(grads[n] - gr).max() / max(abs(gr).max(), 1e-30))
             assert err < 2e-2, (rank, n, err)
