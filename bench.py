@@ -333,13 +333,15 @@ def main():
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random token ids, random-init weights N(0, 0.02^2))",
-        "config": {"workload": f"{cfg.name} synthetic, global seq {S}, batch {b} "
-                               f"(BASELINE.json configs[1]; at N=1 the single-GPU case)",
+        "config": {"workload": f"{cfg.name} synthetic, global seq {S}, batch {b}" + (
+                       " (BASELINE.json configs[1]; at N=1 the single-GPU case)"
+                       if (cfg.name, S) == ("llama3.2-1b", 32768) else ""),
                    "model": cfg.name, "global_batch": b, "seq_len": S,
                    "parallelism": f"sp{P}" + ("+zero1" if zero1 else ""), "passes": passes,
                    "ac_mode": args.ac_mode,
                    "ac_applied": sp_ac.LAST_PLAN.get("mode_applied"),
-                   "l2": "working set (weights 2.5 GB + activations) >> 126 MB L2; no flush"},
+                   "l2": f"working set (weights {2 * cfg.n_params() / 1e9:.1f} GB + activations)"
+                         " >> 126 MB L2; no flush"},
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": {"kernel": "attn_bwd (K4: pre + tcgen05 main + post, per launch)",
