@@ -74,8 +74,11 @@ struct Cfg {
   static constexpr int LAYOUT = SW == 128 ? 2 : (SW == 64 ? 4 : 6);
   static constexpr int SBO = 8 * SW;
   static constexpr int TILE = 128 * D * 2;  // one [128 x D] bf16 tile
-  // Q/dO(+lse/delta) ring depth (3 measured slower than 2 for d = 64)
-  static constexpr int kQStages = D == 128 ? 1 : 2;
+  // Q(+lse/delta) ring depth (3 measured slower than 2 for d = 64) and dO ring depth.
+  // d = 128: Q is double-buffered so S^T(t+1) can be issued right after dV(t) (it only
+  // needs Q(t+1)); dO stays single (freed by dV(t), needed by dP(t+1) much later).
+  static constexpr int kQStages = 2;
+  static constexpr int kDOStages = D == 128 ? 1 : 2;
   // S^T buffers in TMEM: two (S(t+1) overlaps the softmax of t) when d <= 64
   static constexpr int NSB = D == 128 ? 1 : 2;
   // exps per 8 done on the FMA pipe (part 1 is MUFU-bound at 16 exp/clk/SM)
@@ -84,11 +87,15 @@ struct Cfg {
   static constexpr int V_OFF = TILE;
   static constexpr int Q_OFF = 2 * TILE;                       // Q[st]
   static constexpr int DO_OFF = Q_OFF + kQStages * TILE;       // dO[st]
-  static constexpr int DS_OFF = DO_OFF + kQStages * TILE;      // dS^T [128 keys x 128 q] bf16
+  static constexpr int DS_OFF = DO_OFF + kDOStages * TILE;     // dS^T [128 keys x 128 q] bf16
   static constexpr int DQ_OFF = DS_OFF + 128 * 128 * 2;        // 2 fp32 chunks [128 x 32]
   static constexpr int LSE_OFF = DQ_OFF + 2 * 128 * 32 * 4;    // lse[kQStages][128], delta[kQStages][128]
   static constexpr int BAR_OFF = LSE_OFF + 2 * kQStages * 128 * 4;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  // dynamic smem starts 1024-aligned when the kernel has no static smem (measured:
+  // shared address 0x400, tools/microbench/smem_align); d = 128 needs the slack bytes
+  static constexpr int kAlignSlack = D == 128 ? 0 : 1024;
+  static constexpr int SMEM = BAR_OFF + 256 + kAlignSlack;
+  static_assert(SMEM <= 232448, "shared memory budget (227 KB)");
   // TMEM columns.  d <= 64: S0 | S1 | dP | dV | dK; P^T(t) (bf16) occupies columns
   //   [0,32) and [96,128) of S buffer t%2 and dQ(t) (fp32) columns [32, 32+d), so dP(t+1)
   //   never waits for the dQ drain (only S(t+2) does).
@@ -163,10 +170,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   uint64_t* dq_full = ds_ready + 1;             // dQ MMA complete
   uint64_t* dq_empty = dq_full + 1;             // dQ drained from TMEM (128 arrivals)
   uint64_t* acc_full = dq_empty + 1;            // final dK/dV complete
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* do_full = acc_full + 1;             // [kDOStages] dO(t) in smem
+  uint64_t* do_empty = do_full + C::kDOStages;  // [kDOStages] dP(t), dV(t) done with it
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(do_empty + C::kDOStages);
   float* lse_s = reinterpret_cast<float*>(smem + C::LSE_OFF);  // [kQStages][128]
   float* dlt_s = lse_s + C::kQStages * 128;                                   // [kQStages][128]
 
+  if constexpr (C::kAlignSlack == 0) {
+    if (smem_u32(smem_raw) & 1023) asm volatile("trap;");  // layout assumes 1024 alignment
+  }
   const int warp = warp_id();
   const int lane = lane_id();
   const int ktile = blockIdx.x;  // launch order = heaviest (most query tiles) first
@@ -193,6 +205,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 4);
     mbar_init(acc_full, 1);
+    for (int s = 0; s < C::kDOStages; ++s) {
+      mbar_init(do_full + s, 1);
+      mbar_init(do_empty + s, 1);
+    }
     fence_mbar_init();
     tma_prefetch_desc(&p.tm_q);
     tma_prefetch_desc(&p.tm_k);
@@ -241,17 +257,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         const int head = kvh * group + t / per_head;
         const int q0 = (m_first + t % per_head) * BQ;
         mbar_wait(q_empty + st, ph ^ 1);
-        mbar_arrive_expect_tx(q_full + st, 2 * C::TILE + (p.lse_tma ? 2 * 128 * 4 : 0));
+        mbar_arrive_expect_tx(q_full + st, C::TILE + (p.lse_tma ? 2 * 128 * 4 : 0));
         if (p.lse_tma) {  // the softmax warps need lse/delta of these 128 queries
           tma_load_2d(lse_s + st * 128, &p.tm_lse, q_full + st, q0, batch * p.Hq + head);
           tma_load_2d(dlt_s + st * 128, &p.tm_dlt, q_full + st, q0, batch * p.Hq + head);
         }
-        for (int c = 0; c < C::NCH; ++c) {
+        for (int c = 0; c < C::NCH; ++c)
           tma_load_4d(smem + C::Q_OFF + st * C::TILE + c * 128 * C::SW, &p.tm_q, q_full + st,
                       c * C::CE, q0, head, batch, pol_last);
-          tma_load_4d(smem + C::DO_OFF + st * C::TILE + c * 128 * C::SW, &p.tm_do, q_full + st,
+        const int so = t % C::kDOStages;
+        mbar_wait(do_empty + so, ((t / C::kDOStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(do_full + so, C::TILE);
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_4d(smem + C::DO_OFF + so * C::TILE + c * 128 * C::SW, &p.tm_do, do_full + so,
                       c * C::CE, q0, head, batch, pol_last);
-        }
       }
     }
   } else if (warp == kMmaWarp) {
@@ -283,7 +302,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         __syncwarp();
       };
       auto issue_dp = [&](int t) {  // dP^T(t) = V dO(t)^T
-        const uint64_t ddo = make_smem_desc(s_do + (t % C::kQStages) * C::TILE, 16, C::SBO, C::LAYOUT);
+        mbar_wait(do_full + (t % C::kDOStages), (t / C::kDOStages) & 1);
+        tc_fence_after();
+        const uint64_t ddo = make_smem_desc(s_do + (t % C::kDOStages) * C::TILE, 16, C::SBO, C::LAYOUT);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
@@ -299,7 +320,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       for (int t = 0; t < T; ++t) {
         const int st = t % C::kQStages;
         const uint64_t dq_mn = make_smem_desc(s_q + st * C::TILE, 128 * C::SW, C::SBO, C::LAYOUT);
-        const uint64_t ddo_mn = make_smem_desc(s_do + st * C::TILE, 128 * C::SW, C::SBO, C::LAYOUT);
+        const uint64_t ddo_mn = make_smem_desc(s_do + (t % C::kDOStages) * C::TILE, 128 * C::SW,
+                                               C::SBO, C::LAYOUT);
         const uint32_t acc0 = t > 0 ? 1u : 0u;
         if (C::NSB == 2) {
           // dP region: dS(t-1) was consumed by dK(t-1), issued earlier (in-order)
@@ -336,8 +358,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           for (int kk = 0; kk < BQ / 16; ++kk)
             mma_ts(tmem + C::DV_COL, tmem + s_col + pk_col(kk),
                    ddo_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_g, kk > 0 ? 1u : acc0);
+          tc_commit(do_empty + (t % C::kDOStages));  // dP(t) and dV(t) are done with dO(t)
         }
         __syncwarp();
+        // d = 128: S(t+1) reuses the S columns: P(t) has been read by the softmax and is
+        // consumed by dV(t), issued just above (in-order pipe).  Issuing it here instead
+        // of after dK/dQ(t) lets S^T(t+1) run under the dS math of t (needs Q(t+1) only,
+        // which the second Q stage has already loaded).
+        if (C::NSB == 1 && t + 1 < T) {
+          wait_q(t + 1);
+          issue_s(t + 1);
+        }
         // dK += dS^T Q and dQ(t) = dS K once dS is in TMEM + smem
         mbar_wait(ds_ready, t & 1);
         if (lane == 0) BWD_TRACE(3, t);
@@ -356,11 +387,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         }
         __syncwarp();
         if (lane == 0) BWD_TRACE(4, t);
-        // d = 128: S(t+1) reuses the S columns (P(t) consumed by dV(t) and by the softmax)
-        if (C::NSB == 1 && t + 1 < T) {
-          wait_q(t + 1);
-          issue_s(t + 1);
-        }
       }
       if (elect_one()) tc_commit(acc_full);
       __syncwarp();
@@ -550,9 +576,48 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       const int head = kvh * group + t / per_head;
       const int q0 = (m_first + t % per_head) * BQ;
       const uint32_t dq_addr = tmem + lane_base + dq_col(t);
+      // the slot of chunk 0 was last used two chunks ago: wait for that reduce to have
+      // read it BEFORE dQ(t) arrives, off the critical path (dP(t+1) waits for the drain)
+      if (leader) bulk_wait_read1();
       mbar_wait(dq_full, t & 1);
       if (threadIdx.x == kDrainWarp0 * 32) BWD_TRACE(9, t);
       tc_fence_after();
+      // stage one 32-column chunk through a smem slot and TMA-reduce it into dQacc
+      auto stage = [&](const uint32_t (&v)[32], int c) {
+        const int chunk_id = t * NC + c;
+        float* slot = reinterpret_cast<float*>(smem + C::DQ_OFF) + (chunk_id & 1) * (128 * 32);
+        if (leader && c > 0) bulk_wait_read1();  // the reduce that last used this slot has read it
+        named_bar_sync(2, 128);
+        uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          sts128(srow + ((u ^ (row & 7)) << 4),
+                 make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]));
+        fence_proxy_async_smem();
+        named_bar_sync(2, 128);
+        if (leader) {
+          tma_reduce_add_3d(&p.tm_dqacc, slot, c * 32, q0, batch * p.Hq + head);
+          bulk_commit();
+        }
+      };
+      if constexpr (NC == 4) {
+        // d = 128: dQ(t) sits in the dP columns and dP(t+1) waits for them, so the drain
+        // releases them after ONE staging: three chunks in registers, then the fourth
+        // into the registers the first one freed
+        uint32_t va[32], vb[32], vc[32];
+        tmem_ld32(dq_addr + 0, va);
+        tmem_ld32(dq_addr + 32, vb);
+        tmem_ld32(dq_addr + 64, vc);
+        tmem_wait_ld();
+        stage(va, 0);
+        tmem_ld32(dq_addr + 96, va);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive_warp(dq_empty);
+        stage(vb, 1);
+        stage(vc, 2);
+        stage(va, 3);
+      } else
 #pragma unroll
       for (int c2 = 0; c2 < NC; c2 += 2) {
         uint32_t v[2][32];
@@ -565,25 +630,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         }
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
-          const int c = c2 + cc;
-          if (c >= NC) break;
-          // alternate the two staging slots across ALL chunks (also across steps when
-          // NC is odd), so wait_group.read 1 always covers the slot's previous reduce
-          const int chunk_id = t * NC + c;
-          float* slot = reinterpret_cast<float*>(smem + C::DQ_OFF) + (chunk_id & 1) * (128 * 32);
-          if (leader) bulk_wait_read1();  // the reduce that last used this slot has read it
-          named_bar_sync(2, 128);
-          uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            sts128(srow + ((u ^ (row & 7)) << 4),
-                   make_uint4(v[cc][4 * u], v[cc][4 * u + 1], v[cc][4 * u + 2], v[cc][4 * u + 3]));
-          fence_proxy_async_smem();
-          named_bar_sync(2, 128);
-          if (leader) {
-            tma_reduce_add_3d(&p.tm_dqacc, slot, c * 32, q0, batch * p.Hq + head);
-            bulk_commit();
-          }
+          // (the two staging slots alternate across ALL chunks, also across steps when NC
+          // is odd, so wait_group.read 1 always covers the slot's previous reduce)
+          if (c2 + cc < NC) stage(v[cc], c2 + cc);
         }
       }
       if (threadIdx.x == kDrainWarp0 * 32) BWD_TRACE(10, t);
