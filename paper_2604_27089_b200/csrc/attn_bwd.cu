@@ -77,7 +77,10 @@ struct Cfg {
   // Q(+lse/delta) ring depth (3 measured slower than 2 for d = 64) and dO ring depth.
   // d = 128: Q is double-buffered so S^T(t+1) can be issued right after dV(t) (it only
   // needs Q(t+1)); dO stays single (freed by dV(t), needed by dP(t+1) much later).
-  static constexpr int kQStages = 2;
+#ifndef AUTOSP_BWD_QSTAGES64
+#define AUTOSP_BWD_QSTAGES64 3
+#endif
+  static constexpr int kQStages = D == 128 ? 2 : AUTOSP_BWD_QSTAGES64;
   static constexpr int kDOStages = D == 128 ? 1 : 2;
   // S^T buffers in TMEM: two (S(t+1) overlaps the softmax of t) when d <= 64
   static constexpr int NSB = D == 128 ? 1 : 2;
