@@ -29,6 +29,9 @@ extern "C" void autosp_set_error(const char* fmt, ...);
 #ifndef AUTOSP_FWD_EMU
 #define AUTOSP_FWD_EMU 3  // exps per 8 on the FMA pipe for d <= 64
 #endif
+#ifndef AUTOSP_FWD_KVRING64
+#define AUTOSP_FWD_KVRING64 98304  // K/V ring bytes for d <= 64 (3 stages of 128 keys at d = 64)
+#endif
 #ifndef AUTOSP_FWD_EMU128
 #define AUTOSP_FWD_EMU128 2  // exps per 8 on the FMA pipe for d = 128
 #endif
@@ -71,7 +74,7 @@ struct Cfg {
   static constexpr int NCH = D / CE;                        // chunks per row
   static constexpr int TILE_BYTES = BM * D * 2;             // Q tile: 128 x D bf16
   static constexpr int KTILE = BN * D * 2;                  // K / V tile: BN x D bf16
-  static constexpr int KV_RING = D == 128 ? 131072 : 98304;  // bytes of K + V stages
+  static constexpr int KV_RING = D == 128 ? 131072 : AUTOSP_FWD_KVRING64;  // bytes of K+V stages
   static constexpr int kStagesRaw = KV_RING / (2 * KTILE);
   static constexpr int kStages = kStagesRaw < 2 ? 2 : (kStagesRaw > 8 ? 8 : kStagesRaw);
   // exps per 8 computed by the FMA-pipe polynomial instead of MUFU (MUFU is the
