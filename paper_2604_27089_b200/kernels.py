@@ -16,7 +16,6 @@ from . import _lib
 from .errors import ValidationError
 
 SUPPORTED_HEAD_DIMS = (32, 64, 128)
-_DEBUG = bool(__import__("os").environ.get("AUTOSP_DEBUG"))
 
 
 class LaunchLog:
@@ -95,14 +94,6 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool = T
     scale = 1.0 / math.sqrt(d) if scale is None else scale
     o = torch.empty((b, hq, s, d), dtype=torch.bfloat16, device=q.device) if out is None else out
     lse = torch.empty((b, hq, s), dtype=torch.float32, device=q.device)
-    if _DEBUG:
-        print(f"[autosp] attn_fwd q{tuple(q.shape)}{q.stride()} k{tuple(k.shape)}{k.stride()} "
-              f"v{tuple(v.shape)}{v.stride()} ptrs {q.data_ptr() % 256} {k.data_ptr() % 256} "
-              f"{v.data_ptr() % 256} scale {scale}", flush=True)
-    dump = __import__("os").environ.get("AUTOSP_DEBUG_DUMP")
-    if dump:
-        torch.save({"q": q.cpu(), "k": k.cpu(), "v": v.cpu(), "scale": scale}, dump)
-        raise SystemExit(f"dumped attention inputs to {dump}")
     ev = LOG.begin("attn_fwd")
     rc = lib.autosp_attn_fwd(_attn_tensor(q, "q"), _attn_tensor(k, "k"), _attn_tensor(v, "v"),
                              _attn_tensor(o, "o"), lse.data_ptr(), b, hq, hkv, s, d,

@@ -162,3 +162,30 @@ def test_rope_fused_reshard_block_virtual_ranks(P, hq, hkv, d):
     assert torch.equal(o, o_ref)  # RoPE math shared (rope.cuh), reshard bit-exact
     err = float((gq.float() - ref_in.grad.float()).abs().max() / ref_in.grad.float().abs().max())
     assert err < 1e-2, err
+
+
+def test_sp_ac_plan_on_the_cuda_graph():
+    """The GPU graph (autosp rms_norm / qkv_rope / attention ops, not the CPU
+    decompositions) under seq-aware sp_ac keeps, per layer, one residual value, the
+    attention output and its LSE -- nothing O(s * d_ffn) -- and recomputes no attention."""
+    import paper_2604_27089_b200 as autosp
+    from paper_2604_27089_b200 import sp_ac
+    from paper_2604_27089_b200.workloads import LlamaConfig, LlamaDecoder, lm_loss
+    cfg = LlamaConfig("plan", 256, 3, 4, 2, 640, vocab=512)
+    s = 384
+    autosp.reg_passes(["auto_sp", "sp_ac"], ac_mode="seq-aware")
+    autosp.dist.init(1)
+    torch.manual_seed(0)
+    m = LlamaDecoder(cfg, dtype=torch.bfloat16, device="cuda")
+    ids = torch.randint(0, cfg.vocab, (1, s + 1), device="cuda")
+    lm_loss(autosp.compile(m)(ids[:, :-1]), m.lm_head, ids[:, 1:]).backward()
+    torch.cuda.synchronize()
+    det = sp_ac.LAST_PLAN["saved_detail"]
+    resid = [x for x in det if x[2] == (1, s, cfg.d_model)]
+    attn_o = [x for x in det if x[2] == (1, cfg.hq, s, cfg.head_dim)]
+    lse = [x for x in det if x[2] == (1, cfg.hq, s)]
+    ffn = [x for x in det if x[2][:1] == (1,) and x[2][-1] in (cfg.d_ffn, 2 * cfg.d_ffn)]
+    assert len(resid) == cfg.layers, resid
+    assert len(attn_o) == cfg.layers and len(lse) == cfg.layers, det
+    assert not ffn, ffn
+    assert not sp_ac.LAST_PLAN["bw_recomputes_attention"]
