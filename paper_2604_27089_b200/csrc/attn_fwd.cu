@@ -27,7 +27,10 @@
 extern "C" void autosp_set_error(const char* fmt, ...);
 
 #ifndef AUTOSP_FWD_EMU
-#define AUTOSP_FWD_EMU 3  // exps per 8 on the FMA pipe for d <= 64
+#define AUTOSP_FWD_EMU 1  // exps per 8 on the FMA pipe for d <= 64 (A/B: 1 > 0 > 2 > 3)
+#endif
+#ifndef AUTOSP_FWD_RESCALE_T
+#define AUTOSP_FWD_RESCALE_T 8  // lazy rescale / optimistic-pass threshold (log2 units)
 #endif
 #ifndef AUTOSP_FWD_KVRING64
 #define AUTOSP_FWD_KVRING64 98304  // K/V ring bytes for d <= 64 (3 stages of 128 keys at d = 64)
@@ -395,7 +398,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
                                       __uint_as_float(sr[c + 1]));
           if (h == C::NH - 1) {  // whole row seen: decide, then release S_i
             const float mxr = fmaxf(fmax3(mx4[0], mx4[1], mx4[2]), mx4[3]);
-            redo = __any_sync(0xffffffffu, mxr * p.scale_log2 > m + 8.f);
+            redo = __any_sync(0xffffffffu, mxr * p.scale_log2 > m + (float)AUTOSP_FWD_RESCALE_T);
             if (redo) break;  // S_i stays: the two-pass path re-reads it
             tc_fence_before();
             mbar_arrive_warp(s_free + i);
@@ -439,7 +442,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
       }
       const float mx = need_mask ? pass1(std::true_type{}) : pass1(std::false_type{});
       const float m_cand = mx * p.scale_log2;
-      if (m_cand > m + 8.f) {  // lazy rescale (also taken on the first tile)
+      if (m_cand > m + (float)AUTOSP_FWD_RESCALE_T) {  // lazy rescale (also taken on the first tile)
         alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - m_cand);
         rescale = (j > 0);
         m = m_cand;
