@@ -77,9 +77,13 @@ class SymmetricPool:
     ALIGN = 1024
 
     def __init__(self, nbytes: int, world: int, rank: int, device, group=None,
-                 peers: list[tuple[int, int]] | None = None):
+                 peers: list[tuple[int, int]] | None = None, reuse: bool = True):
         lib = _lib.load()
         self.world, self.rank, self.device = world, rank, device
+        # reuse=False: bump allocation, no slot reuse -- for virtual ranks sharing ONE
+        # process (threads share the autograd engine, so slot lifetimes, and with them
+        # first-fit offsets, can differ between ranks; separate processes are symmetric)
+        self.reuse = reuse
         self.capacity = nbytes
         self._owned: list[int] = []
         self._opened: list[int] = []
@@ -117,6 +121,14 @@ class SymmetricPool:
 
     def alloc(self, nbytes: int) -> tuple[int, torch.Tensor]:
         """First-fit slot of the receive region; returns (offset, uint8 view)."""
+        if not self.reuse:
+            need = (nbytes + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+            off = self.high_water
+            if off + need > self.capacity:
+                raise ValidationError("loopback receive region exhausted (bump allocation)")
+            self.high_water = off + need
+            base = _raw_tensor(self.region_ptrs[self.rank] + off, nbytes, self.device)
+            return off, base.view(-1)
         self.slots = [s for s in self.slots if self._busy(s)]
         self.slots.sort(key=lambda s: s.offset)
         need = (nbytes + self.ALIGN - 1) // self.ALIGN * self.ALIGN

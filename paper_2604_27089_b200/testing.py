@@ -109,7 +109,8 @@ def loopback_states(P: int, nbytes: int, device="cuda", prefix: str = "loop"):
     peers = [(flags[j].data_ptr(), regions[j].data_ptr()) for j in range(P)]
     states = []
     for r in range(P):
-        pool = sp_dist.SymmetricPool(nbytes, P, r, torch.device(device), peers=peers)
+        pool = sp_dist.SymmetricPool(nbytes, P, r, torch.device(device), peers=peers,
+                                     reuse=False)
         st = sp_dist.SPState(world=P, rank=r, group=None, device=torch.device(device),
                              pool=pool, name=f"{prefix}{r}")
         sp_dist._REGISTRY[st.name] = st

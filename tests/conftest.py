@@ -2,6 +2,12 @@ import os
 import sys
 from pathlib import Path
 
+# The threaded virtual-rank tests run P ranks in ONE process (one CUDA context): a lazily
+# loaded kernel module on one rank's thread synchronises the context while another rank's
+# handshake kernel spins waiting for it -- a harness-only deadlock (separate processes have
+# separate contexts).  Load every module at context creation instead.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 import pytest
 
 ROOT = Path(__file__).resolve().parents[1]

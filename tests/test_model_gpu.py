@@ -64,19 +64,32 @@ def test_seqcomp_c1_single_gpu_matches_reference_fixture(golden_dir, passes):
         assert not sp_ac.LAST_PLAN["bw_recomputes_attention"]
 
 
+# Virtual ranks are threads of ONE process, so they would share torch's autograd engine
+# thread: rank 0's backward collective could then spin on the GPU waiting for rank 1's,
+# which the same engine thread cannot launch until something synchronises -- a harness
+# deadlock that separate processes do not have (tests/test_multiproc_gpu.py runs the
+# autograd path across processes).  Here each rank calls the ops' forward and their
+# registered backward formulas directly, on its own thread and stream.  (The other
+# one-context hazard, lazy kernel-module loading synchronising the context while a peer's
+# handshake spins, is removed by CUDA_MODULE_LOADING=EAGER in conftest.py.)
+
+
 def _ulysses_rank(st, x_full, do_full, results, r, P, causal=True):
     from paper_2604_27089_b200 import ops
     torch.cuda.set_device(0)
     stream = torch.cuda.Stream()
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream), torch.no_grad():
         sl = x_full[0].shape[2] // P
-        q = x_full[0][:, :, r * sl:(r + 1) * sl].clone().requires_grad_(True)
-        k = x_full[1][:, :, r * sl:(r + 1) * sl].clone().requires_grad_(True)
-        v = x_full[2][:, :, r * sl:(r + 1) * sl].clone().requires_grad_(True)
-        o = ops.ulysses_attention(q, k, v, st.name, is_causal=causal)
-        o.backward(do_full[:, :, r * sl:(r + 1) * sl])
+        q, k, v = (x[:, :, r * sl:(r + 1) * sl].clone() for x in x_full)
+        scale = 1.0 / q.shape[-1] ** 0.5
+        qh, kh, vh = ops.all_to_all([q, k, v], ops.SEQ_TO_HEAD_DIR, st.name)
+        o, lse = ops.attention_a2a(qh, kh, vh, scale, causal, st.name)
+        dqh, dkh, dvh = ops.ulysses_attention_grad(do_full[:, :, r * sl:(r + 1) * sl], o, qh,
+                                                   kh, vh, lse, scale, causal, st.name)
+        dq, dk, dv = ops.all_to_all([dqh, dkh, dvh], ops.HEAD_TO_SEQ_DIR, st.name)
+        # token-major [b, H, s/P, d] views -> [b, h, s/P, d] like the inputs
+        results[r] = tuple(t.clone() for t in (o, dq, dk, dv))
     stream.synchronize()
-    results[r] = (o.detach(), q.grad, k.grad, v.grad)
 
 
 @pytest.mark.parametrize("P,hq,hkv,d", [(2, 4, 2, 64), (4, 8, 4, 128), (8, 8, 8, 32),
@@ -118,14 +131,18 @@ def _qkv_rank(st, qkv_full, pos_full, dout_full, results, r, P, hq, hkv):
     from paper_2604_27089_b200 import ops
     torch.cuda.set_device(0)
     stream = torch.cuda.Stream()
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream), torch.no_grad():
         sl = qkv_full.shape[1] // P
-        qkv = qkv_full[:, r * sl:(r + 1) * sl].clone().requires_grad_(True)
+        qkv = qkv_full[:, r * sl:(r + 1) * sl].clone()
         pos = pos_full[r * sl:(r + 1) * sl].clone()
-        o = ops.ulysses_qkv_block(qkv, pos, 500000.0, hq, hkv, st.name)
-        o.backward(dout_full[:, :, r * sl:(r + 1) * sl])
+        scale = 1.0 / qkv.shape[-1] ** 0.5
+        o, qh, kh, vh, lse = ops.ulysses_qkv_attention(qkv, pos, 500000.0, hq, hkv, scale,
+                                                       st.name)
+        dq, dk, dv = ops.ulysses_attention_grad(dout_full[:, :, r * sl:(r + 1) * sl], o, qh, kh,
+                                                vh, lse, scale, True, st.name)
+        dqkv = ops.qkv_grad_gather(dq, dk, dv, pos, 500000.0, st.name)
+        results[r] = (o.clone(), dqkv.clone())
     stream.synchronize()
-    results[r] = (o.detach().clone(), qkv.grad.clone())
 
 
 @pytest.mark.parametrize("P,hq,hkv,d", [(2, 4, 2, 64), (4, 8, 4, 128), (8, 32, 8, 64)])
