@@ -190,17 +190,20 @@ def test_attn_bwd_matches_oracle(b, hq, hkv, s, d, causal):
         assert err < GRAD_TOL, (name, err)
 
 
-@pytest.mark.parametrize("d", [64, 128])
-def test_attn_fwd_bwd_running_max_jumps(d):
+@pytest.mark.parametrize("d,jump", [(64, 512), (128, 512), (64, 589), (64, 700), (128, 589)])
+def test_attn_fwd_bwd_running_max_jumps(d, jump):
     """Scores that grow along the sequence force the lazy O rescale on some rows of a warp
-    but not others (a divergent-lane path: tcgen05.ld/st must stay warp-uniform)."""
+    but not others (a divergent-lane path: tcgen05.ld/st must stay warp-uniform).  The
+    late jump lands at a tile start (512), in the second 64-key half of a tile (589:
+    the forward's mid-tile rescale after the first half was released) or in a first half
+    (700)."""
     b, h, s = 1, 2, 1024
     g = torch.Generator().manual_seed(d)
     base = torch.randn(b, s, h, d, generator=g)
     ramp = torch.linspace(0.0, 6.0, s).view(1, s, 1, 1) * torch.rand(1, 1, h, 1, generator=g)
     q = base * (1.0 + ramp)
     k = torch.randn(b, s, h, d, generator=g) * (1.0 + ramp.flip(1))
-    k[:, s // 2:] *= 4.0  # a late jump of the running max for some rows only
+    k[:, jump:] *= 4.0  # a late jump of the running max for some rows only
     v = torch.randn(b, s, h, d, generator=g)
     do = torch.randn(b, s, h, d, generator=g)
     qb, kb, vb, dob = (x.bfloat16().double().numpy() for x in (q, k, v, do))
