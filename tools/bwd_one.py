@@ -1,5 +1,8 @@
+"""A few attention-backward launches at the Llama-1B per-layer shape (s = 16K): the
+target for `ncu --set full -k regex:attn_bwd_kernel` captures (dev tool)."""
 import sys
-sys.path.insert(0, '/root/repo')
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch
 from paper_2604_27089_b200 import kernels as K
 b, hq, hkv, s, d = 1, 32, 8, 16384, 64
