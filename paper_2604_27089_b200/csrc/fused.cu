@@ -239,8 +239,11 @@ __global__ void __launch_bounds__(kNormThreads) rms_fwd_kernel(
 // processes and accumulates dy * xhat for them in REGISTERS across rows; the warps of a
 // CTA then combine through shared memory once (shared-memory atomics per element were
 // the bottleneck of the first version).
+#ifndef AUTOSP_RMS_REG
+#define AUTOSP_RMS_REG 1  // keep the row's x / dy in registers between the two passes (1 CTA/SM)
+#endif
 template <int VPL>
-__global__ void __launch_bounds__(kNormThreads) rms_bwd_kernel(
+__global__ void __launch_bounds__(kNormThreads, AUTOSP_RMS_REG ? 1 : 2) rms_bwd_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
     __nv_bfloat16* __restrict__ dx, float* __restrict__ partial, int64_t rows, int d,
@@ -261,13 +264,29 @@ __global__ void __launch_bounds__(kNormThreads) rms_bwd_kernel(
     const __nv_bfloat16* gr = dy + r * lddy;
     const float rs = rstd[r];
     float dot = 0.f;  // sum_c dy*w*xhat
+#if AUTOSP_RMS_REG
+    uint4 xv[VPL], gv[VPL];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int v = lane + 32 * i;
+      if (v < vpr) {
+        xv[i] = *reinterpret_cast<const uint4*>(xr + v * 8);
+        gv[i] = *reinterpret_cast<const uint4*>(gr + v * 8);
+      }
+    }
+#endif
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const int v = lane + 32 * i;
       if (v < vpr) {
         float f[8], g[8], ww[8];
+#if AUTOSP_RMS_REG
+        unpack8(xv[i], f);
+        unpack8(gv[i], g);
+#else
         unpack8(*reinterpret_cast<const uint4*>(xr + v * 8), f);
         unpack8(*reinterpret_cast<const uint4*>(gr + v * 8), g);
+#endif
         unpack8(*reinterpret_cast<const uint4*>(w + v * 8), ww);
 #pragma unroll
         for (int k = 0; k < 8; ++k) dot = fmaf(g[k] * ww[k], f[k] * rs, dot);
@@ -282,8 +301,13 @@ __global__ void __launch_bounds__(kNormThreads) rms_bwd_kernel(
       const int v = lane + 32 * i;
       if (v < vpr) {
         float f[8], g[8], ww[8], o8[8];
+#if AUTOSP_RMS_REG
+        unpack8(xv[i], f);
+        unpack8(gv[i], g);
+#else
         unpack8(*reinterpret_cast<const uint4*>(xr + v * 8), f);
         unpack8(*reinterpret_cast<const uint4*>(gr + v * 8), g);
+#endif
         unpack8(*reinterpret_cast<const uint4*>(w + v * 8), ww);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -324,7 +348,7 @@ int norm_blocks() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  return 2 * sms;
+  return (AUTOSP_RMS_REG ? 1 : 2) * sms;
 }
 
 // ---------------------------------------------------------------- cross entropy
