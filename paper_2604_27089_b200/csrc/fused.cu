@@ -202,7 +202,8 @@ __global__ void rope_seg_kernel(const __grid_constant__ RopeSegArgs a) {
 // small column-sum kernel (torch's path: two kernels, the weight-gradient one at ~1.6 TB/s).
 constexpr int kNormThreads = 256;
 
-__global__ void __launch_bounds__(kNormThreads) rms_fwd_kernel(
+// d > 4096: strided loop, x read twice (the second time from L1)
+__global__ void __launch_bounds__(kNormThreads) rms_fwd_generic_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
     __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int64_t rows, int d, int64_t ldx,
     int64_t ldy, float eps) {
@@ -230,6 +231,53 @@ __global__ void __launch_bounds__(kNormThreads) rms_fwd_kernel(
 #pragma unroll
       for (int k = 0; k < 8; ++k) f[k] = f[k] * rs * g[k];
       *reinterpret_cast<uint4*>(yr + v * 8) = pack8(f);
+    }
+    if (lane == 0) rstd[r] = rs;
+  }
+}
+
+// One warp per row; lane owns VPL 16-byte vectors (v = lane + 32 i), all loaded up front
+// and kept in registers for the normalising pass (no second read of x).
+template <int VPL>
+__global__ void __launch_bounds__(kNormThreads) rms_fwd_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+    __nv_bfloat16* __restrict__ y, float* __restrict__ rstd, int64_t rows, int d, int64_t ldx,
+    int64_t ldy, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (kNormThreads / 32);
+  const int vpr = d / 8;
+  for (int64_t r = (int64_t)blockIdx.x * (kNormThreads / 32) + (threadIdx.x >> 5); r < rows;
+       r += nw) {
+    const __nv_bfloat16* xr = x + r * ldx;
+    uint4 xv[VPL];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+      if (lane + 32 * i < vpr) xv[i] = *reinterpret_cast<const uint4*>(xr + (lane + 32 * i) * 8);
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      if (lane + 32 * i < vpr) {
+        float f[8];
+        unpack8(xv[i], f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ss = fmaf(f[k], f[k], ss);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float rs = rsqrtf(ss / d + eps);
+    __nv_bfloat16* yr = y + r * ldy;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int v = lane + 32 * i;
+      if (v < vpr) {
+        float f[8], g[8];
+        unpack8(xv[i], f);
+        unpack8(*reinterpret_cast<const uint4*>(w + v * 8), g);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] = f[k] * rs * g[k];
+        *reinterpret_cast<uint4*>(yr + v * 8) = pack8(f);
+      }
     }
     if (lane == 0) rstd[r] = rs;
   }
@@ -539,10 +587,19 @@ extern "C" int autosp_rms_norm_fwd(const void* x, const void* w, void* y, float*
   }
   if (rows == 0) return AUTOSP_OK;
   const int64_t warps = rows;
-  rms_fwd_kernel<<<grid_for(warps * 32, kNormThreads), kNormThreads, 0,
-                   static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
-      static_cast<__nv_bfloat16*>(y), rstd, rows, d, ld_x, ld_y, eps);
+  auto go = [&](auto kern) {
+    kern<<<grid_for(warps * 32, kNormThreads), kNormThreads, 0,
+           static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
+        static_cast<__nv_bfloat16*>(y), rstd, rows, d, ld_x, ld_y, eps);
+  };
+  const int vpl = (d / 8 + 31) / 32;
+  if (vpl <= 1) go(rms_fwd_kernel<1>);
+  else if (vpl <= 2) go(rms_fwd_kernel<2>);
+  else if (vpl <= 4) go(rms_fwd_kernel<4>);
+  else if (vpl <= 8) go(rms_fwd_kernel<8>);
+  else if (vpl <= 16) go(rms_fwd_kernel<16>);
+  else go(rms_fwd_generic_kernel);
   return launched("rms_norm_fwd");
 }
 
@@ -616,7 +673,8 @@ int autosp_preload_fused() {
   cudaFuncGetAttributes(&a, swiglu_bwd_kernel);
   cudaFuncGetAttributes(&a, rope_kernel);
   cudaFuncGetAttributes(&a, rope_seg_kernel);
-  cudaFuncGetAttributes(&a, rms_fwd_kernel);
+  cudaFuncGetAttributes(&a, rms_fwd_kernel<8>);
+  cudaFuncGetAttributes(&a, rms_fwd_kernel<16>);
   cudaFuncGetAttributes(&a, rms_bwd_kernel<8>);
   cudaFuncGetAttributes(&a, rms_bwd_kernel<16>);
   cudaFuncGetAttributes(&a, colsum_kernel);
