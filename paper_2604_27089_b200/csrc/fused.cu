@@ -35,23 +35,68 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
   return v;
 }
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+__device__ __forceinline__ float sigmoidf_(float x) {
+  return __fdividef(1.f, 1.f + __expf(-x));  // MUFU ex2 + rcp (bf16 output: ample precision)
+}
+
+// Grid-stride walk over [rows, ffn/8] 16-byte vectors without a 64-bit division per step
+// (row / column advanced incrementally), two vectors in flight per thread.
+struct VecWalk {
+  int64_t i, r, stride, dr;
+  int c, dc, vpr;
+  __device__ VecWalk(int64_t start, int64_t stride_, int vpr_) : i(start), stride(stride_), vpr(vpr_) {
+    r = start / vpr;
+    c = (int)(start - r * vpr);
+    dr = stride / vpr;
+    dc = (int)(stride - dr * vpr);
+  }
+  __device__ void next(int64_t& rr, int& cc) const {  // position one stride further
+    rr = r + dr;
+    cc = c + dc;
+    if (cc >= vpr) {
+      cc -= vpr;
+      ++rr;
+    }
+  }
+};
 
 // ---------------------------------------------------------------- SwiGLU
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out,
                                   int64_t rows, int ffn, int64_t ld_gu, int64_t ld_out) {
   const int vpr = ffn / 8;
   const int64_t total = rows * vpr;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / vpr;
-    const int c = (int)(i - r * vpr) * 8;
+  VecWalk w((int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, vpr);
+  while (w.i < total) {
+    int64_t r2;
+    int c2;
+    w.next(r2, c2);
+    const bool two = w.i + w.stride < total;
+    const __nv_bfloat16* a = gu + w.r * ld_gu + w.c * 8;
+    const __nv_bfloat16* b = gu + r2 * ld_gu + c2 * 8;
+    const uint4 ga = *reinterpret_cast<const uint4*>(a);
+    const uint4 ua = *reinterpret_cast<const uint4*>(a + ffn);
+    uint4 gb = make_uint4(0, 0, 0, 0), ub = gb;
+    if (two) {
+      gb = *reinterpret_cast<const uint4*>(b);
+      ub = *reinterpret_cast<const uint4*>(b + ffn);
+    }
     float g[8], u[8], o[8];
-    unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + c), g);
-    unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + ffn + c), u);
+    unpack8(ga, g);
+    unpack8(ua, u);
 #pragma unroll
     for (int k = 0; k < 8; ++k) o[k] = g[k] * sigmoidf_(g[k]) * u[k];
-    *reinterpret_cast<uint4*>(out + r * ld_out + c) = pack8(o);
+    *reinterpret_cast<uint4*>(out + w.r * ld_out + w.c * 8) = pack8(o);
+    if (two) {
+      unpack8(gb, g);
+      unpack8(ub, u);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = g[k] * sigmoidf_(g[k]) * u[k];
+      *reinterpret_cast<uint4*>(out + r2 * ld_out + c2 * 8) = pack8(o);
+    }
+    w.i += 2 * w.stride;
+    w.r = r2;
+    w.c = c2;
+    w.next(w.r, w.c);
   }
 }
 
@@ -61,22 +106,43 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu,
                                   int64_t ld_gu, int64_t ld_dout, int64_t ld_dgu) {
   const int vpr = ffn / 8;
   const int64_t total = rows * vpr;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / vpr;
-    const int c = (int)(i - r * vpr) * 8;
+  VecWalk w((int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, vpr);
+  auto one = [&](const uint4& gv, const uint4& uv, const uint4& dv, int64_t r, int c) {
     float g[8], u[8], dy[8], dg[8], du[8];
-    unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + c), g);
-    unpack8(*reinterpret_cast<const uint4*>(gu + r * ld_gu + ffn + c), u);
-    unpack8(*reinterpret_cast<const uint4*>(dout + r * ld_dout + c), dy);
+    unpack8(gv, g);
+    unpack8(uv, u);
+    unpack8(dv, dy);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const float sg = sigmoidf_(g[k]);
       du[k] = dy[k] * g[k] * sg;
       dg[k] = dy[k] * u[k] * sg * (1.f + g[k] * (1.f - sg));  // silu_dx (executor.py:85-88)
     }
-    *reinterpret_cast<uint4*>(dgu + r * ld_dgu + c) = pack8(dg);
-    *reinterpret_cast<uint4*>(dgu + r * ld_dgu + ffn + c) = pack8(du);
+    *reinterpret_cast<uint4*>(dgu + r * ld_dgu + c * 8) = pack8(dg);
+    *reinterpret_cast<uint4*>(dgu + r * ld_dgu + ffn + c * 8) = pack8(du);
+  };
+  while (w.i < total) {
+    int64_t r2;
+    int c2;
+    w.next(r2, c2);
+    const bool two = w.i + w.stride < total;
+    const __nv_bfloat16* a = gu + w.r * ld_gu + w.c * 8;
+    const __nv_bfloat16* b = gu + r2 * ld_gu + c2 * 8;
+    const uint4 ga = *reinterpret_cast<const uint4*>(a);
+    const uint4 ua = *reinterpret_cast<const uint4*>(a + ffn);
+    const uint4 da = *reinterpret_cast<const uint4*>(dout + w.r * ld_dout + w.c * 8);
+    uint4 gb = make_uint4(0, 0, 0, 0), ub = gb, db = gb;
+    if (two) {
+      gb = *reinterpret_cast<const uint4*>(b);
+      ub = *reinterpret_cast<const uint4*>(b + ffn);
+      db = *reinterpret_cast<const uint4*>(dout + r2 * ld_dout + c2 * 8);
+    }
+    one(ga, ua, da, w.r, w.c);
+    if (two) one(gb, ub, db, r2, c2);
+    w.i += 2 * w.stride;
+    w.r = r2;
+    w.c = c2;
+    w.next(w.r, w.c);
   }
 }
 
