@@ -485,7 +485,24 @@ __global__ void __launch_bounds__(kCeThreads) ce_fwd_kernel(const __nv_bfloat16*
   const __nv_bfloat16* x = logits + row * ld;
   float m = -INFINITY, s = 0.f;
   const int64_t nv = vocab / 8;
-  for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+  // two 16-byte vectors per step (both loads in flight), one merge per 16 logits
+  int64_t i = threadIdx.x;
+  for (; i + blockDim.x < nv; i += 2 * blockDim.x) {
+    const uint4 va = *reinterpret_cast<const uint4*>(x + i * 8);
+    const uint4 vb = *reinterpret_cast<const uint4*>(x + (i + blockDim.x) * 8);
+    float f[16];
+    unpack8(va, *reinterpret_cast<float(*)[8]>(&f[0]));
+    unpack8(vb, *reinterpret_cast<float(*)[8]>(&f[8]));
+    float m8[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m8[k] = fmaxf(fmaxf(f[k], f[k + 4]), fmaxf(f[k + 8], f[k + 12]));
+    const float lm = fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3]));
+    float ls = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) ls += __expf(f[k] - lm);
+    online_merge(m, s, lm, ls);
+  }
+  for (; i < nv; i += blockDim.x) {
     float f[8];
     unpack8(*reinterpret_cast<const uint4*>(x + i * 8), f);
     float lm = f[0];
