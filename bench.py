@@ -237,7 +237,8 @@ def main():
         from paper_2604_27089_b200.zero import ShardedAdamW
         opt = ShardedAdamW(model.parameters(), st, lr=1e-4)
     else:
-        opt = torch.optim.AdamW(model.parameters(), lr=1e-4, fused=True)
+        from paper_2604_27089_b200.optim import AdamW  # multi-tensor bf16 kernel
+        opt = AdamW(model.parameters(), lr=1e-4)
     cm = autosp.compile(model)
     g = torch.Generator(device="cpu").manual_seed(1234)
     ids_full = torch.randint(0, cfg.vocab, (b, S + 1), generator=g)

@@ -235,6 +235,22 @@ AUTOSP_API int autosp_ce_fwd(const void* logits, const int64_t* labels, float* l
 AUTOSP_API int autosp_ce_bwd(void* logits, const int64_t* labels, const float* lse, float g,
                              int64_t rows, int64_t vocab, int64_t ld, void* stream);
 
+/* Multi-tensor AdamW for bf16 parameters with bf16 moments (the optimizer step of the
+ * training loop the bench times; not part of the reference, whose workload has no
+ * optimizer).  Same update order as torch.optim.AdamW: p *= 1 - lr*wd; m = lerp(m, g, 1-b1);
+ * v = b2 v + (1-b2) g^2; p -= lr/(1-b1^t) * m / (sqrt(v)/sqrt(1-b2^t) + eps), fp32 math.
+ * `tensors` is a host array; up to 64 tensors per kernel launch. */
+typedef struct {
+  void* p;
+  const void* g;
+  void* m;
+  void* v;
+  int64_t n;
+} autosp_adamw_tensor;
+AUTOSP_API int autosp_adamw_bf16(const autosp_adamw_tensor* tensors, int count, float lr,
+                                 float beta1, float beta2, float eps, float weight_decay,
+                                 int step, void* stream);
+
 /* debug only: per-step timeline of the backward's first CTA into dev_buf (16 x 64 int64) */
 AUTOSP_API int autosp_debug_set_bwd_trace(long long* dev_buf);
 AUTOSP_API int autosp_debug_set_fwd_trace(long long* dev_buf);

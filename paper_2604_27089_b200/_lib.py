@@ -95,6 +95,7 @@ EXPORTS = {
                                       C.c_int64, C.c_int64, C.c_void_p]),
     "autosp_ce_fwd": (C.c_int, [C.c_void_p] * 4 + [C.c_int64] * 3 + [C.c_void_p]),
     "autosp_ce_bwd": (C.c_int, [C.c_void_p] * 3 + [C.c_float] + [C.c_int64] * 3 + [C.c_void_p]),
+    "autosp_adamw_bf16": (C.c_int, [C.c_void_p, C.c_int] + [C.c_float] * 5 + [C.c_int, C.c_void_p]),
     "autosp_debug_set_bwd_trace": (C.c_int, [C.c_void_p]),
     "autosp_debug_set_fwd_trace": (C.c_int, [C.c_void_p]),
     "autosp_attn_bwd_workspace_bytes": (C.c_size_t, [C.c_int] * 4),

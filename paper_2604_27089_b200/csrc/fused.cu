@@ -765,3 +765,118 @@ int autosp_preload_fused() {
   cudaFuncGetAttributes(&a, ce_bwd_kernel);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
+
+// ---------------------------------------------------------------- AdamW (bf16 params/state)
+// One launch updates up to kAdamwMaxT tensors: block b works on 2048 elements of the
+// tensor whose chunk range holds b (binary search over the chunk prefix).  Math in fp32,
+// the same sequence as torch's AdamW: p *= 1 - lr*wd; m = lerp(m, g, 1-b1);
+// v = b2*v + (1-b2)*g^2; p -= lr/bc1 * m / (sqrt(v)/sqrt(bc2) + eps).
+namespace adamw_impl {
+constexpr int kAdamwMaxT = 64;
+constexpr int kAdamwThreads = 256;
+constexpr int kAdamwChunk = kAdamwThreads * 8;
+struct AdamwArgs {
+  __nv_bfloat16* p[kAdamwMaxT];
+  const __nv_bfloat16* g[kAdamwMaxT];
+  __nv_bfloat16* m[kAdamwMaxT];
+  __nv_bfloat16* v[kAdamwMaxT];
+  int64_t n[kAdamwMaxT];
+  int64_t chunk0[kAdamwMaxT + 1];  // prefix of chunk counts
+  int count;
+  float lr, b1, b2, eps, decay, step_size, inv_sqrt_bc2;
+};
+
+__device__ __forceinline__ void adamw_one(float& p, float g, float& m, float& v,
+                                          const AdamwArgs& a) {
+  p *= a.decay;
+  m = m + (1.f - a.b1) * (g - m);
+  v = a.b2 * v + (1.f - a.b2) * g * g;
+  p -= a.step_size * m / (sqrtf(v) * a.inv_sqrt_bc2 + a.eps);
+}
+
+__global__ void __launch_bounds__(kAdamwThreads) adamw_bf16_kernel(const __grid_constant__ AdamwArgs a) {
+  const int64_t blk = blockIdx.x;
+  int lo = 0, hi = a.count - 1;  // last t with chunk0[t] <= blk
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.chunk0[mid] <= blk) lo = mid;
+    else hi = mid - 1;
+  }
+  const int t = lo;
+  const int64_t e0 = (blk - a.chunk0[t]) * kAdamwChunk + threadIdx.x * 8;
+  const int64_t n = a.n[t];
+  if (e0 >= n) return;
+  __nv_bfloat16* P = a.p[t] + e0;
+  const __nv_bfloat16* G = a.g[t] + e0;
+  __nv_bfloat16* M = a.m[t] + e0;
+  __nv_bfloat16* V = a.v[t] + e0;
+  const bool vec = e0 + 8 <= n && ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(G) |
+                                     reinterpret_cast<uintptr_t>(M) | reinterpret_cast<uintptr_t>(V)) & 15) == 0;
+  if (vec) {
+    float p[8], g[8], m[8], v[8];
+    unpack8(*reinterpret_cast<const uint4*>(P), p);
+    unpack8(*reinterpret_cast<const uint4*>(G), g);
+    unpack8(*reinterpret_cast<const uint4*>(M), m);
+    unpack8(*reinterpret_cast<const uint4*>(V), v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) adamw_one(p[k], g[k], m[k], v[k], a);
+    *reinterpret_cast<uint4*>(P) = pack8(p);
+    *reinterpret_cast<uint4*>(M) = pack8(m);
+    *reinterpret_cast<uint4*>(V) = pack8(v);
+  } else {
+    for (int k = 0; k < 8 && e0 + k < n; ++k) {
+      float p = __bfloat162float(P[k]), g = __bfloat162float(G[k]);
+      float m = __bfloat162float(M[k]), v = __bfloat162float(V[k]);
+      adamw_one(p, g, m, v, a);
+      P[k] = __float2bfloat16_rn(p);
+      M[k] = __float2bfloat16_rn(m);
+      V[k] = __float2bfloat16_rn(v);
+    }
+  }
+}
+}  // namespace adamw_impl
+
+extern "C" int autosp_adamw_bf16(const autosp_adamw_tensor* tensors, int count, float lr,
+                                 float beta1, float beta2, float eps, float weight_decay, int step,
+                                 void* stream) {
+  if ((count > 0 && !tensors) || count < 0 || step < 1) {
+    autosp_set_error("adamw_bf16: bad arguments (count %d, step %d)", count, step);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
+  for (int base = 0; base < count; base += adamw_impl::kAdamwMaxT) {
+    adamw_impl::AdamwArgs a{};
+    a.count = 0;
+    int64_t chunks = 0;
+    for (int i = base; i < count && a.count < adamw_impl::kAdamwMaxT; ++i) {
+      const autosp_adamw_tensor& t = tensors[i];
+      if (t.n <= 0) continue;
+      if (!t.p || !t.g || !t.m || !t.v) {
+        autosp_set_error("adamw_bf16: tensor %d has a null pointer", i);
+        return AUTOSP_ERR_VALIDATION;
+      }
+      const int j = a.count++;
+      a.p[j] = static_cast<__nv_bfloat16*>(t.p);
+      a.g[j] = static_cast<const __nv_bfloat16*>(t.g);
+      a.m[j] = static_cast<__nv_bfloat16*>(t.m);
+      a.v[j] = static_cast<__nv_bfloat16*>(t.v);
+      a.n[j] = t.n;
+      a.chunk0[j] = chunks;
+      chunks += (t.n + adamw_impl::kAdamwChunk - 1) / adamw_impl::kAdamwChunk;
+    }
+    if (a.count == 0) continue;
+    a.chunk0[a.count] = chunks;
+    a.lr = lr;
+    a.b1 = beta1;
+    a.b2 = beta2;
+    a.eps = eps;
+    a.decay = 1.f - lr * weight_decay;
+    a.step_size = lr / bc1;
+    a.inv_sqrt_bc2 = 1.f / sqrtf(bc2);
+    adamw_impl::adamw_bf16_kernel<<<(unsigned)chunks, adamw_impl::kAdamwThreads, 0,
+                               static_cast<cudaStream_t>(stream)>>>(a);
+    const int rc = launched("adamw_bf16");
+    if (rc) return rc;
+  }
+  return AUTOSP_OK;
+}

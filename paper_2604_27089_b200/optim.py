@@ -1,0 +1,63 @@
+"""AdamW over bf16 parameters with bf16 moments, one multi-tensor sm_100a kernel per 64
+tensors (`autosp_adamw_bf16`, csrc/fused.cu).  Drop-in for
+``torch.optim.AdamW(params, lr, betas, eps, weight_decay, fused=True)`` on bf16 CUDA
+parameters (same update order, fp32 math, bf16 state); the training step the bench
+times ends with it.  No CPU path: CUDA bf16 parameters only."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+
+
+class _Tensor(C.Structure):
+    _fields_ = [("p", C.c_void_p), ("g", C.c_void_p), ("m", C.c_void_p), ("v", C.c_void_p),
+                ("n", C.c_int64)]
+
+
+class AdamW(torch.optim.Optimizer):
+    def __init__(self, params, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
+                 weight_decay: float = 1e-2):
+        super().__init__(params, dict(lr=lr, betas=betas, eps=eps, weight_decay=weight_decay))
+        for group in self.param_groups:
+            for p in group["params"]:
+                if p.dtype != torch.bfloat16 or not p.is_cuda or not p.is_contiguous():
+                    raise ValueError("optim.AdamW: contiguous bf16 CUDA parameters only")
+
+    @torch.no_grad()
+    def step(self, closure=None):
+        loss = closure() if closure is not None else None
+        lib = _lib.load()
+        stream = torch.cuda.current_stream().cuda_stream
+        for group in self.param_groups:
+            live = [p for p in group["params"] if p.grad is not None]
+            if not live:
+                continue
+            arr = (_Tensor * len(live))()
+            step = None
+            for i, p in enumerate(live):
+                st = self.state[p]
+                if not st:
+                    st["step"] = 0
+                    st["exp_avg"] = torch.zeros_like(p)
+                    st["exp_avg_sq"] = torch.zeros_like(p)
+                st["step"] += 1
+                step = st["step"]
+                g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
+                if g.dtype != torch.bfloat16:
+                    raise ValueError("optim.AdamW: bf16 gradients only")
+                st["_g"] = g  # keep a made-contiguous gradient alive until the launch
+                arr[i] = _Tensor(p.data_ptr(), g.data_ptr(), st["exp_avg"].data_ptr(),
+                                 st["exp_avg_sq"].data_ptr(), p.numel())
+            b1, b2 = group["betas"]
+            rc = lib.autosp_adamw_bf16(arr, len(live), group["lr"], b1, b2, group["eps"],
+                                       group["weight_decay"], step, stream)
+            for p in live:
+                self.state[p].pop("_g", None)
+            _lib.check(rc, "adamw_bf16")
+            from .kernels import LOG
+            LOG.end("adamw", None, (len(live) + 63) // 64)
+        return loss

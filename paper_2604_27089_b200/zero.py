@@ -9,7 +9,7 @@ slice r of every chunk.  ``step()``:
   1. per chunk: the per-rank partial gradients (Ulysses SP produces partials, finding 6)
      are packed and reduce-scattered over the SP group -> this rank's summed shard
      (averaged over the DP group when there is one);
-  2. AdamW on the owned shards only (torch's implementation, fused on CUDA) -- optimizer
+  2. AdamW on the owned shards only (optim.AdamW for bf16 on CUDA, torch otherwise) -- optimizer
      state is 1/P of the model per rank;
   3. the updated shards are all-gathered back into the full parameters.
 
@@ -54,9 +54,13 @@ class ShardedAdamW:
             sh = torch.nn.Parameter(self._gather_params(lo, lo + n))
             self.shards.append(sh)
         kw = dict(adamw_kwargs)
-        if self.device.type == "cuda":
-            kw.setdefault("fused", True)
-        self.inner = torch.optim.AdamW(self.shards, **kw)
+        if self.device.type == "cuda" and self.dtype == torch.bfloat16:
+            from .optim import AdamW  # the multi-tensor bf16 kernel
+            self.inner = AdamW(self.shards, **kw)
+        else:
+            if self.device.type == "cuda":
+                kw.setdefault("fused", True)
+            self.inner = torch.optim.AdamW(self.shards, **kw)
 
     # -------------------------------------------------------------- flat-vector helpers
     def _pieces(self, lo: int, hi: int):
