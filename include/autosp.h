@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define AUTOSP_ABI_VERSION 1
+#define AUTOSP_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define AUTOSP_API __attribute__((visibility("default")))
@@ -122,11 +122,15 @@ AUTOSP_API int autosp_a2a_rope(int direction, const autosp_a2a_tensor* tensors, 
                void* const* peer_base, uint32_t* const* peer_flags, uint32_t epoch,
                const float* pos, float theta, void* stream);
 /* Stream-ordered wait until every peer has published `epoch` into this rank's flag
- * block (the receive region then holds the complete a2a output).  `first_dst_offset` is
- * this rank's dst_offset of tensor 0 for the call: every sender records its own view of
- * it and the wait traps on disagreement (symmetric-allocation invariant).           */
+ * block (the receive region then holds the complete a2a output).  `check` is the check
+ * word of the call as THIS rank sees it (autosp_a2a_check of its descriptors, or
+ * autosp_push_check for autosp_attn_fwd_push): every sender publishes the check word of
+ * its own descriptors (all destination offsets, strides and head counts of the call) and
+ * the wait traps on any disagreement (symmetric-allocation invariant).              */
 AUTOSP_API int autosp_a2a_wait(uint32_t* local_flags, int world, int rank, uint32_t epoch,
-                               int64_t first_dst_offset, void* stream);
+                               uint32_t check, void* stream);
+AUTOSP_API uint32_t autosp_a2a_check(int direction, const autosp_a2a_tensor* tensors,
+                                     int n_tensors);
 /* Single-process loopback used by tests / benchmarks on one GPU: marks `epoch` as reached
  * for all `world` virtual ranks whose flag blocks are given.                           */
 AUTOSP_API int autosp_a2a_mark_ready(uint32_t* const* flags, int world, uint32_t epoch, void* stream);
@@ -165,6 +169,8 @@ typedef struct autosp_push_spec {
   uint32_t epoch;
 } autosp_push_spec;
 
+/* check word of an autosp_attn_fwd_push call on `heads` local heads (see autosp_a2a_wait) */
+AUTOSP_API uint32_t autosp_push_check(const autosp_push_spec* push, int heads);
 AUTOSP_API int autosp_attn_fwd_push(autosp_attn_tensor q, autosp_attn_tensor k,
                     autosp_attn_tensor v, autosp_attn_tensor o, float* lse, int b, int hq,
                     int hkv, int s, int d, float scale, int causal,
@@ -196,7 +202,9 @@ AUTOSP_API int autosp_attn_bwd_delta(autosp_attn_tensor q, autosp_attn_tensor k,
  *   rope:   rotate-half RoPE of x [b, s, h, d] (strided) with angles pos[t] * theta^(-2i/d);
  *           inverse = 1 rotates by the negative angle (the backward)
  *   ce:     per-row log-sum-exp / cross entropy over bf16 logits [rows, vocab] (leading dim
- *           ld); ce_bwd overwrites the logits with g * (softmax - onehot(label))          */
+ *           ld); ce_bwd overwrites the logits with g * (softmax - onehot(label)).  Rows whose
+ *           label lies outside [0, vocab) (the -100 padding convention) are ignored: loss 0
+ *           and an all-zero gradient row.                                                */
 AUTOSP_API int autosp_swiglu_fwd(const void* gu, void* out, int64_t rows, int ffn, int64_t ld_gu,
                                  int64_t ld_out, void* stream);
 AUTOSP_API int autosp_swiglu_bwd(const void* gu, const void* dout, void* dgu, int64_t rows,

@@ -33,20 +33,25 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
     build_dir = PKG / "build"
     build_dir.mkdir(exist_ok=True)
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = build_dir / (src + ".o")
         cmd = [NVCC, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
-        if verbose:
-            print(r.stderr, file=sys.stderr)
-        objs.append(str(obj))
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        for src, obj, r in ex.map(compile_one, SOURCES):
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+            if verbose:
+                print(r.stderr, file=sys.stderr)
+            objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs,
            "-o", str(tmp), "-lcudart"]

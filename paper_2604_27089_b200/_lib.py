@@ -13,7 +13,7 @@ from .errors import (CudaError, ExtensionMissingError, SeqcompError, Unsupported
                      ValidationError)
 
 LIB_PATH = Path(os.environ.get("AUTOSP_LIB") or Path(__file__).resolve().parent / "libautosp.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 IPC_HANDLE_BYTES = 64
 MAX_WORLD = 8
 MAX_A2A_TENSORS = 4
@@ -72,7 +72,9 @@ EXPORTS = {
                                   C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p),
                                   C.POINTER(C.c_void_p), C.c_uint32, C.c_void_p, C.c_float,
                                   C.c_void_p]),
-    "autosp_a2a_wait": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_uint32, C.c_int64,
+    "autosp_a2a_check": (C.c_uint32, [C.c_int, C.POINTER(A2ATensor), C.c_int]),
+    "autosp_push_check": (C.c_uint32, [C.c_void_p, C.c_int]),
+    "autosp_a2a_wait": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_uint32, C.c_uint32,
                                   C.c_void_p]),
     "autosp_a2a_mark_ready": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_uint32,
                                         C.c_void_p]),

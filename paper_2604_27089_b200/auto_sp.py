@@ -24,6 +24,7 @@ lowered to the sm_100a kernel.
 from __future__ import annotations
 
 import operator
+import warnings
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -45,13 +46,28 @@ class RewriteReason(str, Enum):  # sp_pass.py:34-37
 ATTN_OPS = (torch._C._nn.scaled_dot_product_attention, F.scaled_dot_product_attention)
 
 
-def positions(n: int, device=None) -> torch.Tensor:
-    """Explicit position-index op (reference OpKind.POSITION_INDEX): auto_sp offsets it by
-    rank * s/P.  Equivalent to torch.arange(n) when run without the pass."""
+@torch.library.custom_op("autosp::positions", mutates_args=())
+def _positions(n: int, device: torch.device) -> torch.Tensor:
     return torch.arange(n, device=device)
 
 
-INDEX_OPS = (positions, torch.arange)
+@_positions.register_fake
+def _positions_fake(n, device):
+    return torch.empty(n, dtype=torch.int64, device=device)
+
+
+def positions(n: int, device=None) -> torch.Tensor:
+    """Explicit position-index op (reference OpKind.POSITION_INDEX,
+    ``executor.py:68-70``): the positions of the n tokens of THIS rank's shard.  auto_sp
+    offsets it by rank * n.  An opaque graph node (not inlined into an arange), so it is
+    found in any Dynamo subgraph, including one with no attention after a graph break.
+    Equal to torch.arange(n) when run without the pass."""
+    dev = torch.device(device) if device is not None else torch.get_default_device()
+    return torch.ops.autosp.positions(n, dev)
+
+
+_POSITIONS = (torch.ops.autosp.positions.default, torch.ops.autosp.positions)
+INDEX_OPS = (*_POSITIONS, torch.arange)
 _LOWERED = (ops.ulysses_attention, ops.sdpa, ops.ulysses_qkv_block)
 FUSE_QKV_ROPE = True  # fold autosp::qkv_rope (RoPE + split + transpose) into the reshard
 
@@ -99,7 +115,7 @@ class SPDims:  # reference infer_dims (sp_pass.py:102-123), on the local shard
 @dataclass
 class SPGraphInfo:
     world_size: int
-    dims: SPDims
+    dims: SPDims | None  # None: a Dynamo subgraph without attention (graph break)
     provenance: dict[str, RewriteReason] = field(default_factory=dict)
 
 
@@ -117,6 +133,20 @@ def infer_dims(gm: fx.GraphModule, example_inputs) -> SPDims:
         raise ValidationError("cannot read [b, h, s, d] from the first attention's query")
     b, h, s, d = qv.shape
     return SPDims(b=int(b), s_local=int(s), h=int(h), d=int(d), layers=len(attn))
+
+
+def _token_input_len(gm: fx.GraphModule) -> int | None:
+    """Local sequence length from the graph's single rank-2 integer input (the token ids;
+    reference infer_dims reads b, s from "the single rank-2 input", sp_pass.py:102-123)."""
+    cands = []
+    for n in gm.graph.nodes:
+        if n.op != "placeholder":
+            continue
+        v = _val(n)
+        if isinstance(v, torch.Tensor) and v.dim() == 2 and not v.dtype.is_floating_point \
+                and v.dtype != torch.bool:
+            cands.append(int(v.shape[1]))
+    return cands[0] if len(set(cands)) == 1 else None
 
 
 def _is_int_arange_of(node: fx.Node, length: int) -> tuple[bool, int, int, int]:
@@ -142,7 +172,13 @@ def auto_sp(gm: fx.GraphModule, example_inputs, st: SPState) -> tuple[fx.GraphMo
     g = gm.graph
     if any(n.op == "call_function" and n.target in _LOWERED for n in g.nodes):
         raise ValidationError("graph already lowered by auto_sp (pass already applied)")
-    dims = infer_dims(gm, example_inputs)
+    has_attn = any(n.op == "call_function" and n.target in ATTN_OPS for n in g.nodes)
+    # a Dynamo subgraph without attention (the model graph-breaks, e.g. between the
+    # embedding / positions and the first layer) is still rewritten: its position indices
+    # need the rank offset.  positions(n) always denotes the local shard; a bare
+    # torch.arange is matched against the local length read from the token-id input.
+    dims = infer_dims(gm, example_inputs) if has_attn else None
+    s_local = dims.s_local if dims is not None else _token_input_len(gm)
     P = st.world
     info = SPGraphInfo(world_size=P, dims=dims)
     for n in list(g.nodes):
@@ -188,15 +224,27 @@ def auto_sp(gm: fx.GraphModule, example_inputs, st: SPState) -> tuple[fx.GraphMo
                     g.erase_node(it)
                 g.erase_node(rq)
         elif n.target in INDEX_OPS and P > 1:
-            if n.target is positions:
+            if n.target in _POSITIONS:
                 length = n.args[0]
                 ok, start, end = isinstance(length, int), 0, length
+                if not ok:
+                    raise ValidationError("autosp.positions needs a static length")
+                local = length
             else:
-                ok, start, end, _ = _is_int_arange_of(n, dims.s_local)
-            if not ok or (end - start) != dims.s_local:
+                if s_local is None:
+                    if n.kwargs.get("dtype") is None or not n.kwargs["dtype"].is_floating_point:
+                        warnings.warn("auto_sp: torch.arange in a subgraph with no attention and "
+                                      "no token-id input is left unshifted; use "
+                                      "autosp.positions(n) for position indices")
+                    continue
+                ok, start, end, _ = _is_int_arange_of(n, s_local)
+                local = s_local
+            if not ok or (end - start) != local:
                 continue
-            off = st.rank * dims.s_local
+            off = st.rank * local
             kwargs = {k: v for k, v in n.kwargs.items() if k in ("device", "dtype")}
+            if n.target in _POSITIONS:
+                kwargs = {"device": n.args[1] if len(n.args) > 1 else n.kwargs["device"]}
             with g.inserting_before(n):
                 new = g.call_function(torch.arange, (start + off, end + off), kwargs)
             new.meta.update(n.meta)

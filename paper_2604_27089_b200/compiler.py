@@ -11,6 +11,8 @@ AcMode + plan_checkpoints (ac_pass.py:26-29,181-184)."""
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import dist as sp_dist
@@ -66,7 +68,42 @@ def backend(passes: list[str] | None = None, ac_mode: AcMode | None = None):
     return _backend
 
 
+def _frames():
+    from torch._dynamo.utils import counters
+    f = counters["frames"]
+    return f.get("total", 0), f.get("ok", 0)
+
+
 def compile(model: torch.nn.Module, passes: list[str] | None = None,
             ac_mode: AcMode | None = None) -> torch.nn.Module:
-    """``model.compile()`` with the AutoSP backend (static shapes)."""
-    return torch.compile(model, backend=backend(passes, ac_mode), dynamic=False, fullgraph=False)
+    """``model.compile()`` with the AutoSP backend (static shapes).
+
+    Graph breaks are allowed (``fullgraph=False``): auto_sp rewrites every Dynamo
+    subgraph, including attention-free ones.  But a frame Dynamo gives up on (e.g. a
+    graph break inside a loop: "skipping the frame and falling back to eager") would run
+    its attention eagerly over the LOCAL shard only -- silently wrong at P > 1.  So at
+    P > 1 a call that left any frame uncompiled raises ValidationError (set
+    AUTOSP_ALLOW_EAGER_FRAMES=1 if the skipped frames are known to hold no attention)."""
+    passes_eff = list(_PASSES if passes is None else passes)
+    cm = torch.compile(model, backend=backend(passes, ac_mode), dynamic=False, fullgraph=False)
+    if "auto_sp" not in passes_eff:
+        return cm
+    snap = {}
+
+    def pre(_mod, _args):
+        snap["f"] = _frames()
+
+    def post(_mod, _args, _out):
+        t0, ok0 = snap.pop("f", (0, 0))
+        t1, ok1 = _frames()
+        if (t1 - t0) > (ok1 - ok0) and sp_dist.state().world > 1 and \
+                os.environ.get("AUTOSP_ALLOW_EAGER_FRAMES") != "1":
+            raise ValidationError(
+                f"{(t1 - t0) - (ok1 - ok0)} frame(s) of the model fell back to eager execution "
+                "(a graph break inside a loop?): attention there would not be sequence-"
+                "parallel.  Move the graph break out of the loop (or set "
+                "AUTOSP_ALLOW_EAGER_FRAMES=1 if those frames hold no attention).")
+
+    cm.register_forward_pre_hook(pre)
+    cm.register_forward_hook(post)
+    return cm

@@ -377,7 +377,7 @@ static int a2a_impl(int direction, const autosp_a2a_tensor* tensors, int n_tenso
   p.P = world;
   p.rank = rank;
   p.epoch = epoch;
-  p.check = (uint32_t)((uint64_t)tensors[0].dst_offset >> 4);
+  p.check = autosp_a2a_check(direction, tensors, n_tensors);
   for (int j = 0; j < world; ++j) {
     p.peer_base[j] = static_cast<char*>(peer_base[j]);
     p.peer_flags[j] = peer_flags[j];
@@ -462,15 +462,42 @@ static int a2a_impl(int direction, const autosp_a2a_tensor* tensors, int n_tenso
   return AUTOSP_OK;
 }
 
+extern "C" uint32_t autosp_a2a_check(int direction, const autosp_a2a_tensor* tensors,
+                                     int n_tensors) {
+  autosp::CheckHash h;
+  h.add(direction);
+  h.add(n_tensors);
+  for (int i = 0; tensors && i < n_tensors; ++i) {
+    const autosp_a2a_tensor& T = tensors[i];
+    h.add(T.dst_offset);
+    h.add(T.dst_stride_b);
+    h.add(T.dst_stride_s);
+    h.add(T.dst_stride_h);
+    h.add(T.heads);
+  }
+  return h.h;
+}
+
+extern "C" uint32_t autosp_push_check(const autosp_push_spec* push, int heads) {
+  if (!push) return 0u;
+  autosp_a2a_tensor t{};
+  t.dst_offset = push->dst_offset;
+  t.dst_stride_b = push->dst_stride_b;
+  t.dst_stride_s = push->dst_stride_s;
+  t.dst_stride_h = push->dst_stride_h;
+  t.heads = heads;
+  return autosp_a2a_check(AUTOSP_HEAD_TO_SEQ, &t, 1);
+}
+
 extern "C" int autosp_a2a_wait(uint32_t* local_flags, int world, int rank, uint32_t epoch,
-                               int64_t first_dst_offset, void* stream) {
+                               uint32_t check, void* stream) {
   if (!local_flags || world < 1 || world > AUTOSP_MAX_WORLD || rank < 0 || rank >= world) {
     autosp_set_error("bad a2a_wait arguments (world %d rank %d)", world, rank);
     return AUTOSP_ERR_VALIDATION;
   }
   if (world == 1) return AUTOSP_OK;
   autosp::a2a_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
-      local_flags, world, rank, epoch, (uint32_t)((uint64_t)first_dst_offset >> 4));
+      local_flags, world, rank, epoch, check);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     autosp_set_error("a2a_wait launch failed: %s", cudaGetErrorString(e));

@@ -612,7 +612,7 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
       p.peer_flags[j] = push->peer_flags[j];
     }
     p.epoch = push->epoch;
-    p.check = (uint32_t)((uint64_t)push->dst_offset >> 4);
+    p.check = autosp_push_check(push, Hq);
   }
   if (!make_map_bhsd(&p.tm_q, q.ptr, B, Hq, S, D, q.stride_b, q.stride_h, q.stride_s, C::CE, BM,
                      C::SW) ||

@@ -36,4 +36,19 @@ AUTOSP_DEV void publish_arrival(uint32_t* const* peer_flags, int P, int rank, ui
   }
 }
 
+// Check word of one call: FNV-1a over every destination descriptor (offset, strides,
+// heads) of the call, computed by the sender from its descriptors and by the receiver from
+// its own; a2a_wait traps when they differ (the symmetric-allocation invariant).
+struct CheckHash {
+  uint32_t h = 2166136261u;
+  void add(int64_t v) {
+    uint64_t u = static_cast<uint64_t>(v);
+    for (int i = 0; i < 8; ++i) {
+      h ^= static_cast<uint32_t>(u & 0xffu);
+      h *= 16777619u;
+      u >>= 8;
+    }
+  }
+};
+
 }  // namespace autosp

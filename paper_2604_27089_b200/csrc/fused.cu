@@ -532,7 +532,9 @@ __global__ void __launch_bounds__(kCeThreads) ce_fwd_kernel(const __nv_bfloat16*
     for (int w = 1; w < kCeThreads / 32; ++w) online_merge(M, Ssum, sm[w], ss[w]);
     const float l = M + logf(Ssum);
     lse[row] = l;
-    loss[row] = l - __bfloat162float(x[labels[row]]);
+    // labels outside [0, vocab) (e.g. the -100 padding convention) are ignored: loss 0
+    const int64_t lab = labels[row];
+    loss[row] = (lab >= 0 && lab < vocab) ? l - __bfloat162float(x[lab]) : 0.f;
   }
 }
 
@@ -546,6 +548,12 @@ __global__ void __launch_bounds__(kCeThreads) ce_bwd_kernel(__nv_bfloat16* __res
   const float l = lse[row];
   const int64_t lab = labels[row];
   const int64_t nv = vocab / 8;
+  if (lab < 0 || lab >= vocab) {  // ignored row: zero gradient
+    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x)
+      *reinterpret_cast<uint4*>(x + i * 8) = make_uint4(0u, 0u, 0u, 0u);
+    for (int64_t i = nv * 8 + threadIdx.x; i < vocab; i += blockDim.x) x[i] = __float2bfloat16(0.f);
+    return;
+  }
   for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
     float f[8];
     unpack8(*reinterpret_cast<const uint4*>(x + i * 8), f);
@@ -844,11 +852,14 @@ extern "C" int autosp_adamw_bf16(const autosp_adamw_tensor* tensors, int count, 
     return AUTOSP_ERR_VALIDATION;
   }
   const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
-  for (int base = 0; base < count; base += adamw_impl::kAdamwMaxT) {
+  // each launch packs the next (up to) 64 NON-EMPTY tensors; `next` is the first tensor
+  // not yet packed, so empty tensors are skipped without updating any tensor twice
+  for (int next = 0; next < count;) {
     adamw_impl::AdamwArgs a{};
     a.count = 0;
     int64_t chunks = 0;
-    for (int i = base; i < count && a.count < adamw_impl::kAdamwMaxT; ++i) {
+    for (; next < count && a.count < adamw_impl::kAdamwMaxT; ++next) {
+      const int i = next;
       const autosp_adamw_tensor& t = tensors[i];
       if (t.n <= 0) continue;
       if (!t.p || !t.g || !t.m || !t.v) {

@@ -106,7 +106,7 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool = T
 def attn_fwd_push(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor | None,
                   lse: torch.Tensor, scale: float, causal: bool, world: int, rank: int,
                   dst_offset: int, dst_strides: tuple[int, int, int], peer_base: list[int],
-                  peer_flags: list[int], epoch: int) -> None:
+                  peer_flags: list[int], epoch: int) -> int:
     """Fused K3 + K2 (autosp_attn_fwd_push): attention into o/lse AND every output row
     pushed to its token owner's receive region (head->seq all-to-all from the epilogue).
     dst_strides are the (b, s, h) element strides of the token-major destination."""
@@ -125,6 +125,7 @@ def attn_fwd_push(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Te
                                   _stream())
     _lib.check(rc, "attn_fwd_push")
     LOG.end("attn_fwd", ev, 2 if world > 1 else 1, causal_attn_flops(b, hq, s, d, causal))
+    return int(lib.autosp_push_check(C.byref(spec), hq))
 
 
 def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = None,
@@ -179,9 +180,9 @@ def a2a_tensor_desc(src: torch.Tensor, heads: int, dst_offset: int,
 
 def a2a_launch(direction: int, descs: list, b: int, s_global: int, d: int, elem_bytes: int,
                world: int, rank: int, peer_base: list[int], peer_flags: list[int],
-               epoch: int, pos: torch.Tensor | None = None, theta: float = 0.0) -> None:
+               epoch: int, pos: torch.Tensor | None = None, theta: float = 0.0) -> int:
     """K1/K2.  With `pos` (fp32 positions of the source tokens) the descriptors flagged
-    rope are rotated on the way (autosp_a2a_rope)."""
+    rope are rotated on the way (autosp_a2a_rope).  Returns the call's check word."""
     lib = _lib.load()
     arr = (_lib.A2ATensor * len(descs))(*descs)
     pb = (C.c_void_p * world)(*peer_base)
@@ -198,11 +199,21 @@ def a2a_launch(direction: int, descs: list, b: int, s_global: int, d: int, elem_
                                  _stream())
     _lib.check(rc, "a2a")
     LOG.end("a2a", ev, 2 if world > 1 else 1)
+    return a2a_check(direction, descs)
 
 
-def a2a_wait(local_flags: int, world: int, rank: int, epoch: int, first_dst_offset: int = 0) -> None:
+def a2a_check(direction: int, descs: list) -> int:
+    """Check word of a call with these destination descriptors (what autosp_a2a_wait
+    compares against every sender's own view)."""
+    arr = (_lib.A2ATensor * len(descs))(*descs)
+    return int(_lib.load().autosp_a2a_check(direction, arr, len(descs)))
+
+
+def a2a_wait(local_flags: int, world: int, rank: int, epoch: int, check: int) -> None:
+    """Wait for every peer's arrival of `epoch`; `check` = this rank's check word of the
+    call (a2a_launch's / attn_fwd_push's return value)."""
     rc = _lib.load().autosp_a2a_wait(local_flags, world, rank, epoch & 0xFFFFFFFF,
-                                     first_dst_offset, _stream())
+                                     check & 0xFFFFFFFF, _stream())
     _lib.check(rc, "a2a_wait")
     LOG.end("a2a_wait", None, 1 if world > 1 else 0)
 
@@ -237,9 +248,9 @@ def a2a_loopback(direction: str, shards: list[torch.Tensor]) -> list[torch.Tenso
     a2a_mark_ready(fptr, 1)
     for r in range(P):
         desc = a2a_tensor_desc(shards[r], h_src, 0, (ostr[0], ostr[1], ostr[2]))
-        a2a_launch(dirn, [desc], b, s_glob, d, eb, P, r, optr, fptr, 1)
+        chk = a2a_launch(dirn, [desc], b, s_glob, d, eb, P, r, optr, fptr, 1)
     for r in range(P):
-        a2a_wait(fptr[r], P, r, 1)
+        a2a_wait(fptr[r], P, r, 1, chk)
     return outs
 
 

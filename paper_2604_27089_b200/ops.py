@@ -149,7 +149,7 @@ def all_to_all(xs: list[torch.Tensor], direction: int, group: str) -> list[torch
     if P == 1:
         return [x.clone() for x in xs]  # executor.py:208-209 (P == 1 -> copy)
     pool = st.pool
-    descs, outs, first_off = [], [], None
+    descs, outs = [], []
     b, _, s, d = xs[0].shape
     for x in xs:
         if x.stride(-1) != 1:
@@ -157,7 +157,6 @@ def all_to_all(xs: list[torch.Tensor], direction: int, group: str) -> list[torch
         shape, strides = _out_geometry(x, direction, P)
         nbytes = math.prod(shape) * x.element_size()
         off, base = pool.alloc(nbytes)
-        first_off = off if first_off is None else first_off
         out = base.view(x.dtype).as_strided(shape, strides)
         outs.append(out)
         # kernel convention: logical [b, s, h, d] element strides of source and destination
@@ -166,9 +165,9 @@ def all_to_all(xs: list[torch.Tensor], direction: int, group: str) -> list[torch
                                              (strides[0], strides[2], strides[1])))
     s_glob = s * P if direction == SEQ_TO_HEAD_DIR else s
     epoch = pool.next_epoch()
-    kernels.a2a_launch(direction, descs, b, s_glob, d, xs[0].element_size(), P, st.rank,
-                       pool.region_ptrs, pool.flag_ptrs, epoch)
-    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, first_off)
+    chk = kernels.a2a_launch(direction, descs, b, s_glob, d, xs[0].element_size(), P, st.rank,
+                             pool.region_ptrs, pool.flag_ptrs, epoch)
+    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, chk)
     return outs
 
 
@@ -216,10 +215,10 @@ def attention_a2a(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: floa
     off, base = pool.alloc(math.prod(shape) * q.element_size())
     o_tok = base.view(q.dtype).as_strided(shape, strides)
     epoch = pool.next_epoch()
-    kernels.attn_fwd_push(q, k, v, None, lse, scale, causal, P, st.rank, off,
-                          (strides[0], strides[2], strides[1]), pool.region_ptrs,
-                          pool.flag_ptrs, epoch)
-    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, off)
+    chk = kernels.attn_fwd_push(q, k, v, None, lse, scale, causal, P, st.rank, off,
+                                (strides[0], strides[2], strides[1]), pool.region_ptrs,
+                                pool.flag_ptrs, epoch)
+    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, chk)
     return o_tok, lse
 
 
@@ -282,21 +281,20 @@ def ulysses_qkv_attention(qkv: torch.Tensor, pos: torch.Tensor, theta: float, hq
     if H3 != hq + 2 * hkv or hq % P or hkv % P:
         raise ValidationError(f"qkv heads {H3} != {hq}+2*{hkv} or not divisible by {P}")
     srcs = (qkv[:, :, :hq], qkv[:, :, hq:hq + hkv], qkv[:, :, hq + hkv:])
-    outs, descs, first = [], [], None
+    outs, descs = [], []
     for x, rot in zip(srcs, (True, True, False)):
         h = x.shape[2]
         shape = (b, h // P, S, d)
         strides = ((h // P) * S * d, S * d, d, 1)
         off, base = pool.alloc(math.prod(shape) * qkv.element_size())
-        first = off if first is None else first
         outs.append(base.view(qkv.dtype).as_strided(shape, strides))
         descs.append(kernels.a2a_tensor_desc(x, h, off, (strides[0], strides[2], strides[1]),
                                              rope=rot))
     epoch = pool.next_epoch()
-    kernels.a2a_launch(SEQ_TO_HEAD_DIR, descs, b, S, d, qkv.element_size(), P, st.rank,
-                       pool.region_ptrs, pool.flag_ptrs, epoch,
-                       pos=pos.to(torch.float32).contiguous(), theta=theta)
-    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, first)
+    chk = kernels.a2a_launch(SEQ_TO_HEAD_DIR, descs, b, S, d, qkv.element_size(), P, st.rank,
+                             pool.region_ptrs, pool.flag_ptrs, epoch,
+                             pos=pos.to(torch.float32).contiguous(), theta=theta)
+    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, chk)
     qh, kh, vh = outs
     o_tok, lse = attention_a2a(qh, kh, vh, scale, True, group)
     return o_tok, qh, kh, vh, lse
@@ -354,9 +352,9 @@ def qkv_grad_gather(dq: torch.Tensor, dk: torch.Tensor, dv: torch.Tensor, pos: t
         descs.append(kernels.a2a_tensor_desc(x.permute(0, 2, 1, 3), x.shape[1], off + h0 * d * es,
                                              (sl * H3 * d, H3 * d, d)))
     epoch = pool.next_epoch()
-    kernels.a2a_launch(HEAD_TO_SEQ_DIR, descs, b, S, d, es, P, st.rank, pool.region_ptrs,
-                       pool.flag_ptrs, epoch)
-    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, off)
+    chk = kernels.a2a_launch(HEAD_TO_SEQ_DIR, descs, b, S, d, es, P, st.rank, pool.region_ptrs,
+                             pool.flag_ptrs, epoch)
+    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, chk)
     kernels.rope_segments([(dqkv[:, :, :hq], dqkv[:, :, :hq], True),
                            (dqkv[:, :, hq:hq + hkv], dqkv[:, :, hq:hq + hkv], True)],
                           pos, theta, inverse=True)

@@ -36,28 +36,33 @@ class AdamW(torch.optim.Optimizer):
             live = [p for p in group["params"] if p.grad is not None]
             if not live:
                 continue
-            arr = (_Tensor * len(live))()
-            step = None
-            for i, p in enumerate(live):
+            # the bias corrections depend on each parameter's own step count: one launch
+            # per distinct step value (normally exactly one)
+            by_step: dict[int, list] = {}
+            for p in live:
                 st = self.state[p]
                 if not st:
                     st["step"] = 0
                     st["exp_avg"] = torch.zeros_like(p)
                     st["exp_avg_sq"] = torch.zeros_like(p)
                 st["step"] += 1
-                step = st["step"]
                 g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
                 if g.dtype != torch.bfloat16:
                     raise ValueError("optim.AdamW: bf16 gradients only")
                 st["_g"] = g  # keep a made-contiguous gradient alive until the launch
-                arr[i] = _Tensor(p.data_ptr(), g.data_ptr(), st["exp_avg"].data_ptr(),
-                                 st["exp_avg_sq"].data_ptr(), p.numel())
+                by_step.setdefault(st["step"], []).append(p)
             b1, b2 = group["betas"]
-            rc = lib.autosp_adamw_bf16(arr, len(live), group["lr"], b1, b2, group["eps"],
-                                       group["weight_decay"], step, stream)
+            for step, ps in by_step.items():
+                arr = (_Tensor * len(ps))()
+                for i, p in enumerate(ps):
+                    st = self.state[p]
+                    arr[i] = _Tensor(p.data_ptr(), st["_g"].data_ptr(), st["exp_avg"].data_ptr(),
+                                     st["exp_avg_sq"].data_ptr(), p.numel())
+                rc = lib.autosp_adamw_bf16(arr, len(ps), group["lr"], b1, b2, group["eps"],
+                                           group["weight_decay"], step, stream)
+                _lib.check(rc, "adamw_bf16")
+                from .kernels import LOG
+                LOG.end("adamw", None, (len(ps) + 63) // 64)
             for p in live:
                 self.state[p].pop("_g", None)
-            _lib.check(rc, "adamw_bf16")
-            from .kernels import LOG
-            LOG.end("adamw", None, (len(live) + 63) // 64)
         return loss

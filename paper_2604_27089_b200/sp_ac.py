@@ -163,9 +163,19 @@ def is_layer_boundary(n: fx.Node, fw: set | None = None, max_nodes: int = 512) -
     return False
 
 
+def is_random(n: fx.Node) -> bool:
+    """Ops drawing random numbers (dropout, rand*, bernoulli, ...): a recomputation in the
+    backward would draw a DIFFERENT mask than the forward used (torch's own min-cut
+    partitioner bans them from recomputation for the same reason)."""
+    if n.op != "call_function":
+        return False
+    tags = getattr(n.target, "tags", ())
+    return torch.Tag.nondeterministic_seeded in tags
+
+
 def guarded(n: fx.Node, mode: AcMode, fw: set | None = None) -> bool:
     """Forward nodes that must not be recomputed (ac_pass.py:103-114 + the AutoSP guard)."""
-    if is_autosp_collective(n) or is_autosp_attention(n):
+    if is_autosp_collective(n) or is_autosp_attention(n) or is_random(n):
         return True
     if is_layer_boundary(n, fw):
         return True

@@ -268,6 +268,9 @@ class ChunkedLMLoss(torch.autograd.Function):
 
 def lm_loss(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor,
             chunk: int = 4096) -> torch.Tensor:
+    """SUM of the token cross-entropies of ``hidden @ weight.T`` against ``labels``.
+    Labels outside [0, vocab) (e.g. -100 padding) are ignored: they add 0 to the loss and
+    get an all-zero gradient row (torch's ignore_index, with reduction='sum')."""
     h = hidden.reshape(-1, hidden.shape[-1])
     return ChunkedLMLoss.apply(h, weight, labels.reshape(-1), chunk)
 

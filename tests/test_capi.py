@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_abi_version_and_sm100a_cubin(lib):
     from paper_2604_27089_b200 import _lib
-    assert lib.autosp_abi_version() == 1
+    assert lib.autosp_abi_version() == 2
     out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
@@ -88,3 +88,23 @@ def test_ops_fail_loudly_without_library(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "LIB_PATH", tmp_path / "missing.so")
     with pytest.raises(ExtensionMissingError):
         _lib.load()
+
+
+def test_check_word_covers_every_tensor_of_a_call(lib):
+    """the symmetric-offset check word folds in EVERY destination descriptor of
+    a call (offset, strides, heads), not only tensor 0's offset."""
+    from paper_2604_27089_b200 import _lib
+
+    def word(offs, heads=(8, 8, 8)):
+        arr = (_lib.A2ATensor * 3)(*[_lib.A2ATensor(16, 0, 0, 0, o, 1, 2, 3, h, 0)
+                                     for o, h in zip(offs, heads)])
+        return lib.autosp_a2a_check(0, arr, 3)
+
+    base = word((0, 4096, 8192))
+    assert base == word((0, 4096, 8192))
+    assert base != word((0, 4096, 9216))   # a later tensor's offset diverged
+    assert base != word((0, 5120, 8192))
+    assert base != word((0, 4096, 8192), heads=(8, 8, 16))
+    spec = _lib.PushSpec(2, 0, 1024, 1, 2, 3, None, None, 1)
+    assert lib.autosp_push_check(ctypes.byref(spec), 4) != lib.autosp_push_check(
+        ctypes.byref(_lib.PushSpec(2, 0, 2048, 1, 2, 3, None, None, 1)), 4)

@@ -94,6 +94,37 @@ def test_cross_entropy_fwd_bwd(n, V):
     assert _rel(dl, lf.grad) < TOL
 
 
+def test_cross_entropy_ignores_out_of_range_labels():
+    """labels outside [0, vocab) (-100 padding, >= vocab) contribute 0 to the
+    loss and get an all-zero gradient row (torch ignore_index with reduction='sum')."""
+    from paper_2604_27089_b200 import kernels
+    from paper_2604_27089_b200.workloads import lm_loss
+    n, V = 9, 1000
+    g = torch.Generator(device="cuda").manual_seed(1)
+    logits = (torch.randn(n, V, device="cuda", generator=g) * 3).bfloat16()
+    labels = torch.randint(0, V, (n,), device="cuda", generator=g)
+    labels[0], labels[4], labels[8] = -100, V, -1
+    lse, loss = kernels.ce_fwd(logits, labels)
+    ref = F.cross_entropy(logits.float(), labels.masked_fill((labels < 0) | (labels >= V), -100),
+                          reduction="none", ignore_index=-100)
+    assert float((loss - ref).abs().max()) < 1e-3 * max(1.0, float(ref.abs().max()))
+    assert float(loss[0]) == 0.0 and float(loss[4]) == 0.0 and float(loss[8]) == 0.0
+    dl = kernels.ce_bwd_(logits.clone(), labels, lse, 1.0)
+    assert not dl[[0, 4, 8]].float().abs().any()
+    # through the chunked LM loss (chunk boundary inside the batch)
+    h = torch.randn(n, 64, device="cuda", generator=g).bfloat16().requires_grad_(True)
+    w = (torch.randn(V, 64, device="cuda", generator=g) * 0.1).bfloat16().requires_grad_(True)
+    tot = lm_loss(h, w, labels, chunk=4)
+    hf, wf = h.detach().float().requires_grad_(True), w.detach().float().requires_grad_(True)
+    lab = labels.masked_fill((labels < 0) | (labels >= V), -100)
+    rf = F.cross_entropy(hf @ wf.t(), lab, reduction="sum", ignore_index=-100)
+    tot.backward()
+    rf.backward()
+    assert abs(float(tot) - float(rf)) < 1e-2 * abs(float(rf))
+    assert not h.grad[[0, 4, 8]].float().abs().any()
+    assert _rel(h.grad, hf.grad) < TOL and _rel(w.grad, wf.grad) < TOL
+
+
 def test_fused_llama_block_matches_unfused():
     """Same weights, fused (autosp rope/swiglu/F.rms_norm) vs plain torch block, fwd+bwd."""
     from paper_2604_27089_b200 import ops

@@ -89,10 +89,10 @@ def test_a2a_strided_qkv_source_folds_transpose():
             kernels.a2a_tensor_desc(v[:, :, hq + hkv:], hkv, (qn + kn) * 2,
                                     ((hkv // P) * s * d, d, s * d)),
         ]
-        kernels.a2a_launch(_lib.SEQ_TO_HEAD, descs, b, s, d, 2, P, r,
-                           [x.data_ptr() for x in regions], fptr, 5)
+        chk = kernels.a2a_launch(_lib.SEQ_TO_HEAD, descs, b, s, d, 2, P, r,
+                                 [x.data_ptr() for x in regions], fptr, 5)
     for r in range(P):
-        kernels.a2a_wait(fptr[r], P, r, 5)
+        kernels.a2a_wait(fptr[r], P, r, 5, chk)
     full = torch.cat([v.float().cpu() for v in views], dim=1)  # [b, s, hq+2hkv, d]
     for r in range(P):
         reg = regions[r].float().cpu()

@@ -49,3 +49,43 @@ def test_layer_boundary_detection_is_per_layer():
     per_layer_2 = p2["saved_bytes"] / 2
     per_layer_8 = p8["saved_bytes"] / 8
     assert per_layer_8 < 1.5 * per_layer_2
+
+
+@pytest.mark.parametrize("mode", ["seq-aware", "seq-aware-all", "conservative"])
+def test_random_ops_are_never_recomputed(mode):
+    """a recomputed dropout would draw a different mask in the backward than the
+    forward used.  Random ops (Tag.nondeterministic_seeded) are guarded, so the backward
+    graph contains none and the gradients equal eager autograd's under the same seed."""
+    from functorch.compile import aot_function, make_boxed_func
+
+    from paper_2604_27089_b200.sp_ac import AcMode, make_partition_fn
+    bw_graphs = []
+
+    def fw_c(gm, _):
+        return make_boxed_func(gm.forward)
+
+    def bw_c(gm, _):
+        bw_graphs.append(gm)
+        return make_boxed_func(gm.forward)
+
+    def f(x, w1, w2):
+        h = torch.nn.functional.dropout(x @ w1, p=0.5, training=True)
+        return (torch.nn.functional.silu(h) @ w2).pow(2).sum()
+
+    g = torch.Generator().manual_seed(0)
+    x, w1, w2 = (torch.randn(*s, generator=g, dtype=torch.float64) for s in
+                 ((64, 32), (32, 48), (48, 16)))
+    cf = aot_function(f, fw_compiler=fw_c, bw_compiler=bw_c,
+                      partition_fn=make_partition_fn(AcMode(mode)))
+    leaves = [t.clone().requires_grad_(True) for t in (x, w1, w2)]
+    torch.manual_seed(123)
+    cf(*leaves).backward()
+    ref = [t.clone().requires_grad_(True) for t in (x, w1, w2)]
+    torch.manual_seed(123)
+    f(*ref).backward()
+    ops = {str(n.target) for n in bw_graphs[0].graph.nodes if n.op == "call_function"}
+    rand = [o for o in ops if ("dropout" in o or "rand" in o or "bernoulli" in o)
+            and "backward" not in o]
+    assert not rand, ops
+    for a, b in zip(leaves, ref):
+        torch.testing.assert_close(a.grad, b.grad, rtol=1e-12, atol=1e-12)

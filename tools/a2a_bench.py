@@ -44,7 +44,7 @@ def call_rank(r, e):
                                      ((hkv // P) * S * d, d, S * d)),
              kernels.a2a_tensor_desc(v[:, :, hq + hkv:], hkv, (qn + kn) * 2,
                                      ((hkv // P) * S * d, d, S * d))]
-    kernels.a2a_launch(_lib.SEQ_TO_HEAD, descs, 1, S, d, 2, P, r, rptr, fptr, e)
+    return kernels.a2a_launch(_lib.SEQ_TO_HEAD, descs, 1, S, d, 2, P, r, rptr, fptr, e)
 
 
 def one_round():
@@ -52,9 +52,9 @@ def one_round():
     e = epoch[0]
     kernels.a2a_mark_ready(fptr, e)  # loopback: all virtual ranks reached epoch e
     for r in range(P):
-        call_rank(r, e)
+        chk = call_rank(r, e)
     for r in range(P):
-        kernels.a2a_wait(fptr[r], P, r, e, 0)
+        kernels.a2a_wait(fptr[r], P, r, e, chk)
 
 
 for _ in range(3):
