@@ -218,14 +218,17 @@ def main():
     rank = tdist.get_rank() if world > 1 else 0
     passes = ["auto_sp"] if args.no_sp_ac else ["auto_sp", "sp_ac"]
     autosp.reg_passes(passes, ac_mode=args.ac_mode)
-    st = autosp.dist.init(world)
-    dev = st.device if st.device.type == "cuda" else torch.device("cuda", 0)
-    torch.cuda.set_device(dev)
     cfg = CONFIGS[args.model]
     if args.layers:
         cfg = LlamaConfig(cfg.name + f"-L{args.layers}", cfg.d_model, args.layers, cfg.hq,
                           cfg.hkv, cfg.d_ffn, cfg.vocab)
     P, b, S = world, args.batch, args.seq
+    # the symmetric receive heap sized up front from the planner (it would grow on demand)
+    from paper_2604_27089_b200.planner import pool_bytes
+    st = autosp.dist.init(world, pool_bytes=(int(pool_bytes(cfg, S, P) * b * 1.05) + (64 << 20))
+                          if P > 1 else None)
+    dev = st.device if st.device.type == "cuda" else torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
     if S % P:
         raise SystemExit("seq not divisible by world")
     sl = S // P

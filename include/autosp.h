@@ -131,6 +131,10 @@ AUTOSP_API int autosp_a2a_wait(uint32_t* local_flags, int world, int rank, uint3
                                uint32_t check, void* stream);
 AUTOSP_API uint32_t autosp_a2a_check(int direction, const autosp_a2a_tensor* tensors,
                                      int n_tensors);
+/* Every flag spin of the reshard protocol (waiting for a peer to reach an epoch or to
+ * finish writing) traps after this many seconds instead of hanging the GPU; default 300.
+ * Host-side setting, applies to launches issued after the call.                       */
+AUTOSP_API int autosp_set_spin_timeout(double seconds);
 /* Single-process loopback used by tests / benchmarks on one GPU: marks `epoch` as reached
  * for all `world` virtual ranks whose flag blocks are given.                           */
 AUTOSP_API int autosp_a2a_mark_ready(uint32_t* const* flags, int world, uint32_t epoch, void* stream);

@@ -76,6 +76,7 @@ EXPORTS = {
     "autosp_push_check": (C.c_uint32, [C.c_void_p, C.c_int]),
     "autosp_a2a_wait": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_uint32, C.c_uint32,
                                   C.c_void_p]),
+    "autosp_set_spin_timeout": (C.c_int, [C.c_double]),
     "autosp_a2a_mark_ready": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_uint32,
                                         C.c_void_p]),
     "autosp_attn_fwd": (C.c_int, [AttnTensor] * 4 + [C.c_void_p] + [C.c_int] * 5 +

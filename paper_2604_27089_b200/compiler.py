@@ -18,7 +18,7 @@ import torch
 from . import dist as sp_dist
 from .auto_sp import auto_sp
 from .errors import ValidationError
-from .sp_ac import AcMode, make_partition_fn
+from .sp_ac import AcMode, is_autosp_collective, make_partition_fn
 
 KNOWN_PASSES = ("auto_sp", "sp_ac")
 _PASSES: list[str] = []
@@ -54,7 +54,24 @@ def backend(passes: list[str] | None = None, ac_mode: AcMode | None = None):
     def _compiler(gm, example_inputs):
         if _COMPILER_OVERRIDE is not None:
             return _COMPILER_OVERRIDE(gm, example_inputs)
-        return make_boxed_func(gm.forward)
+        fn = make_boxed_func(gm.forward)
+        st = sp_dist.state()
+        if st.world > 1 and st.group is not None and \
+                any(is_autosp_collective(n) for n in gm.graph.nodes):
+            # every rank compiles the same graphs in the same order but not at the same
+            # speed: a host barrier before a graph's FIRST run keeps one rank's first
+            # reshard from spinning on a peer that is still compiling
+            first = [True]
+
+            def fn_sync(args):
+                if first[0]:
+                    first[0] = False
+                    sp_dist.barrier(st)
+                return fn(args)
+
+            fn_sync._boxed_call = True
+            return fn_sync
+        return fn
 
     def _backend(gm: torch.fx.GraphModule, example_inputs):
         st = sp_dist.state()

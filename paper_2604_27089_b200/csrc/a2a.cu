@@ -55,15 +55,20 @@ struct A2AParams {
   int64_t total_items;
   const float* pos;  // RoPE positions of the SOURCE tokens (seq_to_head: the local shard)
   float log2_theta;
+  uint64_t timeout_ns;  // flag spins trap after this long (autosp_set_spin_timeout)
 };
 
 AUTOSP_DEV bool epoch_reached(uint32_t v, uint32_t e) { return (int32_t)(v - e) >= 0; }
 
-AUTOSP_DEV void spin_until_epoch(const uint32_t* p, uint32_t e) {
+AUTOSP_DEV void spin_until_epoch(const uint32_t* p, uint32_t e, uint64_t timeout_ns) {
   if (epoch_reached(ld_acquire_sys(p), e)) return;
   uint64_t t0 = globaltimer();
   while (!epoch_reached(ld_acquire_sys(p), e)) {
-    if (globaltimer() - t0 > 10000000000ull) asm volatile("trap;");
+    if (globaltimer() - t0 > timeout_ns) {
+      printf("autosp: peer flag wait timed out after %llu ns (epoch %u, flag %u)\n",
+             (unsigned long long)timeout_ns, e, ld_acquire_sys(p));
+      asm volatile("trap;");
+    }
     __nanosleep(64);
   }
 }
@@ -263,25 +268,27 @@ __global__ void __launch_bounds__(kA2AThreads) a2a_push_kernel(const __grid_cons
 __global__ void a2a_handshake_kernel(const __grid_constant__ A2AParams p) {
   const int tid = threadIdx.x;
   if (tid == 0) st_release_sys(p.peer_flags[p.rank] + kReadyWord, p.epoch);
-  if (tid < p.P && tid != p.rank) spin_until_epoch(p.peer_flags[tid] + kReadyWord, p.epoch);
+  if (tid < p.P && tid != p.rank)
+    spin_until_epoch(p.peer_flags[tid] + kReadyWord, p.epoch, p.timeout_ns);
 }
 
 struct ShakeParams {
   uint32_t* flags[AUTOSP_MAX_WORLD];
   int P, rank;
   uint32_t epoch;
+  uint64_t timeout_ns;
 };
 __global__ void handshake_kernel(const __grid_constant__ ShakeParams s) {
   const int tid = threadIdx.x;
   if (tid == 0) st_release_sys(s.flags[s.rank] + kReadyWord, s.epoch);
-  if (tid < s.P && tid != s.rank) spin_until_epoch(s.flags[tid] + kReadyWord, s.epoch);
+  if (tid < s.P && tid != s.rank) spin_until_epoch(s.flags[tid] + kReadyWord, s.epoch, s.timeout_ns);
 }
 
 __global__ void a2a_wait_kernel(uint32_t* flags, int P, int rank, uint32_t epoch,
-                                uint32_t check) {
+                                uint32_t check, uint64_t timeout_ns) {
   const int j = threadIdx.x;
   if (j < P && j != rank) {
-    spin_until_epoch(flags + kArriveWord + j, epoch);
+    spin_until_epoch(flags + kArriveWord + j, epoch, timeout_ns);
     // every sender must have written where this rank expects the data (symmetric
     // allocation invariant); a divergence is a bug -> fail loudly, never corrupt silently
     if (*(volatile uint32_t*)(flags + kCheckWord + j) != check) asm volatile("trap;");
@@ -303,6 +310,18 @@ __global__ void a2a_mark_ready_kernel(const __grid_constant__ MarkParams m) {
 
 // ---------------------------------------------------------------------------- C ABI
 extern "C" void autosp_set_error(const char* fmt, ...);
+
+// bound of every flag spin (peer ready / arrival); host-side, copied into each launch
+static uint64_t g_spin_timeout_ns = 300ull * 1000000000ull;
+
+extern "C" int autosp_set_spin_timeout(double seconds) {
+  if (!(seconds > 0.0) || seconds > 1e7) {
+    autosp_set_error("spin timeout %g s out of range", seconds);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  g_spin_timeout_ns = (uint64_t)(seconds * 1e9);
+  return AUTOSP_OK;
+}
 
 static int a2a_impl(int direction, const autosp_a2a_tensor* tensors, int n_tensors, int b,
                     int s_global, int d, int elem_bytes, int world, int rank,
@@ -377,6 +396,7 @@ static int a2a_impl(int direction, const autosp_a2a_tensor* tensors, int n_tenso
   p.P = world;
   p.rank = rank;
   p.epoch = epoch;
+  p.timeout_ns = g_spin_timeout_ns;
   p.check = autosp_a2a_check(direction, tensors, n_tensors);
   for (int j = 0; j < world; ++j) {
     p.peer_base[j] = static_cast<char*>(peer_base[j]);
@@ -497,7 +517,7 @@ extern "C" int autosp_a2a_wait(uint32_t* local_flags, int world, int rank, uint3
   }
   if (world == 1) return AUTOSP_OK;
   autosp::a2a_wait_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
-      local_flags, world, rank, epoch, check);
+      local_flags, world, rank, epoch, check, g_spin_timeout_ns);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     autosp_set_error("a2a_wait launch failed: %s", cudaGetErrorString(e));
@@ -533,6 +553,7 @@ int autosp_internal_handshake(uint32_t* const* flags, int world, int rank, uint3
   s.P = world;
   s.rank = rank;
   s.epoch = epoch;
+  s.timeout_ns = g_spin_timeout_ns;
   autosp::handshake_kernel<<<1, 32, 0, stream>>>(s);
   return cudaGetLastError() == cudaSuccess ? AUTOSP_OK : AUTOSP_ERR_CUDA;
 }

@@ -11,7 +11,8 @@ namespace autosp {
 constexpr int kReadyWord = 0;     // "this rank reached epoch e" (its older readers are done)
 constexpr int kArriveWord = 16;   // + src rank: src finished writing call e into me
 constexpr int kCheckWord = 32;    // + src rank: sender's view of the destination offset
-constexpr int kCounterWord = 48;  // CTA completion counter (local use only)
+constexpr int kCounterWord = 48;  // 8 CTA completion counters (local use only), one per
+constexpr int kCounterSlots = 8;  // epoch mod 8: consecutive calls never share a counter
 
 // Completion of a launch that pushed into peers: every thread's (remote) stores are
 // ordered before thread 0's system-scope fence by the CTA barrier (fences are
@@ -22,7 +23,7 @@ AUTOSP_DEV void publish_arrival(uint32_t* const* peer_flags, int P, int rank, ui
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    uint32_t* ctr = peer_flags[rank] + kCounterWord;
+    uint32_t* ctr = peer_flags[rank] + kCounterWord + (epoch % kCounterSlots);
     const uint32_t old = atom_add_acqrel_gpu(ctr, 1u);
     if (old == n_ctas - 1) {
       *ctr = 0u;

@@ -2,20 +2,21 @@
 reference equivalent ``DeviceGroup(P)``, ``executor.py:233-275``).
 
 One process per GPU.  The world is split into data-parallel replicas of
-``sp_group_size`` consecutive ranks.  Inside an SP group every rank owns one
-*symmetric* allocation (identical size on all ranks) holding
+``sp_group_size`` consecutive ranks.  Inside an SP group every rank owns a *symmetric*
+heap: segments of identical size on all ranks, the first one holding
 
-    [ flag block (256 B) | receive region ]
+    [ flag block (256 B used of 4 KB) | receive region ]
 
-mapped once into every peer through CUDA IPC, so the all-to-all kernels write straight
+each mapped into every peer through CUDA IPC, so the all-to-all kernels write straight
 into peers' HBM over NVLink 5 / NVSwitch (no NCCL on the reshard path).  NCCL (or gloo
-on CPU test runs) carries only the host-side rendezvous and the per-step gradient
-reduction.
+on CPU test runs) carries only the host-side rendezvous (the IPC handles of a new
+segment) and the per-step gradient reduction.
 
-Receive-region allocation is deterministic on every rank: a first-fit allocator whose
-slots are released when the storage of the tensor handed out is no longer referenced
-(C++ refcount, identical on all ranks running the same program).  The kernels verify
-at run time that sender and receiver agree on every offset (a mismatch traps)."""
+Receive-heap allocation is deterministic on every rank: first-fit over the segments,
+slots released when the storage of the tensor handed out is no longer referenced (C++
+refcount, identical on all ranks running the same program), and the heap grows
+collectively when nothing fits.  Every call's destination descriptors are folded into a
+check word the receiver compares with each sender's (a mismatch traps)."""
 
 from __future__ import annotations
 
@@ -31,18 +32,24 @@ from . import _lib
 from .errors import ValidationError
 
 FLAG_BYTES = 4096  # flag block (256 B used) padded to keep the receive region aligned
-POOL_FRACTION = 0.12  # of device memory reserved per rank for a2a receive slots
+POOL_INITIAL_BYTES = 2 << 30  # first segment of the symmetric receive heap
+POOL_GROW_BYTES = 2 << 30     # minimum size of each further segment (the heap grows on demand)
+SPIN_TIMEOUT_S = 300.0  # default bound of a flag spin (AUTOSP_SPIN_TIMEOUT_S overrides)
 
 
 def default_pool_bytes(device) -> int:
-    """The a2a outputs that sp_ac keeps (q/k/v head shards + o seq shard per layer) live in
-    the pool until their backward, so size it with the device (override:
-    AUTOSP_POOL_BYTES or dist.init(pool_bytes=...))."""
+    """Initial size of the symmetric heap's first segment (it grows on demand; override:
+    AUTOSP_POOL_BYTES or dist.init(pool_bytes=...), e.g. planner.pool_bytes(cfg, S, P) to
+    get the whole steady-state heap in one segment)."""
     env = os.environ.get("AUTOSP_POOL_BYTES")
     if env:
         return int(env)
-    total = torch.cuda.get_device_properties(device).total_memory
-    return int(total * POOL_FRACTION) // (1 << 20) * (1 << 20)
+    return POOL_INITIAL_BYTES
+
+
+def default_grow_bytes() -> int:
+    env = os.environ.get("AUTOSP_POOL_GROW_BYTES")
+    return int(env) if env else POOL_GROW_BYTES
 
 
 _PyCapsule_New = C.pythonapi.PyCapsule_New
@@ -71,83 +78,176 @@ class _Slot:
     base: torch.Tensor  # uint8 view owned by the pool; busy while its storage is shared
 
 
+@dataclass
+class Slab:
+    """One allocation of the symmetric heap: `view` (uint8, this rank's memory) sits at
+    byte `offset` of segment `segment`, whose receive region rank j maps at regions[j]
+    -- the same offset on every rank, so a sender addresses rank j's copy as
+    regions[j] + offset."""
+    segment: int
+    offset: int
+    view: torch.Tensor
+    regions: list[int]
+
+    pieces: list[tuple[int, torch.Tensor]] = field(default_factory=list)
+
+
+def _align(n: int) -> int:
+    return (n + SymmetricPool.ALIGN - 1) // SymmetricPool.ALIGN * SymmetricPool.ALIGN
+
+
+class _Segment:
+    def __init__(self, capacity: int, regions: list[int]):
+        self.capacity = capacity
+        self.regions = regions
+        self.slots: list[_Slot] = []
+        self.high_water = 0
+
+
 class SymmetricPool:
-    """Receive region + flag block of one rank, with the peers' mappings."""
+    """Symmetric receive heap of one rank: a list of SEGMENTS, each one cudaMalloc per rank
+    mapped into every peer through CUDA IPC; segment 0 also holds the flag block.
+
+    Allocation is first-fit over the segments in order, slots are released when the
+    storage of the tensor handed out is no longer referenced (C++ refcount), so ranks
+    running the same program get identical (segment, offset) pairs.  When no segment has
+    room, the heap GROWS collectively: every rank reaches the same failing allocation at
+    the same point of the program, allocates a new segment of max(need, grow_bytes), and
+    the SP group exchanges the IPC handles (all_gather_object) -- so the receive heap is
+    sized by what sp_ac actually keeps (the q/k/v head shards and token-major O of every
+    layer until its backward), not by a fixed fraction of the device."""
 
     ALIGN = 1024
 
     def __init__(self, nbytes: int, world: int, rank: int, device, group=None,
-                 peers: list[tuple[int, int]] | None = None, reuse: bool = True):
-        lib = _lib.load()
-        self.world, self.rank, self.device = world, rank, device
+                 peers: list[tuple[int, int]] | None = None, reuse: bool = True,
+                 grow_bytes: int | None = None):
+        self.world, self.rank, self.device, self.group = world, rank, device, group
         # reuse=False: bump allocation, no slot reuse -- for virtual ranks sharing ONE
         # process (threads share the autograd engine, so slot lifetimes, and with them
         # first-fit offsets, can differ between ranks; separate processes are symmetric)
         self.reuse = reuse
-        self.capacity = nbytes
+        self.grow_bytes = grow_bytes if grow_bytes is not None else default_grow_bytes()
         self._owned: list[int] = []
         self._opened: list[int] = []
+        self.segments: list[_Segment] = []
         if peers is None:
-            ptr = C.c_void_p()
-            handle = (C.c_char * _lib.IPC_HANDLE_BYTES)()
-            _lib.check(lib.autosp_symm_alloc(FLAG_BYTES + nbytes, C.byref(ptr), handle),
-                       "symm_alloc")
-            self._owned.append(ptr.value)
-            handles = [None] * world
-            if world > 1:
-                tdist.all_gather_object(handles, bytes(handle), group=group)
-            bases = []
-            for j in range(world):
-                if j == rank:
-                    bases.append(ptr.value)
-                else:
-                    pp = C.c_void_p()
-                    _lib.check(lib.autosp_symm_open(handles[j], C.byref(pp)), "symm_open")
-                    self._opened.append(pp.value)
-                    bases.append(pp.value)
+            bases = self._map_segment(FLAG_BYTES + nbytes)
+            if bases is None:
+                raise torch.OutOfMemoryError(f"symmetric heap: cannot allocate {nbytes} bytes")
             self.flag_ptrs = bases
-            self.region_ptrs = [b + FLAG_BYTES for b in bases]
+            self.segments.append(_Segment(nbytes, [b + FLAG_BYTES for b in bases]))
+            self.growable = True
         else:  # explicit (flag_ptr, region_ptr) per rank: single-process loopback
             self.flag_ptrs = [f for f, _ in peers]
-            self.region_ptrs = [r for _, r in peers]
-        self.slots: list[_Slot] = []
+            self.segments.append(_Segment(nbytes, [r for _, r in peers]))
+            self.growable = False
         self.epoch = 0
-        self.high_water = 0
+
+    # ------------------------------------------------------------------ segments
+    def _map_segment(self, nbytes: int) -> list[int] | None:
+        """Collective: allocate `nbytes` on every rank and map all peers' allocations.
+        Returns the per-rank base pointers, or None on every rank if ANY rank failed."""
+        lib = _lib.load()
+        ptr = C.c_void_p()
+        handle = (C.c_char * _lib.IPC_HANDLE_BYTES)()
+        rc = lib.autosp_symm_alloc(nbytes, C.byref(ptr), handle)
+        if rc != 0 and self.device.type == "cuda":
+            torch.cuda.empty_cache()  # cached-but-free blocks of the caching allocator
+            rc = lib.autosp_symm_alloc(nbytes, C.byref(ptr), handle)
+        mine = (rc == 0, bytes(handle))
+        allh = [None] * self.world
+        if self.world > 1 and tdist.is_initialized():
+            tdist.all_gather_object(allh, mine, group=self.group)
+        else:
+            allh = [mine] * self.world
+        if not all(ok for ok, _ in allh):
+            if rc == 0:
+                lib.autosp_symm_free(ptr.value)
+            return None
+        self._owned.append(ptr.value)
+        bases = []
+        for j in range(self.world):
+            if j == self.rank:
+                bases.append(ptr.value)
+            else:
+                pp = C.c_void_p()
+                _lib.check(lib.autosp_symm_open(allh[j][1], C.byref(pp)), "symm_open")
+                self._opened.append(pp.value)
+                bases.append(pp.value)
+        return bases
+
+    @property
+    def region_ptrs(self) -> list[int]:
+        """Segment 0's receive regions (rank j's, as mapped here)."""
+        return self.segments[0].regions
+
+    @property
+    def capacity(self) -> int:
+        return sum(sg.capacity for sg in self.segments)
+
+    @property
+    def high_water(self) -> int:
+        return sum(sg.high_water for sg in self.segments)
 
     # ------------------------------------------------------------------ allocation
     @staticmethod
     def _busy(slot: _Slot) -> bool:
         return torch._C._storage_Use_Count(slot.base.untyped_storage()._cdata) > 2
 
-    def alloc(self, nbytes: int) -> tuple[int, torch.Tensor]:
-        """First-fit slot of the receive region; returns (offset, uint8 view)."""
+    def _fit(self, sg: _Segment, need: int) -> int | None:
         if not self.reuse:
-            need = (nbytes + self.ALIGN - 1) // self.ALIGN * self.ALIGN
-            off = self.high_water
-            if off + need > self.capacity:
-                raise ValidationError("loopback receive region exhausted (bump allocation)")
-            self.high_water = off + need
-            base = _raw_tensor(self.region_ptrs[self.rank] + off, nbytes, self.device)
-            return off, base.view(-1)
-        self.slots = [s for s in self.slots if self._busy(s)]
-        self.slots.sort(key=lambda s: s.offset)
-        need = (nbytes + self.ALIGN - 1) // self.ALIGN * self.ALIGN
+            return sg.high_water if sg.high_water + need <= sg.capacity else None
+        sg.slots = [x for x in sg.slots if self._busy(x)]
+        sg.slots.sort(key=lambda x: x.offset)
         off = 0
-        for s in self.slots:
-            if s.offset - off >= need:
+        for x in sg.slots:
+            if x.offset - off >= need:
                 break
-            off = max(off, s.offset + (s.nbytes + self.ALIGN - 1) // self.ALIGN * self.ALIGN)
-        if off + need > self.capacity:
+            off = max(off, x.offset + _align(x.nbytes))
+        return off if off + need <= sg.capacity else None
+
+    def alloc(self, nbytes: int) -> Slab:
+        """First-fit slab of `nbytes` (growing the heap collectively if nothing fits)."""
+        need = _align(max(nbytes, 1))
+        for i, sg in enumerate(self.segments):
+            off = self._fit(sg, need)
+            if off is not None:
+                return self._take(i, off, nbytes, need)
+        if not (self.growable and self.reuse):
             raise ValidationError(
-                f"symmetric receive region exhausted ({off + need} > {self.capacity} bytes); "
-                "raise AUTOSP_POOL_BYTES / dist.init(pool_bytes=...)")
+                f"symmetric receive region exhausted ({need} bytes requested, "
+                f"{self.capacity} total); loopback pools do not grow")
+        cap = max(need, self.grow_bytes)
+        bases = self._map_segment(cap)
+        if bases is None:
+            raise torch.OutOfMemoryError(
+                f"symmetric heap: growing by {cap} bytes failed on some rank of the SP group "
+                f"(heap {self.capacity} bytes in {len(self.segments)} segments)")
+        self.segments.append(_Segment(cap, bases))
+        return self._take(len(self.segments) - 1, 0, nbytes, need)
+
+    def _take(self, i: int, off: int, nbytes: int, need: int) -> Slab:
+        sg = self.segments[i]
         # a separate storage per slot so its C++ refcount tracks exactly this slot
-        base = _raw_tensor(self.region_ptrs[self.rank] + off, nbytes, self.device)
-        self.slots.append(_Slot(off, nbytes, base))
-        self.high_water = max(self.high_water, off + need)
+        base = _raw_tensor(sg.regions[self.rank] + off, nbytes, self.device)
+        if self.reuse:
+            sg.slots.append(_Slot(off, nbytes, base))
+        sg.high_water = max(sg.high_water, off + need)
         # hand out a VIEW: the caller's reference then holds the slot's storage (the
         # pool's own `base` alone does not count as busy)
-        return off, base.view(-1)
+        return Slab(i, off, base.view(-1), sg.regions)
+
+    def alloc_many(self, sizes: list[int]) -> Slab:
+        """One slab holding consecutive ALIGN-aligned pieces of the given sizes (the
+        destinations of one call; slab.pieces = [(offset, uint8 view)]).  The slot is
+        released when the last piece dies."""
+        slab = self.alloc(sum(_align(n) for n in sizes))
+        cur = 0
+        for n in sizes:
+            slab.pieces.append((slab.offset + cur, slab.view[cur:cur + n]))
+            cur += _align(n)
+        return slab
 
     def next_epoch(self) -> int:
         self.epoch += 1
@@ -214,11 +314,23 @@ def init(sp_group_size: int, pool_bytes: int | None = None, backend: str | None 
             if rank in ranks:
                 st.dp_group = pg
     if sp_group_size > 1 and device.type == "cuda":
+        # bound of the reshard protocol's flag spins (a peer that never arrives traps the
+        # kernel instead of hanging the GPU); compile skew is absorbed by the host barrier
+        # before each compiled graph's first run (compiler.py), not by this timeout
+        _lib.check(_lib.load().autosp_set_spin_timeout(
+            float(os.environ.get("AUTOSP_SPIN_TIMEOUT_S", SPIN_TIMEOUT_S))), "set_spin_timeout")
         st.pool = SymmetricPool(pool_bytes or default_pool_bytes(device), sp_group_size, st.rank,
                                 device, group=st.group)
     _STATE = st
     _REGISTRY[st.name] = st
     return st
+
+
+def barrier(st: SPState | None = None) -> None:
+    """Host barrier over the SP group (no-op without a process group)."""
+    st = st or state()
+    if st.group is not None and st.world > 1 and tdist.is_initialized():
+        tdist.barrier(group=st.group)
 
 
 def state() -> SPState:

@@ -35,6 +35,20 @@ ATTN_DTYPE: torch.dtype | None = torch.bfloat16
 
 
 # ----------------------------------------------------------------------------- attention
+def _kernel_head_dim(d: int) -> int:
+    """Head dims the sm_100a kernels implement are 32/64/128; smaller ones (the reference
+    model's tiny configs use d = 4 / 8) run zero-padded to the next one: zero columns add
+    nothing to q.k or p.v, so the result is unchanged (the scale stays 1/sqrt(d))."""
+    for dp in kernels.SUPPORTED_HEAD_DIMS:
+        if d <= dp:
+            return dp
+    raise ValidationError(f"head_dim {d} > {kernels.SUPPORTED_HEAD_DIMS[-1]} is not supported")
+
+
+def _pad_d(t: torch.Tensor, dp: int) -> torch.Tensor:
+    return torch.nn.functional.pad(t, (0, dp - t.shape[-1]))
+
+
 @torch.library.custom_op("autosp::attention", mutates_args=(), device_types="cuda")
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: float,
               causal: bool) -> tuple[torch.Tensor, torch.Tensor]:
@@ -43,6 +57,12 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: float,
     # free view instead of a copy of the whole output
     b, h, s, d = q.shape
     o = torch.empty((b, s, h, d), dtype=q.dtype, device=q.device).transpose(1, 2)
+    dp = _kernel_head_dim(d)
+    if dp != d:
+        op, lse = kernels.attn_fwd(_pad_d(q, dp), _pad_d(k, dp), _pad_d(v, dp), causal=causal,
+                                   scale=scale)
+        o.copy_(op[..., :d])
+        return o, lse
     return kernels.attn_fwd(q, k, v, causal=causal, scale=scale, out=o)
 
 
@@ -59,6 +79,12 @@ def attention_backward(do: torch.Tensor, q: torch.Tensor, k: torch.Tensor, v: to
                        causal: bool) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
     if do.stride(-1) != 1:
         do = do.contiguous()
+    d = q.shape[-1]
+    dp = _kernel_head_dim(d)
+    if dp != d:
+        gs = kernels.attn_bwd(*(_pad_d(t, dp) for t in (q, k, v, o, do)), lse, causal=causal,
+                              scale=scale)
+        return tuple(g[..., :d].contiguous() for g in gs)
     return kernels.attn_bwd(q, k, v, o, do, lse, causal=causal, scale=scale)
 
 
@@ -74,6 +100,12 @@ def attention_backward_delta(do: torch.Tensor, q: torch.Tensor, k: torch.Tensor,
     """attention_backward with delta = rowsum(dO * O) supplied (no O needed)."""
     if do.stride(-1) != 1:
         do = do.contiguous()
+    d = q.shape[-1]
+    dp = _kernel_head_dim(d)
+    if dp != d:
+        gs = kernels.attn_bwd(*(_pad_d(t, dp) for t in (q, k, v)), None, _pad_d(do, dp), lse,
+                              causal=causal, scale=scale, delta=delta.float().contiguous())
+        return tuple(g[..., :d].contiguous() for g in gs)
     return kernels.attn_bwd(q, k, v, None, do, lse, causal=causal, scale=scale,
                             delta=delta.float().contiguous())
 
@@ -151,14 +183,12 @@ def all_to_all(xs: list[torch.Tensor], direction: int, group: str) -> list[torch
     pool = st.pool
     descs, outs = [], []
     b, _, s, d = xs[0].shape
-    for x in xs:
-        if x.stride(-1) != 1:
-            x = x.contiguous()
-        shape, strides = _out_geometry(x, direction, P)
-        nbytes = math.prod(shape) * x.element_size()
-        off, base = pool.alloc(nbytes)
-        out = base.view(x.dtype).as_strided(shape, strides)
-        outs.append(out)
+    xs = [x if x.stride(-1) == 1 else x.contiguous() for x in xs]
+    geo = [_out_geometry(x, direction, P) for x in xs]
+    # ONE slab per call (all destinations in the same segment, one peer-base array)
+    slab = pool.alloc_many([math.prod(sh) * x.element_size() for x, (sh, _) in zip(xs, geo)])
+    for x, (shape, strides), (off, base) in zip(xs, geo, slab.pieces):
+        outs.append(base.view(x.dtype).as_strided(shape, strides))
         # kernel convention: logical [b, s, h, d] element strides of source and destination
         src_bshd = x.permute(0, 2, 1, 3)
         descs.append(kernels.a2a_tensor_desc(src_bshd, x.shape[1], off,
@@ -166,7 +196,7 @@ def all_to_all(xs: list[torch.Tensor], direction: int, group: str) -> list[torch
     s_glob = s * P if direction == SEQ_TO_HEAD_DIR else s
     epoch = pool.next_epoch()
     chk = kernels.a2a_launch(direction, descs, b, s_glob, d, xs[0].element_size(), P, st.rank,
-                             pool.region_ptrs, pool.flag_ptrs, epoch)
+                             slab.regions, pool.flag_ptrs, epoch)
     kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, chk)
     return outs
 
@@ -212,11 +242,11 @@ def attention_a2a(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: floa
     b, hl, S, d = q.shape
     lse = torch.empty((b, hl, S), dtype=torch.float32, device=q.device)
     shape, strides = _out_geometry(q, HEAD_TO_SEQ_DIR, P)  # (O has q's shape)
-    off, base = pool.alloc(math.prod(shape) * q.element_size())
-    o_tok = base.view(q.dtype).as_strided(shape, strides)
+    slab = pool.alloc(math.prod(shape) * q.element_size())
+    o_tok = slab.view.view(q.dtype).as_strided(shape, strides)
     epoch = pool.next_epoch()
-    chk = kernels.attn_fwd_push(q, k, v, None, lse, scale, causal, P, st.rank, off,
-                                (strides[0], strides[2], strides[1]), pool.region_ptrs,
+    chk = kernels.attn_fwd_push(q, k, v, None, lse, scale, causal, P, st.rank, slab.offset,
+                                (strides[0], strides[2], strides[1]), slab.regions,
                                 pool.flag_ptrs, epoch)
     kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, chk)
     return o_tok, lse
@@ -282,17 +312,17 @@ def ulysses_qkv_attention(qkv: torch.Tensor, pos: torch.Tensor, theta: float, hq
         raise ValidationError(f"qkv heads {H3} != {hq}+2*{hkv} or not divisible by {P}")
     srcs = (qkv[:, :, :hq], qkv[:, :, hq:hq + hkv], qkv[:, :, hq + hkv:])
     outs, descs = [], []
-    for x, rot in zip(srcs, (True, True, False)):
+    slab = pool.alloc_many([b * (x.shape[2] // P) * S * d * qkv.element_size() for x in srcs])
+    for x, rot, (off, base) in zip(srcs, (True, True, False), slab.pieces):
         h = x.shape[2]
         shape = (b, h // P, S, d)
         strides = ((h // P) * S * d, S * d, d, 1)
-        off, base = pool.alloc(math.prod(shape) * qkv.element_size())
         outs.append(base.view(qkv.dtype).as_strided(shape, strides))
         descs.append(kernels.a2a_tensor_desc(x, h, off, (strides[0], strides[2], strides[1]),
                                              rope=rot))
     epoch = pool.next_epoch()
     chk = kernels.a2a_launch(SEQ_TO_HEAD_DIR, descs, b, S, d, qkv.element_size(), P, st.rank,
-                             pool.region_ptrs, pool.flag_ptrs, epoch,
+                             slab.regions, pool.flag_ptrs, epoch,
                              pos=pos.to(torch.float32).contiguous(), theta=theta)
     kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, chk)
     qh, kh, vh = outs
@@ -343,8 +373,9 @@ def qkv_grad_gather(dq: torch.Tensor, dk: torch.Tensor, dv: torch.Tensor, pos: t
     hq, hkv, sl = hql * P, hkvl * P, S // P
     H3 = hq + 2 * hkv
     es = dq.element_size()
-    off, base = pool.alloc(b * sl * H3 * d * es)
-    dqkv = base.view(dq.dtype).as_strided((b, sl, H3, d), (sl * H3 * d, H3 * d, d, 1))
+    slab = pool.alloc(b * sl * H3 * d * es)
+    off = slab.offset
+    dqkv = slab.view.view(dq.dtype).as_strided((b, sl, H3, d), (sl * H3 * d, H3 * d, d, 1))
     descs = []
     for x, h0 in ((dq, 0), (dk, hq), (dv, hq + hkv)):
         if x.stride(-1) != 1:
@@ -352,7 +383,7 @@ def qkv_grad_gather(dq: torch.Tensor, dk: torch.Tensor, dv: torch.Tensor, pos: t
         descs.append(kernels.a2a_tensor_desc(x.permute(0, 2, 1, 3), x.shape[1], off + h0 * d * es,
                                              (sl * H3 * d, H3 * d, d)))
     epoch = pool.next_epoch()
-    chk = kernels.a2a_launch(HEAD_TO_SEQ_DIR, descs, b, S, d, es, P, st.rank, pool.region_ptrs,
+    chk = kernels.a2a_launch(HEAD_TO_SEQ_DIR, descs, b, S, d, es, P, st.rank, slab.regions,
                              pool.flag_ptrs, epoch)
     kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, chk)
     kernels.rope_segments([(dqkv[:, :, :hq], dqkv[:, :, :hq], True),
@@ -390,7 +421,7 @@ def ulysses_attention(q, k, v, group: str, is_causal=True, scale=None):
         vh = kh
     else:
         qh, kh, vh = all_to_all([q, k, v], SEQ_TO_HEAD_DIR, group)
-    if FUSE_OUTPUT_A2A:
+    if FUSE_OUTPUT_A2A and qh.shape[-1] in kernels.SUPPORTED_HEAD_DIMS:
         if not is_causal:
             raise ValidationError("auto_sp attention is causal (reference mask, executor.py:62-65)")
         sc = 1.0 / math.sqrt(qh.shape[-1]) if scale is None else float(scale)

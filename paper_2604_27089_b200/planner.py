@@ -8,11 +8,14 @@ Per rank, with S the global sequence, P the SP size, e = 2 (bf16), L layers:
 
   static     params + grads (e each) + optimizer state: AdamW moments (2e) and, under
              ZeRO-1 (P > 1), the owned fp shard copy, both divided by P
-  saved      what sp_ac keeps per layer:
+  saved      what sp_ac keeps per layer in the caching allocator:
                P == 1: x_in [S, d] + O [S, hq*hd] + LSE / rstd
-               P  > 1: x_in [S/P, d] + the fused op's outputs: o_tokens [S/P, hq*hd],
-                       q/k/v head shards [S, (hq + 2 hkv)/P * hd] + LSE [hq/P, S] fp32
-                       (no head-major O: delta = rowsum(dO*O) is formed token-side)
+               P  > 1: x_in [S/P, d] + LSE [hq/P, S] fp32 + rstd
+  pool       (P > 1) the symmetric receive heap (dist.SymmetricPool, grows on demand):
+             the a2a outputs sp_ac keeps per layer -- q/k/v head shards
+             [S, (hq + 2 hkv)/P * hd] and the token-major O [S/P, hq*hd] (no head-major O:
+             delta = rowsum(dO*O) is formed token-side) -- plus one layer's backward
+             reshards (dO head shard, delta, the packed dq/dk/dv gradient)
   transient  the largest backward working set of one layer: the recomputed MLP chunk
              (gate/up and their gradients, chunked at MLP_CHUNK tokens), the attention
              backward's fp32 dQ accumulator and bf16 dq/dk/dv, the recomputed projections,
@@ -37,10 +40,39 @@ class MemoryEstimate:
     static: float
     saved: float
     transient: float
+    pool: float = 0.0
 
     @property
     def total(self) -> float:
-        return self.static + self.saved + self.transient
+        return self.static + self.saved + self.pool + self.transient
+
+
+ALIGN = 1024  # dist.SymmetricPool.ALIGN
+
+
+def _al(n: int) -> int:
+    return (n + ALIGN - 1) // ALIGN * ALIGN
+
+
+def pool_layer_bytes(cfg: LlamaConfig, S: int, P: int, e: int = 2) -> tuple[int, int]:
+    """(kept, backward-transient) symmetric-heap bytes of ONE layer at P > 1, slab sizes
+    exactly as ops.py allocates them: the q/k/v reshard (one slab of three pieces), the
+    token-major O push; in backward the dO and delta reshards and the packed gradient."""
+    hd, hq, hkv, sl = cfg.head_dim, cfg.hq, cfg.hkv, S // P
+    qkv = _al(_al(e * S * hq // P * hd) + 2 * _al(e * S * hkv // P * hd))
+    o_tok = _al(e * sl * hq * hd)
+    bwd = _al(e * S * hq // P * hd) + _al(4 * S * hq // P) + _al(e * sl * (hq + 2 * hkv) * hd)
+    return qkv + o_tok, bwd
+
+
+def pool_bytes(cfg: LlamaConfig, S: int, P: int, e: int = 2) -> int:
+    """Steady-state high water of the symmetric receive heap of one rank for a training
+    step (every layer's kept a2a outputs + one layer's backward reshards); pass it to
+    dist.init(pool_bytes=...) to get the whole heap as one segment."""
+    if P == 1:
+        return 0
+    kept, bwd = pool_layer_bytes(cfg, S, P, e)
+    return cfg.layers * kept + bwd
 
 
 def step_memory(cfg: LlamaConfig, S: int, P: int = 1, zero1: bool = True,
@@ -53,17 +85,18 @@ def step_memory(cfg: LlamaConfig, S: int, P: int = 1, zero1: bool = True,
     if P == 1:
         per_layer = e * sl * (d + hq * hd) + 4 * sl * (hq + 2)          # x_in, O, LSE, rstd
     else:
-        per_layer = (e * sl * (d + hq * hd)                              # x_in, o_tokens
-                     + e * S * (hq + 2 * hkv) // P * hd                  # q/k/v head shards
-                     + 4 * S * hq // P + 4 * sl * 2)                     # LSE, rstd
+        per_layer = e * sl * d + 4 * S * hq // P + 4 * sl * 2            # x_in, LSE, rstd
     saved = L * per_layer + e * sl * d                                   # + final hidden
+    pool = pool_bytes(cfg, S, P, e)                                      # a2a outputs
     chunk = min(sl, MLP_CHUNK)
     mlp = e * chunk * (2 * F) * 2 + e * chunk * F * 2                    # gate/up (+grad), act (+grad)
-    attn = 4 * S * hq // P * hd + e * S * (hq + 2 * hkv) // P * hd * 2   # dQ acc, dq/dk/dv, do
+    attn = 4 * S * hq // P * hd + e * S * (hq + 2 * hkv) // P * hd       # dQ acc, dq/dk/dv
+    if P == 1:
+        attn += e * S * hq * hd                                          # dO (in the heap at P > 1)
     proj = e * sl * ((hq + 2 * hkv) * hd + 3 * d)                        # recomputed qkv, x_mid, grads
     head = e * CE_CHUNK * cfg.vocab * 2 + e * cfg.vocab * d + e * sl * d  # logits, dW, dh
     transient = max(mlp, attn) + proj + head
-    return MemoryEstimate(static, saved, transient)
+    return MemoryEstimate(static, saved, transient, pool)
 
 
 def predict_max_context(cfg: LlamaConfig, P: int, device_bytes: float,

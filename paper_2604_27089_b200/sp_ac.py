@@ -252,7 +252,10 @@ def plan(joint_module: fx.GraphModule, num_fwd_outputs: int, mode: AcMode):
     saved_sym = [n for n in saved if not isinstance(n.meta.get("val"), torch.Tensor)]
     saved_vals = [n for n in saved if isinstance(n.meta.get("val"), torch.Tensor)]
     recomputed = [n for n in fw if n.op != "placeholder" and n.name + "_out" not in reach]
+    guards = [n.name for n in joint_module.graph.nodes if n in fw and guarded(n, mode, fw)]
     stats = {"cut_bytes": int(cut_value), "saved": [n.name for n in saved_vals],
+             "guarded": guards,
+             "_fw_names": {n.name for n in fw if n.op == "call_function"},
              "saved_bytes": _tensor_bytes([n for n in saved_vals if not _aliases_input(n)]),
              "saved_detail": [(n.name, _opname(n), tuple(n.meta["val"].shape))
                               for n in saved_vals],
@@ -311,6 +314,11 @@ def make_partition_fn(mode: AcMode = AcMode.SEQ_AWARE_NON_ATTENTION):
         bw_mod = reordering_to_mimic_autograd_engine(bw_mod)
         stats["bw_recomputed_ops"] = sorted({_opname(n) for n in bw_mod.graph.nodes
                                              if n.op == "call_function"})
+        # forward nodes re-executed in the backward (the recompute schedule, ref
+        # ac_pass.py:187-219): the extracted backward keeps the joint graph's node names
+        fw_names = stats.pop("_fw_names")
+        stats["recomputed_fw_nodes"] = [n.name for n in bw_mod.graph.nodes
+                                        if n.op == "call_function" and n.name in fw_names]
         # every forward a2a has exactly one gradient a2a in backward; more means a
         # forward collective was recomputed (the reference's failure mode, SURVEY finding 2)
         n_fw = sum(is_autosp_collective(n) for n in fw_mod.graph.nodes)

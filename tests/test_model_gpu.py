@@ -30,15 +30,23 @@ def _c1_fixture(golden_dir, name):
     return z, orc.Dims(b, s, h, d, f, L), P, seed
 
 
-@pytest.mark.parametrize("passes", [["auto_sp", "sp_ac"], ["auto_sp"]])
-def test_seqcomp_c1_single_gpu_matches_reference_fixture(golden_dir, passes):
+@pytest.mark.parametrize("passes,mode", [(["auto_sp", "sp_ac"], "auto"), (["auto_sp"], "auto"),
+                                         (["auto_sp", "sp_ac"], "seq-aware"),
+                                         (["auto_sp", "sp_ac"], "conservative"),
+                                         (["auto_sp", "sp_ac"], "seq-aware-all")])
+def test_seqcomp_c1_single_gpu_matches_reference_fixture(golden_dir, passes, mode):
+    """C1 at P = 1 on the CUDA kernels vs the reference's result; the explicit AcModes make
+    sp_ac really recompute (`auto` resolves to save-all here), so the
+    recomputation that runs on the GPU is compared with the reference too (criterion 3,
+    test_acceptance.py:127-140)."""
     import paper_2604_27089_b200 as autosp
     from paper_2604_27089_b200 import ops, sp_ac
     from paper_2604_27089_b200.workloads import SeqcompDecoder, SeqcompDims
     z, dims, _, seed = _c1_fixture(golden_dir, "c1_p1")
     ops.ATTN_DTYPE = torch.bfloat16
-    autosp.reg_passes(passes)
+    autosp.reg_passes(passes, ac_mode=mode)
     autosp.dist.init(1)
+    sp_ac.LAST_PLAN.clear()
     ids, params = orc.random_leaves(dims, seed)
     model = SeqcompDecoder(SeqcompDims(dims.b, dims.s, dims.h, dims.d, dims.d_ffn, dims.layers),
                            dtype=torch.float32, device="cuda")
@@ -62,6 +70,11 @@ def test_seqcomp_c1_single_gpu_matches_reference_fixture(golden_dir, passes):
         assert abs(np.linalg.norm(grads[n]) / float(z[f"grad_{i}_norm"]) - 1) < GRAD_TOL, n
     if "sp_ac" in passes:
         assert not sp_ac.LAST_PLAN["bw_recomputes_attention"]
+        if mode != "auto":
+            assert sp_ac.LAST_PLAN["mode_applied"] == mode
+            assert sp_ac.LAST_PLAN["recomputed_fw_nodes"], "nothing recomputed"
+            assert not set(sp_ac.LAST_PLAN["recomputed_fw_nodes"]) & \
+                set(sp_ac.LAST_PLAN["guarded"])
 
 
 # Virtual ranks are threads of ONE process, so they would share torch's autograd engine

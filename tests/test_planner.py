@@ -22,3 +22,22 @@ def test_more_ranks_never_shorter():
             s = predict_max_context(cfg, P, DEV)
             assert s >= prev and s % (16 * 128 * P) == 0
             prev = s
+
+
+def test_symmetric_heap_term_matches_the_op_slabs():
+    """at P > 1 the planner models the symmetric receive heap (which
+    now grows on demand) with the exact slab sizes ops.py allocates: per layer one q/k/v
+    slab + one token-major O slab kept, plus one layer's backward reshards."""
+    from paper_2604_27089_b200.planner import pool_bytes, pool_layer_bytes
+    cfg = CONFIGS["llama3-8b"]
+    S, P = 524288, 8
+    kept, bwd = pool_layer_bytes(cfg, S, P)
+    sl, hd = S // P, cfg.head_dim
+    assert kept == 2 * S * (cfg.hq + 2 * cfg.hkv) // P * hd + 2 * sl * cfg.hq * hd
+    assert pool_bytes(cfg, S, P) == cfg.layers * kept + bwd
+    assert abs(pool_bytes(cfg, S, P) / 1e9 - 43.5) < 1.0      # ~43 GB per rank at 512K
+    est = step_memory(cfg, S, P)
+    assert est.pool == pool_bytes(cfg, S, P)
+    assert est.total == est.static + est.saved + est.pool + est.transient
+    assert est.total < 0.97 * DEV                             # C4 512K at SP=8 fits
+    assert step_memory(cfg, S, 1).pool == 0

@@ -89,3 +89,48 @@ def test_random_ops_are_never_recomputed(mode):
     assert not rand, ops
     for a, b in zip(leaves, ref):
         torch.testing.assert_close(a.grad, b.grad, rtol=1e-12, atol=1e-12)
+
+
+def _seqcomp_plan(mode, dims_t=(1, 64, 4, 8, 32, 2, 64)):
+    torch._dynamo.reset()
+    import paper_2604_27089_b200 as autosp
+    from paper_2604_27089_b200 import ops, sp_ac, testing
+    from paper_2604_27089_b200.workloads import SeqcompDecoder, SeqcompDims
+    testing.enable_cpu_lowering()
+    ops.ATTN_DTYPE = None
+    autosp.reg_passes(["auto_sp", "sp_ac"], ac_mode=mode)
+    autosp.dist.init(1)
+    torch.manual_seed(0)
+    m = SeqcompDecoder(SeqcompDims(*dims_t), dtype=torch.float64)
+    with torch.no_grad():
+        for p in m.parameters():
+            p.normal_(0.0, 0.1)
+    _, loss = autosp.compile(m)(torch.randint(0, 64, (dims_t[0], dims_t[1])))
+    loss.backward()
+    return dict(sp_ac.LAST_PLAN)
+
+
+MODES = ("conservative", "seq-aware", "seq-aware-all")
+
+
+@pytest.mark.parametrize("model", ["seqcomp", "llama"])
+def test_mode_cut_values_are_ordered(model):
+    """Reference test_ac_pass.py:89-96: fewer guards can only lower the min cut --
+    cut(seq-aware-all) <= cut(seq-aware) <= cut(conservative)."""
+    if model == "seqcomp":
+        cuts = {m: _seqcomp_plan(m)["cut_bytes"] for m in MODES}
+    else:
+        cuts = {m: _plan(2, 128, m)[1]["cut_bytes"] for m in MODES}
+    assert cuts["seq-aware-all"] <= cuts["seq-aware"] <= cuts["conservative"], cuts
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_guards_never_recomputed(mode):
+    """Reference test_ac_pass.py:98-105: no guarded forward node appears in the backward's
+    recompute schedule; and the non-conservative modes do recompute something."""
+    plan = _seqcomp_plan(mode)
+    rec = set(plan["recomputed_fw_nodes"])
+    assert not rec & set(plan["guarded"]), rec & set(plan["guarded"])
+    assert plan["mode_applied"] == mode
+    assert rec, "the plan recomputes nothing"
+    assert not plan["bw_recomputes_attention"]

@@ -134,8 +134,11 @@ def test_auto_sp_sp_ac_world2_matches_oracle(mode):
         # 2 collectives per layer forward (q/k/v reshard, attention + O push); backward:
         # the 2 gradient reshards + the tiny delta = rowsum(dO*O) reshard (3 per layer);
         # attention never recomputed (sp_ac guard) and no forward collective re-issued
+        # (head dims the kernels do not implement natively -- d = 4 here -- run the
+        # unfused O reshard: backward = dO reshard + gradient reshard, no delta reshard)
+        fused = dims.d in (32, 64, 128)
         assert plan["fw_collectives"] == 2 * dims.layers
-        assert plan["bw_collectives"] == 3 * dims.layers
+        assert plan["bw_collectives"] == (3 if fused else 2) * dims.layers
         assert not plan["bw_recomputes_attention"]
         reasons = sorted(prov.values())
         assert reasons.count("InsertedCollective") == dims.layers
@@ -176,3 +179,21 @@ def test_graph_break_in_loop_fails_loudly_at_p2():
     attention would silently see only the local shard.  compile() raises instead."""
     with pytest.raises(AssertionError, match="fell back to eager"):
         _run(2, (1, 16, 4, 4, 8, 2, 64), seed=5, graph_breaks="loop")
+
+
+def test_c1_size_world2_matches_reference_fixture(golden_dir):
+    """BASELINE configs[0] at its real size (d_model 256, 8 heads, d 32, L 2, d_ffn 1024,
+    s 1024, P 2) through the whole pass stack on gloo, against the reference's own P = 2
+    result (model_c1_p2.npz, fp64): per-rank loss, sampled hidden rows and gradients."""
+    z = np.load(golden_dir / "model_c1_p2.npz")
+    b, s, h, d, f, L, P, seed, _ = (int(v) for v in z["dims"])
+    out = _run(P, (b, s, h, d, f, L, 64), seed=seed, mode="seq-aware")
+    dims = orc.Dims(b, s, h, d, f, L)
+    hidden = np.concatenate([o[1] for o in out], axis=1)
+    assert orc.norm_rel_err(hidden[:, z["hidden_rows"]], z["hidden_sample"]) < 1e-9
+    for r, o in enumerate(out):
+        assert abs(o[2] - z["loss_per_rank"][r]) <= 1e-9 * abs(z["loss_per_rank"][r])
+        for i, n in enumerate(orc.param_names(dims)):
+            g = o[3][n].reshape(-1)
+            assert orc.norm_rel_err(g[z[f"grad_{i}_idx"]], z[f"grad_{i}_val"]) < 1e-9, n
+        assert o[5]["mode_applied"] == "seq-aware" and o[5]["recomputed_fw_nodes"]

@@ -1,5 +1,5 @@
 """Predicted maximum trainable context per SP size (planner.py) next to the measured
-single-GPU frontier.  Prints one JSON document (profiles/max_context_model_r01.json)."""
+single-GPU frontier.  Prints one JSON document (profiles/max_context_model_r02.json)."""
 import json
 import sys
 from pathlib import Path
@@ -27,5 +27,6 @@ for name in ("llama3-8b", "llama3.2-1b"):
                             "measured_max_seq": measured.get((name, P)),
                             "at_prediction_gb": {"static": round(est.static / 1e9, 1),
                                                  "saved": round(est.saved / 1e9, 1),
+                                                 "symmetric_heap": round(est.pool / 1e9, 1),
                                                  "transient": round(est.transient / 1e9, 1)}})
 print(json.dumps(out, indent=1))
