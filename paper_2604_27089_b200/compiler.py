@@ -11,11 +11,14 @@ AcMode + plan_checkpoints (ac_pass.py:26-29,181-184)."""
 
 from __future__ import annotations
 
+import functools
 import os
 
 import torch
+import torch.distributed as tdist
 
 from . import dist as sp_dist
+from . import grad_sync
 from .auto_sp import auto_sp
 from .errors import ValidationError
 from .sp_ac import AcMode, is_autosp_collective, make_partition_fn
@@ -51,9 +54,11 @@ def backend(passes: list[str] | None = None, ac_mode: AcMode | None = None):
     passes = list(_PASSES if passes is None else passes)
     mode = _AC_MODE if ac_mode is None else AcMode(ac_mode)
 
-    def _compiler(gm, example_inputs):
+    def _compiler(gm, example_inputs, sync=None):
         if _COMPILER_OVERRIDE is not None:
             return _COMPILER_OVERRIDE(gm, example_inputs)
+        if sync is not None:  # backward graph: bucketed SP/DP gradient all-reduce
+            grad_sync.insert(gm, *sync)
         fn = make_boxed_func(gm.forward)
         st = sp_dist.state()
         if st.world > 1 and st.group is not None and \
@@ -79,7 +84,15 @@ def backend(passes: list[str] | None = None, ac_mode: AcMode | None = None):
             gm, info = auto_sp(gm, example_inputs, st)
             LAST_INFO["auto_sp"] = info
         part = make_partition_fn(mode) if "sp_ac" in passes else default_partition
-        return aot_autograd(fw_compiler=_compiler, bw_compiler=_compiler,
+        bw = _compiler
+        if grad_sync.enabled(st):
+            # the forward inputs that are parameters: their (partial) gradients are
+            # all-reduced inside the backward graph, overlapped with it (grad_sync.py)
+            pidx = [i for i, x in enumerate(example_inputs) if isinstance(x, torch.nn.Parameter)]
+            dp = tdist.get_world_size() // max(st.world, 1)
+            sync = (pidx, [example_inputs[i] for i in pidx], len(example_inputs), dp)
+            bw = functools.partial(_compiler, sync=sync)
+        return aot_autograd(fw_compiler=_compiler, bw_compiler=bw,
                             partition_fn=part)(gm, example_inputs)
 
     return _backend
@@ -102,6 +115,9 @@ def compile(model: torch.nn.Module, passes: list[str] | None = None,
     P > 1 a call that left any frame uncompiled raises ValidationError (set
     AUTOSP_ALLOW_EAGER_FRAMES=1 if the skipped frames are known to hold no attention)."""
     passes_eff = list(_PASSES if passes is None else passes)
+    st = sp_dist.state()
+    if grad_sync.enabled(st):  # SP-partial gradients summed by the backward itself
+        grad_sync.install(model, tdist.get_world_size() // max(st.world, 1))
     cm = torch.compile(model, backend=backend(passes, ac_mode), dynamic=False, fullgraph=False)
     if "auto_sp" not in passes_eff:
         return cm

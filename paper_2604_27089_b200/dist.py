@@ -75,7 +75,9 @@ def _raw_tensor(ptr: int, nbytes: int, device) -> torch.Tensor:
 class _Slot:
     offset: int
     nbytes: int
-    base: torch.Tensor  # uint8 view owned by the pool; busy while its storage is shared
+    # uint8 views owned by the pool, one storage per piece handed out; the slot is busy
+    # while ANY of those storages is still shared with a caller
+    bases: list[torch.Tensor]
 
 
 @dataclass
@@ -193,7 +195,8 @@ class SymmetricPool:
     # ------------------------------------------------------------------ allocation
     @staticmethod
     def _busy(slot: _Slot) -> bool:
-        return torch._C._storage_Use_Count(slot.base.untyped_storage()._cdata) > 2
+        return any(torch._C._storage_Use_Count(b.untyped_storage()._cdata) > 2
+                   for b in slot.bases)
 
     def _fit(self, sg: _Segment, need: int) -> int | None:
         if not self.reuse:
@@ -207,13 +210,13 @@ class SymmetricPool:
             off = max(off, x.offset + _align(x.nbytes))
         return off if off + need <= sg.capacity else None
 
-    def alloc(self, nbytes: int) -> Slab:
+    def alloc(self, nbytes: int, sizes: list[int] | None = None) -> Slab:
         """First-fit slab of `nbytes` (growing the heap collectively if nothing fits)."""
         need = _align(max(nbytes, 1))
         for i, sg in enumerate(self.segments):
             off = self._fit(sg, need)
             if off is not None:
-                return self._take(i, off, nbytes, need)
+                return self._take(i, off, nbytes, need, sizes)
         if not (self.growable and self.reuse):
             raise ValidationError(
                 f"symmetric receive region exhausted ({need} bytes requested, "
@@ -225,29 +228,37 @@ class SymmetricPool:
                 f"symmetric heap: growing by {cap} bytes failed on some rank of the SP group "
                 f"(heap {self.capacity} bytes in {len(self.segments)} segments)")
         self.segments.append(_Segment(cap, bases))
-        return self._take(len(self.segments) - 1, 0, nbytes, need)
+        return self._take(len(self.segments) - 1, 0, nbytes, need, sizes)
 
-    def _take(self, i: int, off: int, nbytes: int, need: int) -> Slab:
+    def _take(self, i: int, off: int, nbytes: int, need: int,
+              sizes: list[int] | None = None) -> Slab:
         sg = self.segments[i]
-        # a separate storage per slot so its C++ refcount tracks exactly this slot
-        base = _raw_tensor(sg.regions[self.rank] + off, nbytes, self.device)
+        # a separate storage per piece so the C++ refcounts track exactly this slot and
+        # the pieces of one call do not alias each other (custom ops may not return
+        # aliasing outputs)
+        many = sizes is not None
+        sizes = [nbytes] if sizes is None else sizes
+        bases, pieces, cur = [], [], 0
+        for n in sizes:
+            bases.append(_raw_tensor(sg.regions[self.rank] + off + cur, max(n, 1), self.device))
+            # hand out VIEWS: the caller's reference then holds the piece's storage (the
+            # pool's own base alone does not count as busy)
+            pieces.append((off + cur, bases[-1].view(-1)[:n]))
+            cur += _align(n)
         if self.reuse:
-            sg.slots.append(_Slot(off, nbytes, base))
+            sg.slots.append(_Slot(off, need, bases))
         sg.high_water = max(sg.high_water, off + need)
-        # hand out a VIEW: the caller's reference then holds the slot's storage (the
-        # pool's own `base` alone does not count as busy)
-        return Slab(i, off, base.view(-1), sg.regions)
+        slab = Slab(i, off, pieces[0][1], sg.regions)
+        if many:
+            slab.pieces = pieces
+        return slab
 
     def alloc_many(self, sizes: list[int]) -> Slab:
         """One slab holding consecutive ALIGN-aligned pieces of the given sizes (the
-        destinations of one call; slab.pieces = [(offset, uint8 view)]).  The slot is
-        released when the last piece dies."""
-        slab = self.alloc(sum(_align(n) for n in sizes))
-        cur = 0
-        for n in sizes:
-            slab.pieces.append((slab.offset + cur, slab.view[cur:cur + n]))
-            cur += _align(n)
-        return slab
+        destinations of one call, all in one segment so one peer-base array addresses
+        them; slab.pieces = [(offset, uint8 view)], each piece its own storage).  The
+        slot is released when the last piece dies."""
+        return self.alloc(sum(_align(n) for n in sizes), sizes=sizes)
 
     def next_epoch(self) -> int:
         self.epoch += 1
@@ -271,14 +282,21 @@ class SPState:
     device: torch.device = field(default_factory=lambda: torch.device("cpu"))
     pool: SymmetricPool | None = None
     name: str = "sp"
+    grad_sync: bool = True       # compile() all-reduces parameter gradients in-graph
 
 
 _STATE: SPState | None = None
 _REGISTRY: dict[str, SPState] = {}
 
 
-def init(sp_group_size: int, pool_bytes: int | None = None, backend: str | None = None) -> SPState:
-    """Create the SP groups (consecutive ranks), map the symmetric receive regions."""
+def init(sp_group_size: int, pool_bytes: int | None = None, backend: str | None = None,
+         grad_sync: bool = True) -> SPState:
+    """Create the SP groups (consecutive ranks), map the symmetric receive regions.
+
+    grad_sync (default): models compiled afterwards reduce their parameter gradients
+    inside the backward graph (sum over the SP group, mean over DP; grad_sync.py), so
+    the training loop stays ``loss.backward(); optimizer.step()``.  With False the loop
+    must call ``reduce_gradients`` (or use ``zero.ShardedAdamW``)."""
     global _STATE
     if sp_group_size < 1:
         raise ValidationError("sp_group_size must be positive")
@@ -301,7 +319,8 @@ def init(sp_group_size: int, pool_bytes: int | None = None, backend: str | None 
         device = torch.device("cuda", local)
     else:
         device = torch.device("cpu")
-    st = SPState(world=sp_group_size, rank=rank % sp_group_size, device=device)
+    st = SPState(world=sp_group_size, rank=rank % sp_group_size, device=device,
+                 grad_sync=grad_sync)
     if tdist.is_initialized() and world > 1:
         for g0 in range(0, world, sp_group_size):
             ranks = list(range(g0, g0 + sp_group_size))
@@ -362,11 +381,13 @@ def reduce_gradients(params, st: SPState | None = None,
     the reference's tests sum them, test_acceptance.py:89-96) and average over DP.
     Gradients are packed into buckets of at most ``bucket_bytes`` (one collective per
     bucket; a gradient larger than a bucket is reduced in place), so the transient memory
-    is one bucket, not a flat copy of every gradient (16 GB for an 8B model)."""
+    is one bucket, not a flat copy of every gradient (16 GB for an 8B model).
+    Gradients already reduced inside a compiled backward (grad_sync.py) are skipped."""
+    from . import grad_sync
     st = st or state()
     if not tdist.is_initialized():
         return
-    grads = [p.grad for p in params if p.grad is not None]
+    grads = [p.grad for p in grad_sync.consume(params)]
     if not grads:
         return
     sp = st.group if (st.group is not None and st.world > 1) else None

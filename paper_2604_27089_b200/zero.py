@@ -22,6 +22,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as tdist
 
+from . import grad_sync
 from .dist import SPState, state
 
 
@@ -124,10 +125,20 @@ class ShardedAdamW:
     # -------------------------------------------------------------- optimizer API
     @torch.no_grad()
     def step(self) -> None:
+        # gradients the compiled backward already all-reduced (grad_sync.py) are full
+        # sums: take this rank's slice instead of reduce-scattering them again
+        todo = grad_sync.consume(self.params)
+        reduced = not todo or len(todo) < sum(p.grad is not None for p in self.params)
+        if reduced and todo:  # a mix: bring the rest to full sums too
+            from .dist import reduce_gradients
+            reduce_gradients(todo, self.st)
         for (a, b), sh in zip(self.chunks, self.shards):
             n = (b - a) // self.P
             g = torch.empty(n, dtype=self.dtype, device=self.device)
-            self._reduce_scatter(self._flat_grads(a, b), g)  # (zero padding past the end)
+            if reduced:
+                g.copy_(self._flat_grads(a + self.rank * n, a + (self.rank + 1) * n))
+            else:
+                self._reduce_scatter(self._flat_grads(a, b), g)  # (zero padding past the end)
             sh.grad = g
         self.inner.step()
         for (a, b), sh in zip(self.chunks, self.shards):

@@ -56,10 +56,11 @@ def _graph_break_decoder(dims, dtype, in_loop=False):
     return GB(dims, dtype=dtype)
 
 
-def _worker(rank, world, port, dims_t, seed, passes, mode, q, graph_breaks=False):
+def _worker(rank, world, port, dims_t, seed, passes, mode, q, graph_breaks=False, sp=None,
+            grad_sync=False):
     import torch.distributed as tdist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
-                      WORLD_SIZE=str(world))
+                      WORLD_SIZE=str(world), AUTOSP_GRAD_BUCKET_BYTES=str(8 << 10))
     torch._dynamo.reset()
     try:
         tdist.init_process_group("gloo", rank=rank, world_size=world)
@@ -69,16 +70,20 @@ def _worker(rank, world, port, dims_t, seed, passes, mode, q, graph_breaks=False
         testing.enable_cpu_lowering()
         ops.ATTN_DTYPE = None  # keep fp64 end to end on CPU
         autosp.reg_passes(passes, ac_mode=mode)
-        st = autosp.dist.init(world)
+        sp = sp or world
+        st = autosp.dist.init(sp, grad_sync=grad_sync)
         dims = SeqcompDims(*dims_t)
         odims = orc.Dims(*dims_t)
         ids, params = orc.random_leaves(odims, seed)
+        if world > sp:  # data-parallel replica r // sp trains on its own batch
+            ids = orc.random_leaves(odims, seed + 1 + rank // sp)[0]
         model = (_graph_break_decoder(dims, torch.float64, graph_breaks == "loop")
                  if graph_breaks else SeqcompDecoder(dims, dtype=torch.float64))
         model.load_reference(params)
         cm = autosp.compile(model)
-        sl = dims.s // world
-        ids_r = torch.from_numpy(ids[:, rank * sl:(rank + 1) * sl].copy())
+        sl = dims.s // sp
+        r_sp = rank % sp
+        ids_r = torch.from_numpy(ids[:, r_sp * sl:(r_sp + 1) * sl].copy())
         hidden, loss = cm(ids_r)
         loss.backward()
         grads = {k: p.grad.detach().clone() for k, p in model.named_reference_params().items()}
@@ -86,8 +91,12 @@ def _worker(rank, world, port, dims_t, seed, passes, mode, q, graph_breaks=False
         autosp.dist.reduce_gradients(list(model.named_reference_params().values()), st)
         red = {k: p.grad.detach().numpy() for k, p in model.named_reference_params().items()}
         info = compiler.LAST_INFO.get("auto_sp")
+        from paper_2604_27089_b200 import grad_sync
+        plan = dict(sp_ac.LAST_PLAN, grad_sync=dict(grad_sync.LAST),
+                    in_graph=sum(bool(getattr(p, grad_sync.IN_GRAPH, False))
+                                 for p in model.parameters()))
         q.put((rank, hidden.detach().numpy(), local_loss, red,
-               {k: v.numpy() for k, v in grads.items()}, dict(sp_ac.LAST_PLAN),
+               {k: v.numpy() for k, v in grads.items()}, plan,
                {k: v.value for k, v in info.provenance.items()} if info else {}))
     except Exception as e:  # surface worker failures to the parent
         import traceback
@@ -97,12 +106,13 @@ def _worker(rank, world, port, dims_t, seed, passes, mode, q, graph_breaks=False
             tdist.destroy_process_group()
 
 
-def _run(world, dims_t, seed, passes=("auto_sp", "sp_ac"), mode="seq-aware", graph_breaks=False):
+def _run(world, dims_t, seed, passes=("auto_sp", "sp_ac"), mode="seq-aware", graph_breaks=False,
+         sp=None, grad_sync=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, dims_t, seed, list(passes), mode, q,
-                                               graph_breaks))
+                                               graph_breaks, sp, grad_sync))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -197,3 +207,36 @@ def test_c1_size_world2_matches_reference_fixture(golden_dir):
             g = o[3][n].reshape(-1)
             assert orc.norm_rel_err(g[z[f"grad_{i}_idx"]], z[f"grad_{i}_val"]) < 1e-9, n
         assert o[5]["mode_applied"] == "seq-aware" and o[5]["recomputed_fw_nodes"]
+
+
+@pytest.mark.parametrize("world,sp", [(2, 2), (4, 2)])
+def test_in_graph_grad_sync_listing1_loop(world, sp):
+    """Listing 1's unchanged loop: loss.backward() alone leaves every
+    rank with the FULL gradient -- summed over the SP group inside the compiled backward
+    (grad_sync.py), averaged over data-parallel replicas -- no reduce_gradients call.
+    world 4 = SP 2 x DP 2 (paper's ZeRO-1 runs use SP x DP): each DP
+    replica trains on its own batch; expected = mean over replicas of the oracle's
+    summed SP gradients."""
+    dims_t = (1, 16, 4, 4, 8, 2, 64)
+    seed = 11
+    out = _run(world, dims_t, seed=seed, sp=sp, grad_sync=True)
+    dims = orc.Dims(*dims_t)
+    _, params = orc.random_leaves(dims, seed)
+    refs = []
+    for dp in range(world // sp):
+        ids = orc.random_leaves(dims, seed + 1 + dp)[0] if world > sp else \
+            orc.random_leaves(dims, seed)[0]
+        refs.append(orc.sp_forward_backward(dims, ids, params, sp))
+    want = {k: sum(r.total_grads()[k] for r in refs) / len(refs) for k in refs[0].total_grads()}
+    for r, (_, hidden, loss, red, grads, plan, prov) in enumerate(out):
+        ref = refs[r // sp]
+        assert orc.max_rel_err(hidden, ref.hidden[r % sp]) <= 1e-10
+        for k in want:
+            # grads = p.grad right after loss.backward(), before any explicit reduction
+            assert orc.max_rel_err(grads[k], want[k]) <= 1e-9, (r, k)
+            assert orc.max_rel_err(red[k], want[k]) <= 1e-9, (r, k)  # no double reduction
+        # reduced INSIDE the backward graph: every parameter, in >1 bucket (8 KB buckets
+        # here), the first issued well before the graph's end (overlap with the backward)
+        gs = plan["grad_sync"]
+        assert plan["in_graph"] == len(want) == gs["params"]
+        assert gs["buckets"] > 1 and gs["start_positions"][0] < 0.8 * gs["nodes"]

@@ -65,6 +65,8 @@ def test_alloc_many_one_slot_released_with_last_piece():
     offs = [o for o, _ in slab.pieces]
     assert offs == [0, 3072, 4096] and [v.numel() for _, v in slab.pieces] == [3000, 100, 5000]
     a, b, c = (v for _, v in slab.pieces)
+    # one storage per piece: custom ops may not return outputs aliasing each other
+    assert len({t.untyped_storage()._cdata for t in (a, b, c)}) == 3
     del slab
     gc.collect()
     del a, b
