@@ -94,63 +94,172 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU baseline
-def cpu_oracle_sample(cfg, b: int, s: int, budget_s: float = 12.0) -> dict:
-    """Time the CPU oracle (restated reference path, NumPy/OpenBLAS, all host threads)
-    on a bounded sample of the SAME step and scale it to tokens/s:
-      attention: oracle attention_fwd + attention_bwd on one head at s_a tokens (fp32),
-                 rate applied to the step's causal attention FLOPs (fwd 1x + bwd 2.5x);
-      dense:     one transformer layer's projections/MLP fwd+bwd (6 * params * tokens)
-                 on a 512-token sample, rate applied to all layers + LM head."""
+class CpuSampledStep:
+    """The reference's CPU path (the oracle port: NumPy/OpenBLAS fp32 on all host
+    threads, attention by the reference's recipe executor.py:132-142 / autodiff.py:156-214)
+    EXECUTING a bounded sample of the same training step: `blocks` runs of `block`
+    consecutive query tokens at stratified positions t_i = (i + 1/2)·S/blocks of the
+    S-token sequence go through the whole model depth, forward and backward -- every
+    layer's norms, projections, SwiGLU MLP and the LM head + cross entropy on those
+    tokens, and each block's attention rows against their FULL causal prefix of t_i
+    keys/values (all q heads, GQA; the reference's score-matrix recipe on a [block, t_i]
+    slab) -- so the work per sampled token averages the real step's per-token work (mean
+    prefix S/2).
+    Not included: the K/V projections of the prefix tokens (each is the sampled-token
+    projection work of another token), and the optimizer step (per step, not per token:
+    its share of a 32K-token step is < 0.01 %).  One layer's weights serve every layer
+    (the same GEMM shapes; 240 MB per layer streams from DRAM either way)."""
+
+    def __init__(self, cfg, S: int, blocks: int = 1, block: int = 4, seed: int = 0):
+        import numpy as np
+        self.np = np
+        n_tok = blocks * block
+        self.cfg, self.S, self.n, self.block = cfg, S, n_tok, block
+        rng = np.random.default_rng(seed)
+        f32 = np.float32
+        d, dm = cfg.head_dim, cfg.d_model
+        w = lambda *sh: ((rng.random(sh, dtype=f32) - f32(0.5)) * f32(0.04))
+        self.wqkv = w((cfg.hq + 2 * cfg.hkv) * d, dm)
+        self.wo = w(dm, cfg.hq * d)
+        self.w13 = w(2 * cfg.d_ffn, dm)
+        self.w2 = w(dm, cfg.d_ffn)
+        self.wlm = w(cfg.vocab, dm)
+        self.g1 = np.ones(dm, f32)
+        self.g2 = np.ones(dm, f32)
+        self.kbuf = rng.standard_normal((1, S, cfg.hkv, d), dtype=f32)
+        self.vbuf = rng.standard_normal((1, S, cfg.hkv, d), dtype=f32)
+        self.x0 = rng.standard_normal((n_tok, dm), dtype=f32)
+        self.labels = rng.integers(0, cfg.vocab, n_tok)
+        # last query position of each block (the block attends keys [0, t])
+        self.pos = [min(S - 1, int((i + 0.5) * S / blocks) + block - 1) for i in range(blocks)]
+
+    def run(self) -> float:
+        from oracle import seqcomp_oracle as orc
+        np, cfg, n = self.np, self.cfg, self.n
+        d, hq = cfg.head_dim, cfg.hq
+        t0 = time.perf_counter()
+        x, caches = self.x0, []
+        for _ in range(cfg.layers):
+            h1 = orc.rmsnorm(x, self.g1)
+            q = (h1 @ self.wqkv.T)[:, :hq * d].reshape(n, hq, d)
+            o = np.empty_like(q)
+            B = self.block
+            for i, t in enumerate(self.pos):
+                o[i * B:(i + 1) * B] = orc.attention_fwd(
+                    q[None, i * B:(i + 1) * B], self.kbuf[:, :t + 1], self.vbuf[:, :t + 1],
+                    causal=False)[0][0]
+            xm = x + o.reshape(n, hq * d) @ self.wo.T
+            h2 = orc.rmsnorm(xm, self.g2)
+            gu = h2 @ self.w13.T
+            gt, up = gu[:, :cfg.d_ffn], gu[:, cfg.d_ffn:]
+            a = orc.silu(gt) * up
+            caches.append((x, h1, q, o, xm, h2, gt, up, a))
+            x = xm + a @ self.w2.T
+        hf = orc.rmsnorm(x, self.g1)
+        logits = hf @ self.wlm.T
+        p = np.exp(logits - logits.max(-1, keepdims=True))
+        p /= p.sum(-1, keepdims=True)
+        p[np.arange(n), self.labels] -= 1.0
+        _dwlm = p.T @ hf
+        dx = orc.rmsnorm_dx(x, self.g1, p @ self.wlm)
+        for (xi, h1, q, o, xm, h2, gt, up, a) in reversed(caches):
+            _dw2 = dx.T @ a
+            da = dx @ self.w2
+            dgu = np.concatenate([orc.silu_dx(gt, da * up), da * orc.silu(gt)], axis=1)
+            _dw13 = dgu.T @ h2
+            dxm = dx + orc.rmsnorm_dx(xm, self.g2, dgu @ self.w13)
+            _dg2 = orc.rmsnorm_dw(xm, self.g2, dgu @ self.w13)
+            _dwo = dxm.T @ o.reshape(n, hq * d)
+            do = (dxm @ self.wo).reshape(n, hq, d)
+            dq = np.empty_like(q)
+            for i, t in enumerate(self.pos):
+                sl = slice(i * B, (i + 1) * B)
+                dq[sl] = orc.attention_bwd(q[None, sl], self.kbuf[:, :t + 1],
+                                           self.vbuf[:, :t + 1], do[None, sl], causal=False)[0][0]
+            dqkv = np.zeros((n, self.wqkv.shape[0]), np.float32)
+            dqkv[:, :hq * d] = dq.reshape(n, hq * d)
+            _dwqkv = dqkv.T @ h1
+            dx = dxm + orc.rmsnorm_dx(xi, self.g1, dqkv @ self.wqkv)
+        return time.perf_counter() - t0
+
+
+def _attention_extrapolated(cfg, b: int, s: int, budget_s: float = 6.0) -> dict:
+    """BASELINE.md §3 'attention': the oracle attention fwd+bwd on one head at 2048 tokens,
+    its FLOP rate applied to the step's attention FLOPs (labelled extrapolated)."""
     import numpy as np
 
     from oracle import seqcomp_oracle as orc
     from paper_2604_27089_b200.kernels import causal_attn_flops
-
     rng = np.random.default_rng(0)
-    d = cfg.head_dim
-    s_a = 2048
-    q = rng.standard_normal((1, s_a, 1, d)).astype(np.float32)
-    k = rng.standard_normal((1, s_a, 1, d)).astype(np.float32)
-    v = rng.standard_normal((1, s_a, 1, d)).astype(np.float32)
-    do = rng.standard_normal((1, s_a, 1, d)).astype(np.float32)
-    t0 = time.perf_counter()
-    n_att = 0
-    while True:
+    s_a, d = 2048, cfg.head_dim
+    q, k, v, do = (rng.standard_normal((1, s_a, 1, d)).astype(np.float32) for _ in range(4))
+    t0, n = time.perf_counter(), 0
+    while n == 0 or time.perf_counter() - t0 < budget_s:
         orc.attention_fwd(q, k, v)
         orc.attention_bwd(q, k, v, do)
-        n_att += 1
-        if time.perf_counter() - t0 > budget_s / 2:
-            break
-    t_att = (time.perf_counter() - t0) / n_att
-    rate_att = 3.5 * causal_attn_flops(1, 1, s_a, d) / t_att
-
-    ntok, dm = 512, cfg.d_model
-    ws = [rng.standard_normal(sh).astype(np.float32) * 0.02 for sh in
-          [((cfg.hq + 2 * cfg.hkv) * d, dm), (dm, cfg.hq * d), (2 * cfg.d_ffn, dm), (dm, cfg.d_ffn)]]
-    x = rng.standard_normal((ntok, dm)).astype(np.float32)
-    t0 = time.perf_counter()
-    n_den = 0
-    layer_params = sum(w.size for w in ws)
-    while True:
-        for w in ws:
-            xi = x if w.shape[1] == dm else rng.standard_normal((ntok, w.shape[1])).astype(np.float32)
-            y = xi @ w.T
-            _ = y @ w          # dX
-            _ = y.T @ xi       # dW
-        n_den += 1
-        if time.perf_counter() - t0 > budget_s / 2:
-            break
-    t_den = (time.perf_counter() - t0) / n_den
-    rate_den = 6.0 * layer_params * ntok / t_den
-
+        n += 1
+    rate = 3.5 * causal_attn_flops(1, 1, s_a, d) / ((time.perf_counter() - t0) / n)
     att_total = 3.5 * cfg.layers * causal_attn_flops(b, cfg.hq, s, d)
-    dense_total = 6.0 * (cfg.n_params() - cfg.vocab * cfg.d_model) * b * s
-    t_step = att_total / rate_att + dense_total / rate_den
-    return {"value": b * s / t_step, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": (f"oracle attention fwd+bwd, 1 head x {s_a} tokens (fp32, {n_att} reps, "
-                       f"{rate_att/1e9:.1f} GFLOP/s) + one layer's dense fwd+bwd on {ntok} tokens "
-                       f"({rate_den/1e9:.1f} GFLOP/s), scaled by FLOPs to the {s}-token step"),
-            "seconds_per_step_extrapolated": t_step}
+    return {"gflops": rate / 1e9, "sample": f"1 head x {s_a} tokens fp32, {n} reps",
+            "attention_seconds_per_step_extrapolated": att_total / rate}
+
+
+def _c1_end_to_end() -> dict:
+    """BASELINE.md §3 'end-to-end': the oracle's restatement of execute_ranks on the SP
+    joint graph (executor.py:344-352) for configs[0] (s 1024, h 8, d 32, d_ffn 1024, L 2,
+    P 2), forward + backward, fp32 and fp64 -> tokens/s (measured, not scaled)."""
+    import numpy as np
+
+    from oracle import seqcomp_oracle as orc
+    dims = orc.Dims(1, 1024, 8, 32, 1024, 2)
+    ids, params = orc.random_leaves(dims, 0)
+    out = {}
+    for name, dt in (("fp32", np.float32), ("fp64", np.float64)):
+        orc.sp_forward_backward(dims, ids, params, 2, dtype=dt)
+        t0 = time.perf_counter()
+        orc.sp_forward_backward(dims, ids, params, 2, dtype=dt)
+        out[name] = dims.s / (time.perf_counter() - t0)
+    return {"tokens_per_s": out, "config": "configs[0]: s 1024, d_model 256, 8 heads, L 2, P 2"}
+
+
+def _a2a_gbs() -> dict:
+    """BASELINE.md §3 'per-op': the oracle's all_to_all_shards (executor.py:203-230) at
+    the per-layer Q shapes of configs[1] (Llama-1B 32K) and configs[2] (Llama-8B 128K),
+    P = 8, bf16 payload as uint16, all ranks in one process -> GB/s copied."""
+    import numpy as np
+
+    from oracle import seqcomp_oracle as orc
+    out = {}
+    for name, s, d in (("llama3.2-1b_32k_p8", 32768, 64), ("llama3-8b_128k_p8", 131072, 128)):
+        shards = [np.full((1, s // 8, 32, d), j, np.uint16) for j in range(8)]
+        orc.all_to_all_shards("seq_to_head", shards)
+        t0 = time.perf_counter()
+        orc.all_to_all_shards("seq_to_head", shards)
+        out[name] = sum(x.nbytes for x in shards) / (time.perf_counter() - t0) / 1e9
+    return out
+
+
+def cpu_baseline(cfg, b: int, s: int, steps: int = 2, warmup: int = 1, blocks: int = 1,
+                 block: int = 4, extras: bool = True) -> dict:
+    """Measured CPU baseline (see CpuSampledStep): tokens/s = sampled tokens / measured
+    seconds per sampled step, plus the BASELINE.md §3 figures."""
+    smp = CpuSampledStep(cfg, s, blocks, block)
+    n_tok = smp.n
+    times = [smp.run() for _ in range(warmup + steps)][warmup:]
+    t = statistics.median(times)
+    out = {"value": b * n_tok / t, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+           "sample": (f"{n_tok} query tokens per step ({blocks} runs of {block} consecutive "
+                      f"tokens at stratified positions of the {s}-token sequence), full depth ({cfg.layers} layers) fwd+bwd + LM head, each "
+                      f"attending its full causal prefix (mean {s // 2}); NumPy fp32, "
+                      f"OPENBLAS_NUM_THREADS={os.environ.get('OPENBLAS_NUM_THREADS', 'unset')}; "
+                      f"optimizer step excluded"),
+           "seconds_per_sampled_step": t, "sampled_step_times": times,
+           "tokens_per_step": b * n_tok}
+    if extras:
+        att = _attention_extrapolated(cfg, b, s)
+        out["baseline_md_s3"] = {"c1_end_to_end": _c1_end_to_end(), "a2a_gbs": _a2a_gbs(),
+                                 "attention_extrapolated": att}
+    return out
 
 
 def run_reference(args):
@@ -159,20 +268,16 @@ def run_reference(args):
         return 0
     from paper_2604_27089_b200.workloads import CONFIGS
     cfg = CONFIGS[args.model]
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_oracle_sample(cfg, args.batch, args.seq, budget_s=4.0)
-        if i >= args.warmup:
-            vals.append(r["value"])
-    v = statistics.median(vals)
-    r["value"] = v
+    r = cpu_baseline(cfg, args.batch, args.seq, steps=args.steps, warmup=args.warmup)
+    v = r["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": args.batch * args.seq / v * 1e3, "higher_is_better": True,
+            "ms_per_step": r["seconds_per_sampled_step"] * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{cfg.name} seq {args.seq} (CPU oracle, bounded sample)",
+            "config": {"workload": (f"{cfg.name} seq {args.seq}: CPU oracle port executing a "
+                                    f"bounded sample of the step ({r['sample']})"),
                        "model": cfg.name, "global_batch": args.batch, "seq_len": args.seq,
-                       "parallelism": f"sp{args.gpus}"},
+                       "tokens_per_step": r["tokens_per_step"], "parallelism": "cpu"},
             "cpu_baseline": r,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -194,6 +299,8 @@ def main():
                          "seq-aware, conservative, seq-aware-all")
     ap.add_argument("--no-sp-ac", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sp-ac-block", action="store_true",
+                    help="skip the extra seq-aware-vs-save-all comparison steps")
     ap.add_argument("--no-zero1", action="store_true",
                     help="N > 1: all-reduce gradients + replicated AdamW instead of ZeRO-1")
     ap.add_argument("--layers", type=int, default=None, help="override (debug only; invalid bench)")
@@ -251,13 +358,11 @@ def main():
     labels = lab_host.to(dev)
     params = list(model.parameters())
 
-    def step(ids_, labels_):
-        hidden = cm(ids_)
+    def step(ids_, labels_, cm_=None):
+        hidden = (cm if cm_ is None else cm_)(ids_)
         loss = lm_loss(hidden, model.lm_head, labels_)
-        loss.backward()
-        if P > 1 and not zero1:
-            autosp.dist.reduce_gradients(params, st)
-        opt.step()  # (ShardedAdamW reduces the SP-partial gradients itself)
+        loss.backward()  # (P > 1: the SP-partial gradients are all-reduced in-graph)
+        opt.step()
         opt.zero_grad(set_to_none=True)
         return loss
 
@@ -312,6 +417,40 @@ def main():
            "h2d_bytes_per_step": (ids_host.numel() + lab_host.numel()) * ids_host.element_size(),
            "d2h_bytes_per_step": 4}
 
+    ac_applied = sp_ac.LAST_PLAN.get("mode_applied")
+
+    # ---------------- sp_ac block: the same step with seq-aware recomputation forced,
+    # against the planner's choice (paper: SP+AC vs SP-only 1.07x step time, 1.66x
+    # trainability) -- step time and steady-state peak memory
+    spac = None
+    if "sp_ac" in passes and ac_applied == "save-all" and not args.no_sp_ac_block:
+        def timed(cm_, n):
+            torch.cuda.reset_peak_memory_stats(dev)
+            barrier()
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(n):
+                step(ids, labels, cm_)
+            z.record()
+            barrier()
+            ms = torch.tensor([a.elapsed_time(z) / n, torch.cuda.max_memory_allocated(dev)],
+                              dtype=torch.float64, device=dev)
+            if world > 1:
+                tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
+            return float(ms[0]), float(ms[1])
+        base_ms, base_mem = timed(cm, 2)
+        cm_sa = autosp.compile(model, ac_mode="seq-aware")
+        step(ids, labels, cm_sa)  # compile + warm-up
+        plan = dict(sp_ac.LAST_PLAN)
+        sa_ms, sa_mem = timed(cm_sa, 2)
+        spac = {"mode": plan.get("mode_applied"), "ms_per_step": sa_ms,
+                "save_all_ms_per_step": base_ms, "step_time_ratio": sa_ms / base_ms,
+                "peak_mem_gb": sa_mem / 1e9, "save_all_peak_mem_gb": base_mem / 1e9,
+                "peak_mem_ratio": base_mem / sa_mem,
+                "saved_bytes_per_rank_gb": (plan.get("saved_bytes") or 0) / 1e9,
+                "recomputed_fw_nodes": len(plan.get("recomputed_fw_nodes") or []),
+                "paper": "SP+AC vs SP-only: 7 % slower, 1.66x trainability (PAPER.md:321)"}
+
     if rank != 0:
         if world > 1:
             tdist.barrier()
@@ -332,6 +471,19 @@ def main():
                 "share_of_step": v["ms"] / t_ms,
                 "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None}
             for k, v in ksum.items()}
+    a2a = None
+    if "a2a" in ksum and P > 1:
+        v = ksum["a2a"]
+        a2a = {"kernel": "K1/K2 push (handshake + push launches; the O reshard fused into "
+                         "attn_fwd is not separately timed)",
+               "calls_per_step": v["calls"] / args.steps,
+               "bytes_per_call": v["bytes"] / max(v["calls"], 1),
+               "us_per_call": v["ms"] * 1e3 / max(v["calls"], 1),
+               "gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] else None,
+               "peak_gbs": 900.0, "peak_kind": "NVLink 5 per direction per GPU (nominal)"}
+        a2a["frac"] = a2a["gbs"] / 900.0 if a2a["gbs"] else None
+        if os.environ.get("AUTOSP_BENCH_BACKEND") == "gloo":
+            a2a["note"] = "ranks share ONE GPU (test harness): loopback, not NVLink"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
@@ -343,7 +495,7 @@ def main():
                    "model": cfg.name, "global_batch": b, "seq_len": S,
                    "parallelism": f"sp{P}" + ("+zero1" if zero1 else ""), "passes": passes,
                    "ac_mode": args.ac_mode,
-                   "ac_applied": sp_ac.LAST_PLAN.get("mode_applied"),
+                   "ac_applied": ac_applied,
                    "l2": f"working set (weights {2 * cfg.n_params() / 1e9:.1f} GB + activations)"
                          " >> 126 MB L2; no flush"},
         "e2e": e2e,
@@ -356,12 +508,14 @@ def main():
                      "algorithmic_flops_per_launch": dom["flops"] / max(dom["calls"], 1),
                      "traffic": traffic},
         "kernels": kern,
+        "a2a": a2a,
+        "sp_ac": spac,
         "peak_mem_gb": peak_mem / 1e9,
         "final_loss": loss_v,
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_oracle_sample(cfg, b, S)
+        line["cpu_baseline"] = cpu_baseline(cfg, b, S)
     print(json.dumps(line), flush=True)
     if world > 1:
         tdist.barrier()

@@ -199,6 +199,19 @@ AUTOSP_API int autosp_attn_bwd_delta(autosp_attn_tensor q, autosp_attn_tensor k,
                     autosp_attn_tensor dv, void* workspace, int b, int hq, int hkv, int s, int d,
                     float scale, int causal, void* stream);
 
+/* autosp_attn_bwd_delta fused with the head->seq all-to-all of the gradients (the
+ * backward of the RoPE-fused seq->head reshard, autodiff.py:252-262): nothing is written
+ * locally; every dQ / dK / dV row goes straight into the token owner's receive region as
+ * the PACKED QKV-projection gradient [b, s/P, hq*P + 2*hkv*P, d] (push->dst_* strides;
+ * dq at global head rank*hq + h, dk at hq*P + rank*hkv + h, dv at hq*P + hkv*P + rank*hkv
+ * + h; hq/hkv are this rank's local head counts).  The ready handshake runs first; the
+ * arrival is published when the last dQ row is out.  Check word: autosp_push_check(push,
+ * hq + 2*hkv).  The receiver waits with autosp_a2a_wait. */
+AUTOSP_API int autosp_attn_bwd_push(autosp_attn_tensor q, autosp_attn_tensor k,
+                    autosp_attn_tensor v, const float* delta, autosp_attn_tensor d_o,
+                    const float* lse, void* workspace, int b, int hq, int hkv, int s, int d,
+                    float scale, int causal, const autosp_push_spec* push, void* stream);
+
 /* ------------------------------------------------------------------ fused elementwise
  * HBM-bound bf16 kernels for the layer around the Ulysses path (fp32 math):
  *   swiglu: out[r, :] = silu(gu[r, :F]) * gu[r, F:2F]        (reference silu executor.py:33-34,

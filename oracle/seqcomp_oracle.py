@@ -154,9 +154,9 @@ def attention_bwd(q, k, v, do, causal: bool = True, scale: float | None = None):
     dscores = dmasked * q.dtype.type(scale)
     dq = np.matmul(dscores, kh)
     dk = np.matmul(np.swapaxes(dscores, -1, -2), qh)
-    g = hq // hkv
-    dk = dk.reshape(b, hkv, g, s, d).sum(axis=2)
-    dv = dv.reshape(b, hkv, g, s, d).sum(axis=2)
+    g, sk = hq // hkv, k.shape[1]  # (sk != s: a query block against a longer key prefix)
+    dk = dk.reshape(b, hkv, g, sk, d).sum(axis=2)
+    dv = dv.reshape(b, hkv, g, sk, d).sum(axis=2)
     return (np.transpose(dq, (0, 2, 1, 3)), np.transpose(dk, (0, 2, 1, 3)),
             np.transpose(dv, (0, 2, 1, 3)))
 

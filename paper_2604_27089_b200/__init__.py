@@ -5,8 +5,8 @@ User API (Listing 1):
     autosp.reg_passes(['auto_sp', 'sp_ac'])
     autosp.dist.init(SP_GROUP_SIZE)
     model = autosp.compile(model)           # model.compile(backend=autosp.backend())
-    loss = model(batch[:, sp_slice]); loss.backward()
-    autosp.dist.reduce_gradients(model.parameters()); opt.step()
+    loss = model(batch[:, sp_slice]); loss.backward()   # grads summed over SP in-graph
+    opt.step()
 """
 
 from . import dist

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/autosp.h"
+#include "flags.cuh"
 #include "ptx.cuh"
 #include "tma.cuh"
 
@@ -124,6 +125,12 @@ struct Params {
   float scale, scale_log2;
   int causal;
   int n_ktiles;
+  // fused head->seq all-to-all of the gradients (autosp_attn_bwd_push): dK / dV rows go
+  // straight into the token owner's packed [b, s/P, hq+2hkv, d] QKV gradient (global
+  // heads hq*P + rank*hkv + kvh and hq*P + hkv*P + rank*hkv + kvh); push == 0: local
+  int push, P, rank, s_loc;
+  int64_t dst_off, d_sb, d_ss, d_sh;  // bytes / elements
+  char* peer_base[AUTOSP_MAX_WORLD];
 };
 
 constexpr int kTraceSteps = 64;
@@ -542,9 +549,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       tc_fence_after();
       const uint32_t src = tmem + lane_base + (half ? C::DK_COL : C::DV_COL);
       const float sc = half ? p.scale : 1.f;
-      __nv_bfloat16* dst =
-          half ? p.dk + (int64_t)batch * p.dk_sb + (int64_t)kvh * p.dk_sh + (int64_t)key * p.dk_ss
-               : p.dv + (int64_t)batch * p.dv_sb + (int64_t)kvh * p.dv_sh + (int64_t)key * p.dv_ss;
+      __nv_bfloat16* dst;
+      if (p.push) {  // fused K2: the row goes to the owner of token `key`
+        const int j = min(key, p.S - 1) / p.s_loc;
+        const int gh = p.Hq * p.P + (half ? 0 : p.Hkv * p.P) + p.rank * p.Hkv + kvh;
+        dst = reinterpret_cast<__nv_bfloat16*>(p.peer_base[j] + p.dst_off) +
+              (int64_t)batch * p.d_sb + (int64_t)(key - j * p.s_loc) * p.d_ss +
+              (int64_t)gh * p.d_sh;
+      } else {
+        dst = half ? p.dk + (int64_t)batch * p.dk_sb + (int64_t)kvh * p.dk_sh + (int64_t)key * p.dk_ss
+                   : p.dv + (int64_t)batch * p.dv_sb + (int64_t)kvh * p.dv_sh + (int64_t)key * p.dv_ss;
+      }
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t a[32];
@@ -645,6 +660,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   tc_fence_before();
   __syncthreads();
   if (warp == kAllocWarp) tmem_dealloc<512>(tmem);
+  // pushed dK/dV rows: visible system-wide before bwd_post publishes the arrival (the
+  // CTA barrier above orders every thread's stores before this cumulative fence)
+  if (p.push && threadIdx.x == 0) __threadfence_system();
 }
 
 
@@ -662,6 +680,13 @@ struct PrePost {
   int Hq, S, D;
   int64_t rows;
   float scale;
+  // push: dq rows go to the token owner's packed gradient (global head rank*Hq + h) and
+  // the last CTA publishes the call's arrival (flags.cuh)
+  int push, P, rank, s_loc;
+  int64_t dst_off, d_sb, d_ss, d_sh;
+  char* peer_base[AUTOSP_MAX_WORLD];
+  uint32_t* peer_flags[AUTOSP_MAX_WORLD];
+  uint32_t epoch, check;
 };
 
 // delta[row] = sum_d dO*O ; nlse2[row] = -lse[row] * log2(e) ; dqacc[row, :] = 0.
@@ -709,20 +734,29 @@ __global__ void bwd_post_kernel(const __grid_constant__ PrePost a) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t row = gid / lpr;
   const int sub = (int)(gid % lpr);
-  if (row >= a.rows) return;
-  const int64_t bh = row / a.S;
-  const int q = (int)(row % a.S);
-  const int h = (int)(bh % a.Hq);
-  const int64_t bi = bh / a.Hq;
-  const float4* src = reinterpret_cast<const float4*>(a.dqacc + row * a.D + sub * 8);
-  const float4 x = src[0], y = src[1];
-  uint4 v;
-  v.x = pack_bf16(x.x * a.scale, x.y * a.scale);
-  v.y = pack_bf16(x.z * a.scale, x.w * a.scale);
-  v.z = pack_bf16(y.x * a.scale, y.y * a.scale);
-  v.w = pack_bf16(y.z * a.scale, y.w * a.scale);
-  *reinterpret_cast<uint4*>(a.dq + bi * a.dq_sb + h * a.dq_sh + (int64_t)q * a.dq_ss + sub * 8) =
-      v;
+  if (row < a.rows) {
+    const int64_t bh = row / a.S;
+    const int q = (int)(row % a.S);
+    const int h = (int)(bh % a.Hq);
+    const int64_t bi = bh / a.Hq;
+    const float4* src = reinterpret_cast<const float4*>(a.dqacc + row * a.D + sub * 8);
+    const float4 x = src[0], y = src[1];
+    uint4 v;
+    v.x = pack_bf16(x.x * a.scale, x.y * a.scale);
+    v.y = pack_bf16(x.z * a.scale, x.w * a.scale);
+    v.z = pack_bf16(y.x * a.scale, y.y * a.scale);
+    v.w = pack_bf16(y.z * a.scale, y.w * a.scale);
+    if (a.push) {  // lanes of one row store its D*2 contiguous bytes together
+      const int j = q / a.s_loc;
+      *reinterpret_cast<uint4*>(
+          reinterpret_cast<__nv_bfloat16*>(a.peer_base[j] + a.dst_off) + bi * a.d_sb +
+          (int64_t)(q - j * a.s_loc) * a.d_ss + (int64_t)(a.rank * a.Hq + h) * a.d_sh + sub * 8) = v;
+    } else {
+      *reinterpret_cast<uint4*>(a.dq + bi * a.dq_sb + h * a.dq_sh + (int64_t)q * a.dq_ss +
+                                sub * 8) = v;
+    }
+  }
+  if (a.push) publish_arrival(a.peer_flags, a.P, a.rank, a.epoch, a.check, gridDim.x);
 }
 
 inline bool make_map_f32_3d(CUtensorMap* map, void* ptr, int BH, int S, int D) {
@@ -757,7 +791,8 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
            const autosp_attn_tensor& o, const autosp_attn_tensor& d_o, const float* lse,
            const autosp_attn_tensor& dq, const autosp_attn_tensor& dk,
            const autosp_attn_tensor& dv, void* ws, int B, int Hq, int Hkv, int S, float scale,
-           int causal, const float* delta_in, cudaStream_t stream) {
+           int causal, const float* delta_in, const autosp_push_spec* push,
+           cudaStream_t stream) {
   using C = Cfg<D>;
   float* dqacc = static_cast<float*>(ws);
   float* delta = delta_in ? const_cast<float*>(delta_in) : dqacc + (size_t)B * Hq * S * D;
@@ -779,6 +814,22 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   a.D = D;
   a.rows = (int64_t)B * Hq * S;
   a.scale = scale;
+  if (push) {
+    a.push = 1;
+    a.P = push->world;
+    a.rank = push->rank;
+    a.s_loc = S / push->world;
+    a.dst_off = push->dst_offset;
+    a.d_sb = push->dst_stride_b;
+    a.d_ss = push->dst_stride_s;
+    a.d_sh = push->dst_stride_h;
+    for (int j = 0; j < push->world; ++j) {
+      a.peer_base[j] = static_cast<char*>(push->peer_base[j]);
+      a.peer_flags[j] = push->peer_flags[j];
+    }
+    a.epoch = push->epoch;
+    a.check = autosp_push_check(push, Hq + 2 * Hkv);
+  }
   {
     const int rpw = 32 / (D / 8);
     const int64_t warps = (a.rows + rpw - 1) / rpw;
@@ -817,6 +868,17 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   p.scale_log2 = scale * 1.4426950408889634f;
   p.causal = causal;
   p.n_ktiles = (S + BK - 1) / BK;
+  if (push) {
+    p.push = 1;
+    p.P = a.P;
+    p.rank = a.rank;
+    p.s_loc = a.s_loc;
+    p.dst_off = a.dst_off;
+    p.d_sb = a.d_sb;
+    p.d_ss = a.d_ss;
+    p.d_sh = a.d_sh;
+    for (int j = 0; j < a.P; ++j) p.peer_base[j] = a.peer_base[j];
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -846,7 +908,10 @@ static int attn_bwd_impl(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn
                          autosp_attn_tensor o, const float* delta, autosp_attn_tensor d_o,
                          const float* lse, autosp_attn_tensor dq, autosp_attn_tensor dk,
                          autosp_attn_tensor dv, void* workspace, int b, int hq, int hkv, int s,
-                         int d, float scale, int causal, void* stream);
+                         int d, float scale, int causal, const autosp_push_spec* push,
+                         void* stream);
+int autosp_internal_handshake(uint32_t* const* flags, int world, int rank, uint32_t epoch,
+                              cudaStream_t stream);
 
 extern "C" int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
                                autosp_attn_tensor o, autosp_attn_tensor d_o, const float* lse,
@@ -856,7 +921,7 @@ extern "C" int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autos
   int rc;
   if ((rc = autosp_check_attn_tensor(o, "o"))) return rc;
   return attn_bwd_impl(q, k, v, o, nullptr, d_o, lse, dq, dk, dv, workspace, b, hq, hkv, s, d,
-                       scale, causal, stream);
+                       scale, causal, nullptr, stream);
 }
 
 extern "C" int autosp_attn_bwd_delta(autosp_attn_tensor q, autosp_attn_tensor k,
@@ -871,14 +936,60 @@ extern "C" int autosp_attn_bwd_delta(autosp_attn_tensor q, autosp_attn_tensor k,
     return AUTOSP_ERR_VALIDATION;
   }
   return attn_bwd_impl(q, k, v, q /* unused */, delta, d_o, lse, dq, dk, dv, workspace, b, hq,
-                       hkv, s, d, scale, causal, stream);
+                       hkv, s, d, scale, causal, nullptr, stream);
+}
+
+extern "C" int autosp_attn_bwd_push(autosp_attn_tensor q, autosp_attn_tensor k,
+                                    autosp_attn_tensor v, const float* delta,
+                                    autosp_attn_tensor d_o, const float* lse, void* workspace,
+                                    int b, int hq, int hkv, int s, int d, float scale,
+                                    int causal, const autosp_push_spec* push, void* stream) {
+  if (!delta || (reinterpret_cast<uintptr_t>(delta) & 15)) {
+    autosp_set_error("attn_bwd_push: delta must be non-null and 16-byte aligned");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (!push || push->world < 1 || push->world > AUTOSP_MAX_WORLD || push->rank < 0 ||
+      push->rank >= push->world || !push->peer_base || !push->peer_flags) {
+    autosp_set_error("attn_bwd_push: bad push spec");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (s % push->world) {
+    autosp_set_error("attn_bwd_push: sequence %d not divisible by world size %d", s,
+                     push->world);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  if (push->dst_offset % 16 || push->dst_stride_b % 8 || push->dst_stride_s % 8 ||
+      push->dst_stride_h % 8 || push->dst_stride_h < d) {
+    autosp_set_error("attn_bwd_push: destination offset/strides must be 16-byte multiples");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  for (int j = 0; j < push->world; ++j)
+    if (!push->peer_base[j] || !push->peer_flags[j] ||
+        (reinterpret_cast<uintptr_t>(push->peer_base[j]) & 15)) {
+      autosp_set_error("attn_bwd_push: peer %d base/flags null or misaligned", j);
+      return AUTOSP_ERR_VALIDATION;
+    }
+  autosp_attn_tensor none{};
+  none.ptr = q.ptr;  // dq/dk/dv are never written locally (validated shape-only)
+  none.stride_b = q.stride_b; none.stride_h = q.stride_h; none.stride_s = q.stride_s;
+  if (push->world > 1) {
+    int rc = autosp_internal_handshake(push->peer_flags, push->world, push->rank, push->epoch,
+                                       static_cast<cudaStream_t>(stream));
+    if (rc) {
+      autosp_set_error("attn_bwd_push: handshake launch failed");
+      return rc;
+    }
+  }
+  return attn_bwd_impl(q, k, v, q /* unused */, delta, d_o, lse, none, none, none, workspace, b,
+                       hq, hkv, s, d, scale, causal, push, stream);
 }
 
 static int attn_bwd_impl(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
                          autosp_attn_tensor o, const float* delta, autosp_attn_tensor d_o,
                          const float* lse, autosp_attn_tensor dq, autosp_attn_tensor dk,
                          autosp_attn_tensor dv, void* workspace, int b, int hq, int hkv, int s,
-                         int d, float scale, int causal, void* stream) {
+                         int d, float scale, int causal, const autosp_push_spec* push,
+                         void* stream) {
   if (b < 1 || hq < 1 || hkv < 1 || s < 1 || hq % hkv) {
     autosp_set_error("attn_bwd: bad shape b=%d hq=%d hkv=%d s=%d", b, hq, hkv, s);
     return AUTOSP_ERR_VALIDATION;
@@ -897,13 +1008,13 @@ static int attn_bwd_impl(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn
   switch (d) {
     case 32:
       return autosp::bwd::launch<32>(q, k, v, o, d_o, lse, dq, dk, dv, workspace, b, hq, hkv, s,
-                                     scale, causal, delta, st);
+                                     scale, causal, delta, push, st);
     case 64:
       return autosp::bwd::launch<64>(q, k, v, o, d_o, lse, dq, dk, dv, workspace, b, hq, hkv, s,
-                                     scale, causal, delta, st);
+                                     scale, causal, delta, push, st);
     case 128:
       return autosp::bwd::launch<128>(q, k, v, o, d_o, lse, dq, dk, dv, workspace, b, hq, hkv, s,
-                                      scale, causal, delta, st);
+                                      scale, causal, delta, push, st);
     default:
       autosp_set_error("attn_bwd: head_dim %d unsupported (32, 64, 128)", d);
       return AUTOSP_ERR_UNSUPPORTED;

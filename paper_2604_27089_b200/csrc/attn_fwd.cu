@@ -545,44 +545,60 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
       mbar_wait(o_done + i, (n - 1) & 1);
       tc_fence_after();
       const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
-      __nv_bfloat16* orow = p.o + (int64_t)batch * p.o_sb + (int64_t)head * p.o_sh +
-                            (int64_t)qi * p.o_ss;
-      // fused K2: the same row goes to the rank owning token qi (token-major, global head
-      // rank * Hq + head), written while the other tiles of this CTA are still computing
-      uint4* prow = nullptr;
-      if (p.push && qi < p.S) {
-        const int j = qi / p.s_loc;
-        prow = reinterpret_cast<uint4*>(
-            p.peer_base[j] + p.dst_off +
-            ((int64_t)batch * p.d_sb + (int64_t)(qi - j * p.s_loc) * p.d_ss +
-             (int64_t)(p.rank * p.Hq + head) * p.d_sh) * 2);
-      }
+      // O rows leave through shared memory: every MMA of tile i is complete (o_done), so
+      // the Q_i tile is free and becomes this warp's staging area [32 rows x D bf16]
+      // (16-byte units XOR-swizzled by row: conflict-free both ways).  The warp then
+      // stores 32 / VPR whole rows per instruction -- row-contiguous 16-byte vectors,
+      // full 128-byte lines -- instead of one 16-byte piece of 32 scattered rows: the
+      // pattern NVLink (fused K2 push into the token owners' receive regions, global
+      // head rank * Hq + head, token-major) and HBM both want.
+      constexpr int ROWB = D * 2;
+      constexpr int VPR = ROWB / 16;  // 16-byte units per row
+      constexpr int RPI = 32 / VPR;   // rows per warp store instruction
+      uint8_t* stage = smem + C::Q_OFF + i * C::TILE_BYTES + quarter * 32 * ROWB;
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t orr[32];
         tmem_ld32(o_addr + c, orr);
         tmem_wait_ld();
-        if (qi < p.S) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + c);
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            uint4 v;
-            v.x = pack_bf16(__uint_as_float(orr[8 * t + 0]) * inv_l,
-                            __uint_as_float(orr[8 * t + 1]) * inv_l);
-            v.y = pack_bf16(__uint_as_float(orr[8 * t + 2]) * inv_l,
-                            __uint_as_float(orr[8 * t + 3]) * inv_l);
-            v.z = pack_bf16(__uint_as_float(orr[8 * t + 4]) * inv_l,
-                            __uint_as_float(orr[8 * t + 5]) * inv_l);
-            v.w = pack_bf16(__uint_as_float(orr[8 * t + 6]) * inv_l,
-                            __uint_as_float(orr[8 * t + 7]) * inv_l);
-            if (p.o) dst[t] = v;  // (push without a local copy: o == nullptr)
-            if (prow) prow[c / 8 + t] = v;
-          }
+        for (int t = 0; t < 4; ++t) {
+          uint4 v;
+          v.x = pack_bf16(__uint_as_float(orr[8 * t + 0]) * inv_l,
+                          __uint_as_float(orr[8 * t + 1]) * inv_l);
+          v.y = pack_bf16(__uint_as_float(orr[8 * t + 2]) * inv_l,
+                          __uint_as_float(orr[8 * t + 3]) * inv_l);
+          v.z = pack_bf16(__uint_as_float(orr[8 * t + 4]) * inv_l,
+                          __uint_as_float(orr[8 * t + 5]) * inv_l);
+          v.w = pack_bf16(__uint_as_float(orr[8 * t + 6]) * inv_l,
+                          __uint_as_float(orr[8 * t + 7]) * inv_l);
+          const int u = c / 8 + t;
+          sts128(stage + lane * ROWB + ((u ^ ((lane & 7) & (VPR - 1))) << 4), v);
         }
       }
       if (qi < p.S)
         p.lse[((int64_t)batch * p.Hq + head) * p.S + qi] =
             (m + __log2f(l)) * 0.69314718055994531f;
+      __syncwarp();
+      const int u = lane % VPR;
+#pragma unroll
+      for (int it = 0; it < 32 / RPI; ++it) {
+        const int r = it * RPI + lane / VPR;  // row within this warp's 32
+        const int qr = q0 + i * BM + quarter * 32 + r;
+        if (qr < p.S) {
+          const uint4 v = lds128u(stage + r * ROWB + ((u ^ ((r & 7) & (VPR - 1))) << 4));
+          if (p.o)  // (push without a local copy: o == nullptr)
+            reinterpret_cast<uint4*>(p.o + (int64_t)batch * p.o_sb + (int64_t)head * p.o_sh +
+                                     (int64_t)qr * p.o_ss)[u] = v;
+          if (p.push) {
+            const int jr = qr / p.s_loc;
+            reinterpret_cast<uint4*>(
+                p.peer_base[jr] + p.dst_off +
+                ((int64_t)batch * p.d_sb + (int64_t)(qr - jr * p.s_loc) * p.d_ss +
+                 (int64_t)(p.rank * p.Hq + head) * p.d_sh) * 2)[u] = v;
+          }
+        }
+      }
     }
   }
   tc_fence_before();

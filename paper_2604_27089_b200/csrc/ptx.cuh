@@ -53,6 +53,13 @@ AUTOSP_DEV void sts128(const void* p, uint4 v) {
                "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
 }
+AUTOSP_DEV uint4 lds128u(const void* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p)) : "memory");
+  return v;
+}
 AUTOSP_DEV float4 lds128(const void* p) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"

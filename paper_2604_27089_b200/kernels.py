@@ -29,11 +29,12 @@ class LaunchLog:
         self.launches = 0
         self.events: dict[str, list] = {}
         self.flops: dict[str, float] = {}
+        self.bytes: dict[str, float] = {}
 
     def reset(self, timing: bool = False):
         self.enabled, self.timing = True, timing
         self.launches = 0
-        self.events, self.flops = {}, {}
+        self.events, self.flops, self.bytes = {}, {}, {}
 
     def begin(self, name: str):
         if not (self.enabled and self.timing):
@@ -42,7 +43,7 @@ class LaunchLog:
         e.record()
         return e
 
-    def end(self, name: str, start, n_kernels: int, flops: float = 0.0):
+    def end(self, name: str, start, n_kernels: int, flops: float = 0.0, nbytes: float = 0.0):
         if self.enabled:
             self.launches += n_kernels
         if start is not None:
@@ -50,12 +51,14 @@ class LaunchLog:
             e.record()
             self.events.setdefault(name, []).append((start, e))
             self.flops[name] = self.flops.get(name, 0.0) + flops
+            self.bytes[name] = self.bytes.get(name, 0.0) + nbytes
 
     def summary(self) -> dict:
         out = {}
         for name, pairs in self.events.items():
             ms = sum(a.elapsed_time(b) for a, b in pairs)
-            out[name] = {"calls": len(pairs), "ms": ms, "flops": self.flops.get(name, 0.0)}
+            out[name] = {"calls": len(pairs), "ms": ms, "flops": self.flops.get(name, 0.0),
+                         "bytes": self.bytes.get(name, 0.0)}
         return out
 
 
@@ -167,6 +170,35 @@ def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = Non
     return dq, dk, dv
 
 
+def attn_bwd_push(q, k, v, do, lse, delta, scale: float, causal: bool, world: int, rank: int,
+                  dst_offset: int, dst_strides: tuple[int, int, int], peer_base: list[int],
+                  peer_flags: list[int], epoch: int) -> int:
+    """K4 fused with the head->seq all-to-all of its gradients (autosp_attn_bwd_push): no
+    local dq/dk/dv; every row lands in the token owner's packed [b, s/P, H3, d] QKV
+    gradient (dst_strides = its (b, s, h) element strides).  Returns the check word."""
+    lib = _lib.load()
+    b, hq, s, d = q.shape
+    hkv = k.shape[1]
+    if lse.dtype != torch.float32 or not lse.is_contiguous() or \
+            delta.dtype != torch.float32 or not delta.is_contiguous() or \
+            tuple(delta.shape) != (b, hq, s):
+        raise ValidationError("attn_bwd_push: lse / delta must be contiguous fp32 [b, hq, s]")
+    ws = torch.empty(lib.autosp_attn_bwd_workspace_bytes(b, hq, s, d), dtype=torch.uint8,
+                     device=q.device)
+    pb = (C.c_void_p * world)(*peer_base)
+    pf = (C.c_void_p * world)(*peer_flags)
+    spec = _lib.PushSpec(world, rank, dst_offset, dst_strides[0], dst_strides[1], dst_strides[2],
+                         C.cast(pb, C.c_void_p), C.cast(pf, C.c_void_p), epoch & 0xFFFFFFFF)
+    ev = LOG.begin("attn_bwd")
+    rc = lib.autosp_attn_bwd_push(_attn_tensor(q, "q"), _attn_tensor(k, "k"), _attn_tensor(v, "v"),
+                                  delta.data_ptr(), _attn_tensor(do, "do"), lse.data_ptr(),
+                                  ws.data_ptr(), b, hq, hkv, s, d, float(scale), int(causal),
+                                  C.byref(spec), _stream())
+    _lib.check(rc, "attn_bwd_push")
+    LOG.end("attn_bwd", ev, 4 if world > 1 else 3, 2.5 * causal_attn_flops(b, hq, s, d, causal))
+    return int(lib.autosp_push_check(C.byref(spec), hq + 2 * hkv))
+
+
 # ----------------------------------------------------------------------------- all-to-all
 def a2a_tensor_desc(src: torch.Tensor, heads: int, dst_offset: int,
                     dst_strides: tuple[int, int, int], rope: bool = False) -> _lib.A2ATensor:
@@ -198,7 +230,9 @@ def a2a_launch(direction: int, descs: list, b: int, s_global: int, d: int, elem_
                                  rank, pb, pf, epoch & 0xFFFFFFFF, pos.data_ptr(), float(theta),
                                  _stream())
     _lib.check(rc, "a2a")
-    LOG.end("a2a", ev, 2 if world > 1 else 1)
+    # bytes sent to peers = (P-1)/P of this rank's local share of every tensor
+    local = sum(b * s_global * dsc.heads * d * elem_bytes for dsc in descs) // max(world, 1)
+    LOG.end("a2a", ev, 2 if world > 1 else 1, nbytes=local * (world - 1) / max(world, 1))
     return a2a_check(direction, descs)
 
 

@@ -349,12 +349,59 @@ def _uqa_setup(ctx, inputs, output):
     ctx.qkv_shape = tuple(qkv.shape)
 
 
+FUSE_GRAD_A2A = True  # K4's epilogues push dq/dk/dv to the token owners (no separate K1)
+
+
 def _uqa_bwd(ctx, d_otok, *unused):
     pos, qh, kh, vh, o_tok, lse = ctx.saved_tensors
+    if FUSE_GRAD_A2A and qh.shape[-1] in kernels.SUPPORTED_HEAD_DIMS:
+        acc = torch.promote_types(d_otok.dtype, torch.float32)
+        delta_tok = (d_otok.to(acc) * o_tok.to(acc)).sum(-1, keepdim=True)
+        (do,) = all_to_all([d_otok], SEQ_TO_HEAD_DIR, ctx.group)
+        (delta,) = all_to_all([delta_tok], SEQ_TO_HEAD_DIR, ctx.group)
+        dqkv = qkv_attention_grad(do, qh, kh, vh, delta.squeeze(-1), lse, pos, ctx.theta,
+                                  ctx.scale, ctx.group)
+        return dqkv, None, None, None, None, None, None
     dq, dk, dv = ulysses_attention_grad(d_otok, o_tok, qh, kh, vh, lse, ctx.scale, True,
                                         ctx.group)
     dqkv = qkv_grad_gather(dq, dk, dv, pos, ctx.theta, ctx.group)
     return dqkv, None, None, None, None, None, None
+
+
+@torch.library.custom_op("autosp::qkv_attention_grad", mutates_args=(), device_types="cuda")
+def qkv_attention_grad(do: torch.Tensor, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                       delta: torch.Tensor, lse: torch.Tensor, pos: torch.Tensor, theta: float,
+                       scale: float, group: str) -> torch.Tensor:
+    """The attention backward (K4) with the head->seq all-to-all of its gradients fused
+    into its epilogues (autodiff.py:252-262 + the attention recipes :156-214): dK/dV rows
+    leave K4's epilogue and dQ rows its finalisation straight for the token owners'
+    packed [b, s/P, hq+2hkv, d] QKV gradient (no local dq/dk/dv, no K1 launch); then the
+    inverse RoPE of the q/k heads in place (one launch)."""
+    st = sp_dist.lookup(group)
+    P, pool = st.world, st.pool
+    b, hql, S, d = q.shape
+    hkvl = k.shape[1]
+    hq, hkv, sl = hql * P, hkvl * P, S // P
+    H3 = hq + 2 * hkv
+    slab = pool.alloc(b * sl * H3 * d * q.element_size())
+    dqkv = slab.view.view(q.dtype).as_strided((b, sl, H3, d), (sl * H3 * d, H3 * d, d, 1))
+    epoch = pool.next_epoch()
+    chk = kernels.attn_bwd_push(q, k, v, do, lse, delta.contiguous(), scale, True, P, st.rank,
+                                slab.offset, (sl * H3 * d, H3 * d, d), slab.regions,
+                                pool.flag_ptrs, epoch)
+    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, chk)
+    kernels.rope_segments([(dqkv[:, :, :hq], dqkv[:, :, :hq], True),
+                           (dqkv[:, :, hq:hq + hkv], dqkv[:, :, hq:hq + hkv], True)],
+                          pos, theta, inverse=True)
+    return dqkv
+
+
+@qkv_attention_grad.register_fake
+def _qkv_attention_grad_fake(do, q, k, v, delta, lse, pos, theta, scale, group):
+    P = sp_dist.lookup(group).world
+    b, hql, S, d = q.shape
+    H3 = (hql + 2 * k.shape[1]) * P
+    return q.new_empty((b, S // P, H3, d))
 
 
 ulysses_qkv_attention.register_autograd(_uqa_bwd, setup_context=_uqa_setup)

@@ -63,7 +63,8 @@ def is_autosp_collective(n: fx.Node) -> bool:
     return n.op == "call_function" and _opname(n) in ("autosp::all_to_all",
                                                       "autosp::attention_a2a",
                                                       "autosp::ulysses_qkv_attention",
-                                                      "autosp::qkv_grad_gather")
+                                                      "autosp::qkv_grad_gather",
+                                                      "autosp::qkv_attention_grad")
 
 
 def is_autosp_attention(n: fx.Node) -> bool:

@@ -102,14 +102,11 @@ class ShardedAdamW:
 
     # -------------------------------------------------------------- collectives
     def _reduce_scatter(self, flat: torch.Tensor, out: torch.Tensor) -> None:
+        # (the same collectives on NCCL and on gloo, so the CPU tests run this code)
         if self.P == 1:
             out.copy_(flat)
-        elif tdist.get_backend(self.group) == "nccl":
+        else:
             tdist.reduce_scatter_tensor(out, flat, group=self.group)
-        else:  # gloo (CPU tests): all-reduce, keep my slice
-            tdist.all_reduce(flat, group=self.group)
-            n = out.numel()
-            out.copy_(flat[self.rank * n:(self.rank + 1) * n])
         if self.dp is not None:
             tdist.all_reduce(out, group=self.dp)
             out /= tdist.get_world_size(self.dp)
@@ -117,10 +114,8 @@ class ShardedAdamW:
     def _all_gather(self, shard: torch.Tensor, flat: torch.Tensor) -> None:
         if self.P == 1:
             flat.copy_(shard)
-        elif tdist.get_backend(self.group) == "nccl":
-            tdist.all_gather_into_tensor(flat, shard, group=self.group)
         else:
-            tdist.all_gather(list(flat.chunk(self.P)), shard, group=self.group)
+            tdist.all_gather_into_tensor(flat, shard, group=self.group)
 
     # -------------------------------------------------------------- optimizer API
     @torch.no_grad()

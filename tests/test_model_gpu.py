@@ -151,10 +151,17 @@ def _qkv_rank(st, qkv_full, pos_full, dout_full, results, r, P, hq, hkv):
         scale = 1.0 / qkv.shape[-1] ** 0.5
         o, qh, kh, vh, lse = ops.ulysses_qkv_attention(qkv, pos, 500000.0, hq, hkv, scale,
                                                        st.name)
-        dq, dk, dv = ops.ulysses_attention_grad(dout_full[:, :, r * sl:(r + 1) * sl], o, qh, kh,
-                                                vh, lse, scale, True, st.name)
+        d_otok = dout_full[:, :, r * sl:(r + 1) * sl]
+        dq, dk, dv = ops.ulysses_attention_grad(d_otok, o, qh, kh, vh, lse, scale, True,
+                                                st.name)
         dqkv = ops.qkv_grad_gather(dq, dk, dv, pos, 500000.0, st.name)
-        results[r] = (o.clone(), dqkv.clone())
+        # the same backward with the gradient reshard fused into K4's epilogues
+        delta_tok = (d_otok.float() * o.float()).sum(-1, keepdim=True)
+        (do,) = ops.all_to_all([d_otok], ops.SEQ_TO_HEAD_DIR, st.name)
+        (delta,) = ops.all_to_all([delta_tok], ops.SEQ_TO_HEAD_DIR, st.name)
+        dqkv_f = ops.qkv_attention_grad(do, qh, kh, vh, delta.squeeze(-1), lse, pos, 500000.0,
+                                        scale, st.name)
+        results[r] = (o.clone(), dqkv.clone(), dqkv_f.clone())
     stream.synchronize()
 
 
@@ -192,6 +199,13 @@ def test_rope_fused_reshard_block_virtual_ranks(P, hq, hkv, d):
     assert torch.equal(o, o_ref)  # RoPE math shared (rope.cuh), reshard bit-exact
     err = float((gq.float() - ref_in.grad.float()).abs().max() / ref_in.grad.float().abs().max())
     assert err < 1e-2, err
+    # K4 pushing its own gradients (autosp_attn_bwd_push): dK / dV bit-exact against the
+    # unfused K4 + K1 path (both accumulate in TMEM in the same order); dQ within the
+    # order-dependent rounding of the fp32 reduce-add accumulator
+    gf = torch.cat([x[2] for x in results], dim=1)
+    assert torch.equal(gf[:, :, hq:], gq[:, :, hq:])
+    errf = float((gf.float() - ref_in.grad.float()).abs().max() / ref_in.grad.float().abs().max())
+    assert errf < 1e-2, errf
 
 
 def test_sp_ac_plan_on_the_cuda_graph():

@@ -56,7 +56,11 @@ def _worker(rank, world, port, mode, q):
         loss.backward()
         params = list(model.parameters())
         if world > 1:
-            autosp.dist.reduce_gradients(params, st)
+            # Listing 1's loop: no explicit reduction -- the compiled backward all-reduced
+            # the SP-partial gradients (grad_sync.py; lm_head, used outside the compiled
+            # graph by the eager loss, through its post-accumulate hook)
+            from paper_2604_27089_b200 import grad_sync
+            assert not grad_sync.consume(params)
             lt = torch.tensor([float(loss)])
             tdist.all_reduce(lt)
             total = float(lt)

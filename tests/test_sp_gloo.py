@@ -91,9 +91,15 @@ def _worker(rank, world, port, dims_t, seed, passes, mode, q, graph_breaks=False
         autosp.dist.reduce_gradients(list(model.named_reference_params().values()), st)
         red = {k: p.grad.detach().numpy() for k, p in model.named_reference_params().items()}
         info = compiler.LAST_INFO.get("auto_sp")
-        from paper_2604_27089_b200 import grad_sync
-        plan = dict(sp_ac.LAST_PLAN, grad_sync=dict(grad_sync.LAST),
-                    in_graph=sum(bool(getattr(p, grad_sync.IN_GRAPH, False))
+        from paper_2604_27089_b200 import grad_sync as gsync
+        if grad_sync:  # ZeRO-1 on top of the in-graph reduction: slice, AdamW, all-gather
+            from paper_2604_27089_b200.zero import ShardedAdamW
+            opt = ShardedAdamW(model.parameters(), st, bucket_bytes=4096, lr=1e-2)
+            opt.step()
+            red = dict(red, **{"after_adamw/" + k: p.detach().numpy().copy()
+                               for k, p in model.named_reference_params().items()})
+        plan = dict(sp_ac.LAST_PLAN, grad_sync=dict(gsync.LAST),
+                    in_graph=sum(bool(getattr(p, gsync.IN_GRAPH, False))
                                  for p in model.parameters()))
         q.put((rank, hidden.detach().numpy(), local_loss, red,
                {k: v.numpy() for k, v in grads.items()}, plan,
@@ -240,3 +246,9 @@ def test_in_graph_grad_sync_listing1_loop(world, sp):
         gs = plan["grad_sync"]
         assert plan["in_graph"] == len(want) == gs["params"]
         assert gs["buckets"] > 1 and gs["start_positions"][0] < 0.8 * gs["nodes"]
+        # ZeRO-1 step on the already-reduced gradients == AdamW on the expected gradients
+        for k in want:
+            p = torch.nn.Parameter(torch.from_numpy(np.asarray(params[k], np.float64).copy()))
+            p.grad = torch.from_numpy(np.asarray(want[k], np.float64).copy())
+            torch.optim.AdamW([p], lr=1e-2).step()
+            assert orc.max_rel_err(red["after_adamw/" + k], p.detach().numpy()) <= 1e-9, k
