@@ -212,6 +212,26 @@ AUTOSP_API int autosp_attn_bwd_push(autosp_attn_tensor q, autosp_attn_tensor k,
                     const float* lse, void* workspace, int b, int hq, int hkv, int s, int d,
                     float scale, int causal, const autosp_push_spec* push, void* stream);
 
+/* K0: the packed QKV projection Y = X W^T (X [M, K] bf16 with row stride ldx -- M = b * s_loc
+ * tokens of this rank; W [N, K] with N = (hq + 2hkv) * d, the nn.Linear weight; fp32
+ * accumulation in TMEM; tcgen05 + TMA, persistent) with the seq->head all-to-all folded
+ * into its epilogue (replaces the projection Linear + AllToAll of transformer.py:66-72 /
+ * executor.py:203-230 in the reference's lowered graph):
+ *   dst3 != NULL: every (token, head) row is rounded to bf16, RoPE-rotated when it is a q
+ *     or k head and rope != 0 (pos[t] of this rank's token t, theta; bit-identical to K1's
+ *     rotation), and stored into the owning rank's receive region at dst3[i].dst_offset as
+ *     the contiguous head-major [b, h/P, s_loc * world, d] operand (i = q, k, v; heads =
+ *     hq / hkv / hkv GLOBAL head counts).  Ready handshake first; arrival published at the
+ *     end; the receiver waits with autosp_a2a_wait(check = autosp_a2a_check(SEQ_TO_HEAD,
+ *     dst3, 3)).
+ *   dst3 == NULL: a plain GEMM into the local row-major Y (ldy >= N); rope must be 0.
+ * Needs M % 128 == 0, s_loc % 128 == 0, N % 256 == 0, K % 64 == 0 (else status 3). */
+AUTOSP_API int autosp_qkv_gemm(const void* x, int64_t ldx, const void* w, int64_t ldw, int M,
+                    int K, int hq, int hkv, int d, int s_loc, const float* pos, float theta,
+                    int rope, void* y, int64_t ldy, const autosp_a2a_tensor* dst3, int world,
+                    int rank, void* const* peer_base, uint32_t* const* peer_flags,
+                    uint32_t epoch, void* stream);
+
 /* ------------------------------------------------------------------ fused elementwise
  * HBM-bound bf16 kernels for the layer around the Ulysses path (fp32 math):
  *   swiglu: out[r, :] = silu(gu[r, :F]) * gu[r, F:2F]        (reference silu executor.py:33-34,

@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "libautosp.so"
-SOURCES = ["capi.cu", "a2a.cu", "attn_fwd.cu", "attn_bwd.cu", "fused.cu"]
+SOURCES = ["capi.cu", "a2a.cu", "attn_fwd.cu", "attn_bwd.cu", "fused.cu", "qkv_gemm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

@@ -70,6 +70,7 @@ _POSITIONS = (torch.ops.autosp.positions.default, torch.ops.autosp.positions)
 INDEX_OPS = (*_POSITIONS, torch.arange)
 _LOWERED = (ops.ulysses_attention, ops.sdpa, ops.ulysses_qkv_block)
 FUSE_QKV_ROPE = True  # fold autosp::qkv_rope (RoPE + split + transpose) into the reshard
+FUSE_QKV_PROJ = True  # and the projection GEMM in front of it (K0 pushes from its epilogue)
 
 
 def _transposed_item(node, idx):
@@ -103,6 +104,31 @@ def _match_qkv_rope(q, k, v):
     return r
 
 
+def _match_qkv_proj(rq):
+    """qkv = view(matmul(h, t(w)), b, s, H3, d) feeding the matched qkv_rope, every link
+    used once, within K0's tile constraints -> (view, matmul, t, h, w) else None."""
+    qkv = rq.args[0]
+    if not (isinstance(qkv, fx.Node) and qkv.op == "call_method" and
+            qkv.target in ("view", "reshape") and len(qkv.users) == 1):
+        return None
+    mm = qkv.args[0]
+    if not (isinstance(mm, fx.Node) and mm.op == "call_function" and
+            mm.target in (operator.matmul, torch.matmul) and len(mm.users) == 1):
+        return None
+    h, tt = mm.args[:2]
+    if not (isinstance(tt, fx.Node) and tt.op == "call_method" and tt.target == "t" and
+            len(tt.users) == 1):
+        return None
+    w = tt.args[0]
+    hv, wv = _val(h), _val(w)
+    if hv is None or wv is None or hv.dim() != 3 or wv.dim() != 2 or \
+            hv.dtype != torch.bfloat16 or wv.dtype != torch.bfloat16:
+        return None
+    if not ops.qkv_proj_fusable(tuple(hv.shape), tuple(wv.shape), rq.args[3], rq.args[4]):
+        return None
+    return qkv, mm, tt, h, w
+
+
 @dataclass
 class SPDims:  # reference infer_dims (sp_pass.py:102-123), on the local shard
     b: int
@@ -117,6 +143,7 @@ class SPGraphInfo:
     world_size: int
     dims: SPDims | None  # None: a Dynamo subgraph without attention (graph break)
     provenance: dict[str, RewriteReason] = field(default_factory=dict)
+    fused_qkv_proj: int = 0  # attention blocks whose projection GEMM pushes (K0)
 
 
 def _val(n):
@@ -201,8 +228,16 @@ def auto_sp(gm: fx.GraphModule, example_inputs, st: SPState) -> tuple[fx.GraphMo
             if hq % P or hkv % P:
                 raise ValidationError(f"head count {hq}/{hkv} not divisible by world size {P}")
             rq = _match_qkv_rope(q, k, v) if (P > 1 and FUSE_QKV_ROPE) else None
+            proj = _match_qkv_proj(rq) if (rq is not None and FUSE_QKV_PROJ) else None
             with g.inserting_before(n):
-                if rq is not None:
+                if proj is not None:
+                    _, pos, theta, nq, nkv = rq.args[:5]
+                    new = g.call_function(ops.ulysses_qkv_proj_block,
+                                          (proj[3], proj[4], pos, theta, nq, nkv),
+                                          {"group": st.name, "scale": scale})
+                    info.provenance[new.name] = RewriteReason.INSERTED_COLLECTIVE
+                    info.fused_qkv_proj += 1
+                elif rq is not None:
                     qkv, pos, theta, nq, nkv = rq.args[:5]
                     new = g.call_function(ops.ulysses_qkv_block, (qkv, pos, theta, nq, nkv),
                                           {"group": st.name, "scale": scale})
@@ -223,6 +258,9 @@ def auto_sp(gm: fx.GraphModule, example_inputs, st: SPState) -> tuple[fx.GraphMo
                     g.erase_node(x)
                     g.erase_node(it)
                 g.erase_node(rq)
+            if proj is not None:  # and the projection feeding it (view, matmul, t)
+                for x in proj[:3]:
+                    g.erase_node(x)
         elif n.target in INDEX_OPS and P > 1:
             if n.target in _POSITIONS:
                 length = n.args[0]

@@ -459,8 +459,10 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
         m = m_cand;
       }
       // PV_i(j-1) must be complete before O is rescaled and (SEP_P) before P_i is
-      // overwritten; it was issued a whole softmax ago, so this rarely waits.
-      if (j > 0 && (C::SEP_P || __any_sync(0xffffffffu, rescale))) {
+      // overwritten; it was issued a whole softmax ago, so this rarely waits.  (Without
+      // SEP_P it is already implied by s_full(j) -- in-order pipe -- but every phase of
+      // o_done is observed, which keeps the parity waits trivially sound.)
+      if (j > 0) {
         mbar_wait(o_done + i, (j - 1) & 1);
         tc_fence_after();
       }

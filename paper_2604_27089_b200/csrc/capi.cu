@@ -128,10 +128,11 @@ int autosp_preload_a2a();
 int autosp_preload_fwd();
 int autosp_preload_bwd();
 int autosp_preload_fused();
+int autosp_preload_gemm();
 
 extern "C" int autosp_preload_kernels(void) {
   int rc = autosp_preload_a2a() | autosp_preload_fwd() | autosp_preload_bwd() |
-           autosp_preload_fused();
+           autosp_preload_fused() | autosp_preload_gemm();
   if (rc) {
     autosp_set_error("preloading kernels failed: %s", cudaGetErrorString(cudaGetLastError()));
     return AUTOSP_ERR_CUDA;

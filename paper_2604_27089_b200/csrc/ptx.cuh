@@ -34,6 +34,9 @@ AUTOSP_DEV uint64_t globaltimer() {
 AUTOSP_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+AUTOSP_DEV void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 template <uint32_t kRegs>
 AUTOSP_DEV void reg_alloc() {  // whole warpgroup
@@ -109,6 +112,32 @@ AUTOSP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
     if (globaltimer() - t0 > 4000000000ull) {
       printf("autosp: mbarrier wait timed out (block %d,%d,%d thread %d, smem bar 0x%x, parity %u)\n",
+             blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, smem_u32(bar), parity);
+      asm volatile("trap;");
+    }
+  }
+}
+
+// Busy-polling variant (mbarrier.test_wait never suspends the thread): for the single
+// latency-critical issuer warps, which must react to a completed phase immediately.
+AUTOSP_DEV bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+AUTOSP_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  if (mbar_test_wait(bar, parity)) return;
+  uint64_t t0 = globaltimer();
+  uint32_t n = 0;
+  while (!mbar_test_wait(bar, parity)) {
+    if ((++n & 255) == 0 && globaltimer() - t0 > 4000000000ull) {
+      printf("autosp: mbarrier spin timed out (block %d,%d,%d thread %d, smem bar 0x%x, parity %u)\n",
              blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, smem_u32(bar), parity);
       asm volatile("trap;");
     }

@@ -199,6 +199,48 @@ def attn_bwd_push(q, k, v, do, lse, delta, scale: float, causal: bool, world: in
     return int(lib.autosp_push_check(C.byref(spec), hq + 2 * hkv))
 
 
+def qkv_gemm(x: torch.Tensor, w: torch.Tensor, hq: int, hkv: int, s_loc: int,
+             y: torch.Tensor | None = None, pos: torch.Tensor | None = None,
+             theta: float = 0.0, dst3: list | None = None, world: int = 1, rank: int = 0,
+             peer_base: list[int] | None = None, peer_flags: list[int] | None = None,
+             epoch: int = 0) -> torch.Tensor | int:
+    """K0 (autosp_qkv_gemm): x [M, K] bf16 (rows = b * s_loc tokens), w [N, K] with
+    N = (hq + 2hkv) * d.  dst3 None: plain GEMM into y [M, N] (returned).  dst3 = three
+    a2a descriptors (q, k, v destinations, head-major [b, h/P, S, d]): the epilogue rounds,
+    RoPE-rotates q/k rows (pos/theta) and pushes them to their head owners; returns the
+    call's check word (for a2a_wait)."""
+    lib = _lib.load()
+    M, K = x.shape
+    N = w.shape[0]
+    d = N // (hq + 2 * hkv)
+    if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16 or x.stride(1) != 1 or \
+            w.stride(1) != 1 or w.shape[1] != K or N != (hq + 2 * hkv) * d:
+        raise ValidationError("qkv_gemm: bf16 x [M, K] and w [(hq+2hkv)*d, K], rows contiguous")
+    posp = 0
+    if pos is not None:
+        if pos.dtype != torch.float32 or not pos.is_contiguous() or not pos.is_cuda:
+            raise ValidationError("qkv_gemm: positions must be a contiguous CUDA fp32 tensor")
+        posp = pos.data_ptr()
+    ev = LOG.begin("qkv_gemm")
+    if dst3 is None:
+        y = torch.empty((M, N), dtype=torch.bfloat16, device=x.device) if y is None else y
+        rc = lib.autosp_qkv_gemm(x.data_ptr(), x.stride(0), w.data_ptr(), w.stride(0), M, K, hq,
+                                 hkv, d, s_loc, posp or None, float(theta), 0, y.data_ptr(),
+                                 y.stride(0), None, 1, 0, None, None, 0, _stream())
+        _lib.check(rc, "qkv_gemm")
+        LOG.end("qkv_gemm", ev, 1, 2.0 * M * N * K)
+        return y
+    arr = (_lib.A2ATensor * 3)(*dst3)
+    pb = (C.c_void_p * world)(*peer_base)
+    pf = (C.c_void_p * world)(*peer_flags)
+    rc = lib.autosp_qkv_gemm(x.data_ptr(), x.stride(0), w.data_ptr(), w.stride(0), M, K, hq, hkv,
+                             d, s_loc, posp or None, float(theta), int(pos is not None), None, 0,
+                             arr, world, rank, pb, pf, epoch & 0xFFFFFFFF, _stream())
+    _lib.check(rc, "qkv_gemm")
+    LOG.end("qkv_gemm", ev, 2 if world > 1 else 1, 2.0 * M * N * K)
+    return a2a_check(_lib.SEQ_TO_HEAD, list(dst3))
+
+
 # ----------------------------------------------------------------------------- all-to-all
 def a2a_tensor_desc(src: torch.Tensor, heads: int, dst_offset: int,
                     dst_strides: tuple[int, int, int], rope: bool = False) -> _lib.A2ATensor:

@@ -23,7 +23,7 @@ import math
 import torch
 
 from . import dist as sp_dist
-from . import kernels
+from . import _lib, kernels
 from ._lib import HEAD_TO_SEQ, SEQ_TO_HEAD
 from .errors import ValidationError
 
@@ -451,6 +451,106 @@ def ulysses_qkv_block(qkv, pos, theta: float, hq: int, hkv: int, group: str, sca
     """What auto_sp substitutes for qkv_rope -> transpose -> SDPA at P > 1 (bf16)."""
     sc = 1.0 / math.sqrt(qkv.shape[-1]) if scale is None else float(scale)
     return ulysses_qkv_attention(qkv, pos, theta, hq, hkv, sc, group)[0]
+
+
+def qkv_proj_fusable(h_shape, w_shape, hq: int, hkv: int) -> bool:
+    """K0's tile constraints (autosp_qkv_gemm): 128-token tiles of every batch element,
+    256-column output tiles, 64-deep K blocks."""
+    b, sl, K = h_shape
+    N = w_shape[0]
+    d = N // (hq + 2 * hkv)
+    return (sl % 128 == 0 and N % 256 == 0 and K % 64 == 0 and d in (32, 64, 128) and
+            w_shape[1] == K and N == (hq + 2 * hkv) * d)
+
+
+def ulysses_qkv_proj_block(h, w, pos, theta: float, hq: int, hkv: int, group: str, scale=None):
+    """What auto_sp substitutes for h @ wqkv.t() -> qkv_rope -> transpose -> SDPA at P > 1
+    when K0's tile constraints hold: the projection GEMM pushes RoPE'd head-major q/k/v
+    rows to their owners from its epilogue."""
+    d = w.shape[0] // (hq + 2 * hkv)
+    sc = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    return ulysses_qkv_proj_attention(h, w, pos, theta, hq, hkv, sc, group)[0]
+
+
+@torch.library.custom_op("autosp::ulysses_qkv_proj_attention", mutates_args=(),
+                         device_types="cuda")
+def ulysses_qkv_proj_attention(h: torch.Tensor, w: torch.Tensor, pos: torch.Tensor, theta: float,
+                               hq: int, hkv: int, scale: float,
+                               group: str) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor,
+                                                    torch.Tensor, torch.Tensor]:
+    """The Ulysses attention block from the projection INPUT h [b, s/P, K] (sp_pass.py:
+    172-195 with the projection Linear of transformer.py:66-72 in front):
+      K0 (autosp_qkv_gemm): Y = h W^T on the tensor cores, each (token, head) row of the
+         epilogue RoPE-rotated (q/k) and pushed head-major [b, h/P, s, d] into its
+         owner's receive region -- the reshard overlaps the GEMM, and the packed
+         projection output is never written to HBM;
+      K3+K2: causal attention on the local heads, O pushed back to the token owners.
+    Returns (o_tokens, q_heads, k_heads, v_heads, lse) like ulysses_qkv_attention."""
+    st = sp_dist.lookup(group)
+    P, pool = st.world, st.pool
+    b, sl, K = h.shape
+    N = w.shape[0]
+    d = N // (hq + 2 * hkv)
+    S = sl * P
+    if not qkv_proj_fusable(tuple(h.shape), tuple(w.shape), hq, hkv) or hq % P or hkv % P:
+        raise ValidationError(f"ulysses_qkv_proj_attention: shapes {tuple(h.shape)} x "
+                              f"{tuple(w.shape)} ({hq}/{hkv} heads, P={P}) not supported by K0")
+    x2 = h.reshape(b * sl, K)
+    if x2.stride(1) != 1:
+        x2 = x2.contiguous()
+    slab = pool.alloc_many([b * (x // P) * S * d * h.element_size() for x in (hq, hkv, hkv)])
+    outs, dst3 = [], []
+    for x, (off, base) in zip((hq, hkv, hkv), slab.pieces):
+        shape = (b, x // P, S, d)
+        strides = ((x // P) * S * d, S * d, d, 1)
+        outs.append(base.view(h.dtype).as_strided(shape, strides))
+        dst3.append(_lib.A2ATensor(None, 0, 0, 0, off, strides[0], strides[2], strides[1], x, 0))
+    epoch = pool.next_epoch()
+    chk = kernels.qkv_gemm(x2, w, hq, hkv, sl, pos=pos.to(torch.float32).contiguous(),
+                           theta=theta, dst3=dst3, world=P, rank=st.rank,
+                           peer_base=slab.regions, peer_flags=pool.flag_ptrs, epoch=epoch)
+    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, chk)
+    qh, kh, vh = outs
+    o_tok, lse = attention_a2a(qh, kh, vh, scale, True, group)
+    return o_tok, qh, kh, vh, lse
+
+
+@ulysses_qkv_proj_attention.register_fake
+def _uqpa_fake(h, w, pos, theta, hq, hkv, scale, group):
+    P = sp_dist.lookup(group).world
+    b, sl, _ = h.shape
+    d = w.shape[0] // (hq + 2 * hkv)
+    S = sl * P
+    heads = lambda x: h.new_empty_strided((b, x // P, S, d), ((x // P) * S * d, S * d, d, 1))
+    return (h.new_empty_strided((b, hq, sl, d), (sl * hq * d, d, hq * d, 1)), heads(hq),
+            heads(hkv), heads(hkv), h.new_empty((b, hq // P, S), dtype=torch.float32))
+
+
+def _uqpa_setup(ctx, inputs, output):
+    h, w, pos, theta, hq, hkv, scale, group = inputs
+    o_tok, qh, kh, vh, lse = output
+    ctx.save_for_backward(h, w, pos, qh, kh, vh, o_tok, lse)
+    ctx.theta, ctx.hq, ctx.hkv, ctx.scale, ctx.group = theta, hq, hkv, scale, group
+
+
+def _uqpa_bwd(ctx, d_otok, *unused):
+    """dqkv from K4 with its gradient push (qkv_attention_grad), then the projection's
+    two gradient GEMMs (cuBLAS): dh = dqkv W, dW = dqkv^T h."""
+    h, w, pos, qh, kh, vh, o_tok, lse = ctx.saved_tensors
+    acc = torch.promote_types(d_otok.dtype, torch.float32)
+    delta_tok = (d_otok.to(acc) * o_tok.to(acc)).sum(-1, keepdim=True)
+    (do,) = all_to_all([d_otok], SEQ_TO_HEAD_DIR, ctx.group)
+    (delta,) = all_to_all([delta_tok], SEQ_TO_HEAD_DIR, ctx.group)
+    dqkv = qkv_attention_grad(do, qh, kh, vh, delta.squeeze(-1), lse, pos, ctx.theta, ctx.scale,
+                              ctx.group)
+    b, sl, K = h.shape
+    g2 = dqkv.reshape(b * sl, w.shape[0])
+    dh = (g2 @ w).view(b, sl, K)
+    dw = g2.t() @ h.reshape(b * sl, K)
+    return dh, dw, None, None, None, None, None, None
+
+
+ulysses_qkv_proj_attention.register_autograd(_uqpa_bwd, setup_context=_uqpa_setup)
 
 
 FUSE_OUTPUT_A2A = True  # attention epilogue pushes O (K3 + K2 in one kernel)

@@ -63,6 +63,7 @@ def is_autosp_collective(n: fx.Node) -> bool:
     return n.op == "call_function" and _opname(n) in ("autosp::all_to_all",
                                                       "autosp::attention_a2a",
                                                       "autosp::ulysses_qkv_attention",
+                                                      "autosp::ulysses_qkv_proj_attention",
                                                       "autosp::qkv_grad_gather",
                                                       "autosp::qkv_attention_grad")
 
@@ -70,7 +71,8 @@ def is_autosp_collective(n: fx.Node) -> bool:
 def is_autosp_attention(n: fx.Node) -> bool:
     return n.op == "call_function" and _opname(n) in ("autosp::attention",
                                                       "autosp::attention_a2a",
-                                                      "autosp::ulysses_qkv_attention")
+                                                      "autosp::ulysses_qkv_attention",
+                                                      "autosp::ulysses_qkv_proj_attention")
 
 
 def _is_matmul(n: fx.Node) -> bool:

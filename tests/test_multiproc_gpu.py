@@ -68,13 +68,15 @@ def _worker(rank, world, port, mode, q):
             total = float(loss)
         torch.cuda.synchronize()
         grads = {n: p.grad.float().cpu().numpy() for n, p in model.named_parameters()}
+        from paper_2604_27089_b200 import compiler
+        info = compiler.LAST_INFO.get("auto_sp")
         q.put((rank, total, grads, sp_ac.LAST_PLAN.get("fw_collectives"),
-               sp_ac.LAST_PLAN.get("bw_collectives")))
+               sp_ac.LAST_PLAN.get("bw_collectives"), info.fused_qkv_proj if info else 0))
         if world > 1:
             tdist.barrier()
     except Exception:
         import traceback
-        q.put((rank, "ERROR", traceback.format_exc(), None, None))
+        q.put((rank, "ERROR", traceback.format_exc(), None, None, None))
     finally:
         if world > 1 and tdist.is_initialized():
             tdist.destroy_process_group()
@@ -102,8 +104,10 @@ def _run(world, mode):
 def test_two_processes_ipc_match_unsharded(mode):
     ref = _run(1, mode)[0]
     out = _run(2, mode)
-    _, ref_loss, ref_grads, _, _ = ref
-    for rank, loss, grads, n_fw, n_bw in out:
+    _, ref_loss, ref_grads, _, _, _ = ref
+    for rank, loss, grads, n_fw, n_bw, n_proj in out:
+        # the QKV projection GEMM itself pushes RoPE'd head-major rows (K0) in every layer
+        assert n_proj == CFG["layers"], n_proj
         assert abs(loss - ref_loss) / abs(ref_loss) < 1e-3, (loss, ref_loss)
         # forward: ONE collective op per layer (RoPE-fused q/k/v reshard + attention whose
         # epilogue pushes O); backward: dO and delta reshards + packed-gradient gather
