@@ -164,6 +164,16 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_gemm_kernel(const __grid_cons
       const int bi = m / p.s_loc, t = m - bi * p.s_loc;
       const float tp = p.rope ? __ldg(p.pos + t) : 0.f;
       const uint32_t acc = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN;
+      // d <= 64: the token's rotation angles are shared by every q/k head of the tile --
+      // computed once per tile (same rope_sincos calls as K1: bit-identical values)
+      constexpr bool kHoist = D <= 64;
+      float rs[kHoist ? D / 2 : 1], rc[kHoist ? D / 2 : 1];
+      if constexpr (kHoist) {
+        if (p.rope && n0 / D < p.hq + p.hkv) {
+#pragma unroll
+          for (int j = 0; j < D / 2; ++j) rope_sincos(tp, j, D, p.log2_theta, &rs[j], &rc[j]);
+        }
+      }
 #pragma unroll 1
       for (int hh = 0; hh < HPT; ++hh) {
         const int gh = n0 / D + hh;  // head in the packed [hq | hkv | hkv] order
@@ -187,8 +197,12 @@ __global__ void __launch_bounds__(kThreads, 1) qkv_gemm_kernel(const __grid_cons
             const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&v[D / 4 + i]);
             const float2 l2 = __bfloat1622float2(lo), h2 = __bfloat1622float2(hi);
             float s0, c0, s1, c1;
-            rope_sincos(tp, 2 * i, D, p.log2_theta, &s0, &c0);
-            rope_sincos(tp, 2 * i + 1, D, p.log2_theta, &s1, &c1);
+            if constexpr (kHoist) {
+              s0 = rs[2 * i], c0 = rc[2 * i], s1 = rs[2 * i + 1], c1 = rc[2 * i + 1];
+            } else {
+              rope_sincos(tp, 2 * i, D, p.log2_theta, &s0, &c0);
+              rope_sincos(tp, 2 * i + 1, D, p.log2_theta, &s1, &c1);
+            }
             const __nv_bfloat162 nlo = __floats2bfloat162_rn(rope_lo(l2.x, h2.x, c0, s0),
                                                              rope_lo(l2.y, h2.y, c1, s1));
             const __nv_bfloat162 nhi = __floats2bfloat162_rn(rope_hi(l2.x, h2.x, c0, s0),

@@ -11,12 +11,16 @@ __device__ __forceinline__ void rope_sincos(float p, int j, int d, float log2_th
   const float inv_freq = exp2f(-(2.f * j / d) * log2_theta);
   sincosf(p * inv_freq, sn, cs);
 }
-// first half element x1 with partner x2: x1 c - x2 s; second half x2: x2 c + x1 s
+// first half element x1 with partner x2: x1 c - x2 s; second half x2: x2 c + x1 s.
+// The rounding is pinned with explicit intrinsics (one product rounded, then one fma):
+// left to the compiler, the FMA contraction of a*b + c*d depends on the surrounding code,
+// and the kernels sharing this math (segmented RoPE, K1's RoPE push, K0's epilogue) must
+// agree bit for bit.
 __device__ __forceinline__ float rope_lo(float x1, float x2, float c, float s) {
-  return x1 * c - x2 * s;
+  return __fmaf_rn(x1, c, __fmul_rn(-x2, s));
 }
 __device__ __forceinline__ float rope_hi(float x1, float x2, float c, float s) {
-  return x2 * c + x1 * s;
+  return __fmaf_rn(x2, c, __fmul_rn(x1, s));
 }
 
 }  // namespace autosp
