@@ -474,8 +474,9 @@ def main():
     a2a = None
     if "a2a" in ksum and P > 1:
         v = ksum["a2a"]
-        a2a = {"kernel": "K1/K2 push (handshake + push launches; the O reshard fused into "
-                         "attn_fwd is not separately timed)",
+        a2a = {"kernel": "standalone reshard launches (handshake + push; per layer the "
+                         "dO + delta reshard of the backward).  The q/k/v push runs in K0's "
+                         "epilogue, O in K3's, dq/dk/dv in K4's: not separately timed",
                "calls_per_step": v["calls"] / args.steps,
                "bytes_per_call": v["bytes"] / max(v["calls"], 1),
                "us_per_call": v["ms"] * 1e3 / max(v["calls"], 1),

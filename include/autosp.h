@@ -121,6 +121,16 @@ AUTOSP_API int autosp_a2a_rope(int direction, const autosp_a2a_tensor* tensors, 
                int b, int s_global, int d, int elem_bytes, int world, int rank,
                void* const* peer_base, uint32_t* const* peer_flags, uint32_t epoch,
                const float* pos, float theta, void* stream);
+/* The backward's seq->head reshard of the attention-output gradient fused with
+ * delta = rowsum(dO * O) (softmax_dx's correction term, executor.py:89-91), formed on the
+ * token owner: t2[0] = dO (token-major source, head-major [b, h/P, S, d] destination as in
+ * autosp_a2a), t2[1] = O (token-major source, same logical shape) whose DESTINATION is the
+ * fp32 delta [b, h/P, S] (dst strides in fp32 elements, dst_stride_s = 1).  bf16, d in
+ * {32, 64, 128}.  One handshake + one push launch; the receiver waits with autosp_a2a_wait
+ * (check = autosp_a2a_check(AUTOSP_SEQ_TO_HEAD, t2, 2)).                              */
+AUTOSP_API int autosp_a2a_grad_out(const autosp_a2a_tensor* t2, int b, int s_global, int d,
+               int world, int rank, void* const* peer_base, uint32_t* const* peer_flags,
+               uint32_t epoch, void* stream);
 /* Stream-ordered wait until every peer has published `epoch` into this rank's flag
  * block (the receive region then holds the complete a2a output).  `check` is the check
  * word of the call as THIS rank sees it (autosp_a2a_check of its descriptors, or

@@ -107,6 +107,9 @@ EXPORTS = {
     "autosp_attn_bwd_delta": (C.c_int, [AttnTensor] * 3 + [C.c_void_p, AttnTensor, C.c_void_p] +
                               [AttnTensor] * 3 + [C.c_void_p] + [C.c_int] * 5 +
                               [C.c_float, C.c_int, C.c_void_p]),
+    "autosp_a2a_grad_out": (C.c_int, [C.POINTER(A2ATensor)] + [C.c_int] * 5 +
+                            [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_uint32,
+                             C.c_void_p]),
     "autosp_qkv_gemm": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64] + [C.c_int] * 6 +
                         [C.c_void_p, C.c_float, C.c_int, C.c_void_p, C.c_int64,
                          C.POINTER(A2ATensor), C.c_int, C.c_int, C.POINTER(C.c_void_p),

@@ -197,6 +197,74 @@ __global__ void __launch_bounds__(kA2AThreads) a2a_push_fast(const __grid_consta
   push_complete(p);
 }
 
+// The backward's seq->head reshard of the attention-output gradient, fused with
+// delta = rowsum(dO * O) (the softmax-gradient correction term, reference softmax_dx
+// executor.py:89-91, formed on the token owner where O lives): tensor 0 of the call is
+// dO (pushed head-major like any a2a tensor), tensor 1 describes O (its source) and the
+// fp32 delta destination [b, h/P, S].  One warp per (batch, head, 16-token tile); the
+// row's lanes reduce their 8-element partial dot products with shuffles.
+template <int ROWB>
+__global__ void __launch_bounds__(kA2AThreads) a2a_grad_out_kernel(const __grid_constant__ A2AParams p) {
+  constexpr int VPR = ROWB / 16;
+  constexpr int RPP = 32 / VPR;
+  constexpr int PASSES = kTileTokens / RPP;
+  const int lane = threadIdx.x & 31;
+  const int r_in = lane / VPR;
+  const int voff = (lane % VPR) * 16;
+  const A2ATensorDev& G = p.t[0];
+  const A2ATensorDev& O = p.t[1];
+  const int warps_total = gridDim.x * (kA2AThreads / 32);
+  const int total = (int)G.items;
+  for (int item = blockIdx.x * (kA2AThreads / 32) + (threadIdx.x >> 5); item < total;
+       item += warps_total) {
+    const int tile = item % G.tiles;
+    const int bh = item / G.tiles;
+    const int hh = bh % G.heads;
+    const int bi = bh / G.heads;
+    const int t0 = tile * kTileTokens;
+    const int last = min(t0 + kTileTokens, p.s_loc) - 1;
+    const char* gsrc = G.src + ((int64_t)bi * G.ss_b + (int64_t)t0 * G.ss_s +
+                                (int64_t)hh * G.ss_h) * 2 + voff;
+    const char* osrc = O.src + ((int64_t)bi * O.ss_b + (int64_t)t0 * O.ss_s +
+                                (int64_t)hh * O.ss_h) * 2 + voff;
+    uint4 g[PASSES], o[PASSES];
+#pragma unroll
+    for (int ps = 0; ps < PASSES; ++ps) {
+      const int r = ps * RPP + r_in;
+      if (t0 + r <= last) {
+        g[ps] = __ldg(reinterpret_cast<const uint4*>(gsrc + r * G.ss_s * 2));
+        o[ps] = __ldg(reinterpret_cast<const uint4*>(osrc + r * O.ss_s * 2));
+      }
+    }
+    const int hl = G.heads / p.P;
+    const int j = hh / hl;
+    const int64_t tok = (int64_t)p.rank * p.s_loc + t0;
+    char* gdst = p.peer_base[j] + G.dst_off +
+                 ((int64_t)bi * G.ds_b + tok * G.ds_s + (int64_t)(hh - j * hl) * G.ds_h) * 2 + voff;
+    float* ddst = reinterpret_cast<float*>(p.peer_base[j] + O.dst_off) +
+                  ((int64_t)bi * O.ds_b + tok * O.ds_s + (int64_t)(hh - j * hl) * O.ds_h);
+#pragma unroll
+    for (int ps = 0; ps < PASSES; ++ps) {
+      const int r = ps * RPP + r_in;
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g[ps]);
+      const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&o[ps]);
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 a = __bfloat1622float2(g2[k]), b = __bfloat1622float2(o2[k]);
+        acc = fmaf(a.x, b.x, fmaf(a.y, b.y, acc));
+      }
+#pragma unroll
+      for (int off = VPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (t0 + r <= last) {
+        *reinterpret_cast<uint4*>(gdst + r * G.ds_s * 2) = g[ps];
+        if (lane % VPR == 0) ddst[r * O.ds_s] = acc;
+      }
+    }
+  }
+  push_complete(p);
+}
+
 // G = bytes moved per lane per row-chunk (16, 8, 4 or 2).
 template <typename V>
 __global__ void __launch_bounds__(kA2AThreads) a2a_push_kernel(const __grid_constant__ A2AParams p) {
@@ -482,6 +550,81 @@ static int a2a_impl(int direction, const autosp_a2a_tensor* tensors, int n_tenso
   return AUTOSP_OK;
 }
 
+extern "C" int autosp_a2a_grad_out(const autosp_a2a_tensor* t2, int b, int s_global, int d,
+                                   int world, int rank, void* const* peer_base,
+                                   uint32_t* const* peer_flags, uint32_t epoch, void* stream) {
+  using namespace autosp;
+  if (!t2 || !t2[0].src || !t2[1].src || (d != 32 && d != 64 && d != 128) || b < 1 ||
+      world < 1 || world > AUTOSP_MAX_WORLD || rank < 0 || rank >= world || s_global % world ||
+      t2[0].heads < 1 || t2[0].heads % world || t2[1].heads != t2[0].heads || !peer_base ||
+      !peer_flags) {
+    autosp_set_error("a2a_grad_out: bad arguments (d=%d world=%d rank=%d)", d, world, rank);
+    return AUTOSP_ERR_VALIDATION;
+  }
+  A2AParams p{};
+  p.n = 2;
+  p.dir = AUTOSP_SEQ_TO_HEAD;
+  p.b = b;
+  p.s_glob = s_global;
+  p.s_loc = s_global / world;
+  p.d = d;
+  p.eb = 2;
+  p.P = world;
+  p.rank = rank;
+  p.epoch = epoch;
+  p.timeout_ns = g_spin_timeout_ns;
+  p.check = autosp_a2a_check(AUTOSP_SEQ_TO_HEAD, t2, 2);
+  uint64_t align = 0;
+  for (int i = 0; i < 2; ++i) {
+    const autosp_a2a_tensor& T = t2[i];
+    A2ATensorDev& D = p.t[i];
+    D.src = static_cast<const char*>(T.src);
+    D.ss_b = T.src_stride_b; D.ss_s = T.src_stride_s; D.ss_h = T.src_stride_h;
+    D.dst_off = T.dst_offset;
+    D.ds_b = T.dst_stride_b; D.ds_s = T.dst_stride_s; D.ds_h = T.dst_stride_h;
+    D.heads = T.heads;
+    D.tiles = (p.s_loc + kTileTokens - 1) / kTileTokens;
+    D.items = (int64_t)b * T.heads * D.tiles;
+    align |= (uint64_t)(uintptr_t)T.src | (uint64_t)(T.src_stride_b | T.src_stride_s |
+                                                      T.src_stride_h) * 2;
+  }
+  align |= (uint64_t)t2[0].dst_offset | (uint64_t)(t2[0].dst_stride_b | t2[0].dst_stride_s |
+                                                   t2[0].dst_stride_h) * 2;
+  align |= (uint64_t)(t2[1].dst_offset & 3);
+  if (align & 15) {
+    autosp_set_error("a2a_grad_out: sources / dO destination must be 16-byte aligned rows "
+                     "(delta destination 4-byte aligned)");
+    return AUTOSP_ERR_VALIDATION;
+  }
+  for (int j = 0; j < world; ++j) {
+    if (!peer_base[j] || !peer_flags[j] || (reinterpret_cast<uintptr_t>(peer_base[j]) & 15)) {
+      autosp_set_error("a2a_grad_out: peer %d base/flags null or misaligned", j);
+      return AUTOSP_ERR_VALIDATION;
+    }
+    p.peer_base[j] = static_cast<char*>(peer_base[j]);
+    p.peer_flags[j] = peer_flags[j];
+  }
+  p.total_items = p.t[0].items;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int64_t blocks = (p.total_items + (kA2AThreads / 32) - 1) / (kA2AThreads / 32);
+  if (blocks > (int64_t)sms * 4) blocks = (int64_t)sms * 4;
+  if (blocks < 1) blocks = 1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (world > 1) a2a_handshake_kernel<<<1, 32, 0, st>>>(p);
+  switch (d) {
+    case 32: a2a_grad_out_kernel<64><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
+    case 64: a2a_grad_out_kernel<128><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
+    default: a2a_grad_out_kernel<256><<<(int)blocks, kA2AThreads, 0, st>>>(p); break;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    autosp_set_error("a2a_grad_out launch failed: %s", cudaGetErrorString(e));
+    return AUTOSP_ERR_CUDA;
+  }
+  return AUTOSP_OK;
+}
+
 extern "C" uint32_t autosp_a2a_check(int direction, const autosp_a2a_tensor* tensors,
                                      int n_tensors) {
   autosp::CheckHash h;
@@ -572,5 +715,8 @@ int autosp_preload_a2a() {
   cudaFuncGetAttributes(&a, autosp::a2a_handshake_kernel);
   cudaFuncGetAttributes(&a, autosp::a2a_wait_kernel);
   cudaFuncGetAttributes(&a, autosp::a2a_mark_ready_kernel);
+  cudaFuncGetAttributes(&a, autosp::a2a_grad_out_kernel<64>);
+  cudaFuncGetAttributes(&a, autosp::a2a_grad_out_kernel<128>);
+  cudaFuncGetAttributes(&a, autosp::a2a_grad_out_kernel<256>);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }

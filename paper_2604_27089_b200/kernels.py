@@ -278,6 +278,24 @@ def a2a_launch(direction: int, descs: list, b: int, s_global: int, d: int, elem_
     return a2a_check(direction, descs)
 
 
+def a2a_grad_out(do_desc, o_desc, b: int, s_global: int, d: int, world: int, rank: int,
+                 peer_base: list[int], peer_flags: list[int], epoch: int) -> int:
+    """autosp_a2a_grad_out: dO reshard seq->head fused with delta = rowsum(dO * O) (o_desc's
+    destination is the fp32 delta).  Returns the check word."""
+    lib = _lib.load()
+    arr = (_lib.A2ATensor * 2)(do_desc, o_desc)
+    pb = (C.c_void_p * world)(*peer_base)
+    pf = (C.c_void_p * world)(*peer_flags)
+    ev = LOG.begin("a2a")
+    rc = lib.autosp_a2a_grad_out(arr, b, s_global, d, world, rank, pb, pf, epoch & 0xFFFFFFFF,
+                                 _stream())
+    _lib.check(rc, "a2a_grad_out")
+    local = b * s_global * do_desc.heads * d * 2 // max(world, 1)
+    LOG.end("a2a", ev, 2 if world > 1 else 1,
+            nbytes=(local + local // (2 * d) * 4) * (world - 1) / max(world, 1))
+    return a2a_check(_lib.SEQ_TO_HEAD, [do_desc, o_desc])
+
+
 def a2a_check(direction: int, descs: list) -> int:
     """Check word of a call with these destination descriptors (what autosp_a2a_wait
     compares against every sender's own view)."""

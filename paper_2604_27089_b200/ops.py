@@ -267,16 +267,55 @@ def _attn_a2a_setup(ctx, inputs, output):
     ctx.scale, ctx.causal, ctx.group = scale, causal, group
 
 
+@torch.library.custom_op("autosp::grad_out_reshard", mutates_args=(), device_types="cuda")
+def grad_out_reshard(d_otok: torch.Tensor, o_tok: torch.Tensor,
+                     group: str) -> tuple[torch.Tensor, torch.Tensor]:
+    """The backward's first reshard (the inverse of the fused head->seq push of O,
+    autodiff.py:252-262): dO seq->head, head-major [b, h/P, S, d], together with
+    delta = rowsum(dO * O) [b, h/P, S] fp32 -- formed on the token owner, where the
+    token-major O already is (kept for the O-projection weight gradient), in the SAME push
+    kernel (autosp_a2a_grad_out: one launch instead of an fp32 elementwise product, a
+    reduction and two reshards)."""
+    st = sp_dist.lookup(group)
+    P, pool = st.world, st.pool
+    b, H, sl, d = d_otok.shape
+    if P == 1 or d_otok.dtype != torch.bfloat16 or d not in kernels.SUPPORTED_HEAD_DIMS or \
+            o_tok.dtype != torch.bfloat16:
+        delta_tok = (d_otok.float() * o_tok.float()).sum(-1, keepdim=True)
+        (do,) = all_to_all([d_otok], SEQ_TO_HEAD_DIR, group)
+        (delta,) = all_to_all([delta_tok], SEQ_TO_HEAD_DIR, group)
+        return do, delta.squeeze(-1).contiguous()
+    if H % P:
+        raise ValidationError(f"heads {H} not divisible by world size {P}")
+    hl, S = H // P, sl * P
+    slab = pool.alloc_many([b * hl * S * d * 2, b * hl * S * 4])
+    (off0, p0), (off1, p1) = slab.pieces
+    do = p0.view(torch.bfloat16).as_strided((b, hl, S, d), (hl * S * d, S * d, d, 1))
+    delta = p1.view(torch.float32).view(b, hl, S)
+    t0 = kernels.a2a_tensor_desc(d_otok.permute(0, 2, 1, 3), H, off0, (hl * S * d, d, S * d))
+    t1 = kernels.a2a_tensor_desc(o_tok.permute(0, 2, 1, 3), H, off1, (hl * S, 1, S))
+    epoch = pool.next_epoch()
+    chk = kernels.a2a_grad_out(t0, t1, b, S, d, P, st.rank, slab.regions, pool.flag_ptrs, epoch)
+    kernels.a2a_wait(pool.flag_ptrs[st.rank], P, st.rank, epoch, chk)
+    return do, delta
+
+
+@grad_out_reshard.register_fake
+def _grad_out_reshard_fake(d_otok, o_tok, group):
+    P = sp_dist.lookup(group).world
+    b, H, sl, d = d_otok.shape
+    hl, S = H // P, sl * P
+    return (d_otok.new_empty_strided((b, hl, S, d), (hl * S * d, S * d, d, 1)),
+            d_otok.new_empty((b, hl, S), dtype=torch.float32))
+
+
 def ulysses_attention_grad(d_otok, o_tok, q, k, v, lse, scale, causal, group):
     """Backward of the fused attention + head->seq reshard: delta = rowsum(dO * O) is
     formed on the token owner from the token-major output (kept anyway for the
-    O-projection weight gradient) and resharded with dO (the inverse all-to-all of the
-    fused one, autodiff.py:252-262)."""
-    acc = torch.promote_types(d_otok.dtype, torch.float32)             # fp32 (fp64 on CPU tests)
-    delta_tok = (d_otok.to(acc) * o_tok.to(acc)).sum(-1, keepdim=True)   # [b, H, s/P, 1]
-    (do,) = all_to_all([d_otok], SEQ_TO_HEAD_DIR, group)
-    (delta,) = all_to_all([delta_tok], SEQ_TO_HEAD_DIR, group)          # [b, h/P, s, 1]
-    return attention_backward_delta(do, q, k, v, delta.squeeze(-1), lse, scale, causal)
+    O-projection weight gradient) and resharded with dO in one push (grad_out_reshard,
+    the inverse all-to-all of the fused one, autodiff.py:252-262)."""
+    do, delta = grad_out_reshard(d_otok, o_tok, group)
+    return attention_backward_delta(do, q, k, v, delta, lse, scale, causal)
 
 
 def _attn_a2a_bwd(ctx, d_otok, d_lse):
@@ -355,12 +394,9 @@ FUSE_GRAD_A2A = True  # K4's epilogues push dq/dk/dv to the token owners (no sep
 def _uqa_bwd(ctx, d_otok, *unused):
     pos, qh, kh, vh, o_tok, lse = ctx.saved_tensors
     if FUSE_GRAD_A2A and qh.shape[-1] in kernels.SUPPORTED_HEAD_DIMS:
-        acc = torch.promote_types(d_otok.dtype, torch.float32)
-        delta_tok = (d_otok.to(acc) * o_tok.to(acc)).sum(-1, keepdim=True)
-        (do,) = all_to_all([d_otok], SEQ_TO_HEAD_DIR, ctx.group)
-        (delta,) = all_to_all([delta_tok], SEQ_TO_HEAD_DIR, ctx.group)
-        dqkv = qkv_attention_grad(do, qh, kh, vh, delta.squeeze(-1), lse, pos, ctx.theta,
-                                  ctx.scale, ctx.group)
+        do, delta = grad_out_reshard(d_otok, o_tok, ctx.group)
+        dqkv = qkv_attention_grad(do, qh, kh, vh, delta, lse, pos, ctx.theta, ctx.scale,
+                                  ctx.group)
         return dqkv, None, None, None, None, None, None
     dq, dk, dv = ulysses_attention_grad(d_otok, o_tok, qh, kh, vh, lse, ctx.scale, True,
                                         ctx.group)
@@ -537,12 +573,8 @@ def _uqpa_bwd(ctx, d_otok, *unused):
     """dqkv from K4 with its gradient push (qkv_attention_grad), then the projection's
     two gradient GEMMs (cuBLAS): dh = dqkv W, dW = dqkv^T h."""
     h, w, pos, qh, kh, vh, o_tok, lse = ctx.saved_tensors
-    acc = torch.promote_types(d_otok.dtype, torch.float32)
-    delta_tok = (d_otok.to(acc) * o_tok.to(acc)).sum(-1, keepdim=True)
-    (do,) = all_to_all([d_otok], SEQ_TO_HEAD_DIR, ctx.group)
-    (delta,) = all_to_all([delta_tok], SEQ_TO_HEAD_DIR, ctx.group)
-    dqkv = qkv_attention_grad(do, qh, kh, vh, delta.squeeze(-1), lse, pos, ctx.theta, ctx.scale,
-                              ctx.group)
+    do, delta = grad_out_reshard(d_otok, o_tok, ctx.group)
+    dqkv = qkv_attention_grad(do, qh, kh, vh, delta, lse, pos, ctx.theta, ctx.scale, ctx.group)
     b, sl, K = h.shape
     g2 = dqkv.reshape(b * sl, w.shape[0])
     dh = (g2 @ w).view(b, sl, K)

@@ -65,7 +65,8 @@ def is_autosp_collective(n: fx.Node) -> bool:
                                                       "autosp::ulysses_qkv_attention",
                                                       "autosp::ulysses_qkv_proj_attention",
                                                       "autosp::qkv_grad_gather",
-                                                      "autosp::qkv_attention_grad")
+                                                      "autosp::qkv_attention_grad",
+                                                      "autosp::grad_out_reshard")
 
 
 def is_autosp_attention(n: fx.Node) -> bool:

@@ -54,6 +54,14 @@ def enable_cpu_lowering() -> None:
         dv = (p.transpose(-1, -2) @ do).unflatten(1, (k.shape[1], g)).sum(2)
         return dq, dk, dv
 
+    @torch.library.register_kernel("autosp::grad_out_reshard", "cpu")
+    def _grad_out_reshard_cpu(d_otok, o_tok, group):
+        acc = torch.promote_types(d_otok.dtype, torch.float32)
+        delta_tok = (d_otok.to(acc) * o_tok.to(acc)).sum(-1, keepdim=True)
+        (do,) = ops.all_to_all([d_otok], ops.SEQ_TO_HEAD_DIR, group)
+        (delta,) = ops.all_to_all([delta_tok], ops.SEQ_TO_HEAD_DIR, group)
+        return do, delta.squeeze(-1).contiguous()
+
     @torch.library.register_kernel("autosp::all_to_all", "cpu")
     def _all_to_all_cpu(xs, direction, group):
         st = sp_dist.lookup(group)

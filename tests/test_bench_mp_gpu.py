@@ -30,8 +30,10 @@ def test_bench_two_ranks_one_gpu():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     assert d["final_loss"] == d["final_loss"]  # finite (not NaN)
     # all-to-all block: bytes per call (algorithmic, (P-1)/P of the local share), time, GB/s
+    # of the standalone reshard launches -- one per layer (dO + delta in the backward); the
+    # q/k/v, O and gradient reshards run inside K0 / K3 / K4's epilogues
     a = d["a2a"]
-    assert a["calls_per_step"] >= 2 * 2 and a["bytes_per_call"] > 0 and a["gbs"] > 0
+    assert a["calls_per_step"] >= 2 and a["bytes_per_call"] > 0 and a["gbs"] > 0
     assert 0 < a["frac"] and a["peak_gbs"] == 900.0
     # sp_ac block: the seq-aware plan really ran (recomputation) next to save-all
     sp = d["sp_ac"]

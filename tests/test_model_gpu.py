@@ -155,12 +155,11 @@ def _qkv_rank(st, qkv_full, pos_full, dout_full, results, r, P, hq, hkv):
         dq, dk, dv = ops.ulysses_attention_grad(d_otok, o, qh, kh, vh, lse, scale, True,
                                                 st.name)
         dqkv = ops.qkv_grad_gather(dq, dk, dv, pos, 500000.0, st.name)
-        # the same backward with the gradient reshard fused into K4's epilogues
-        delta_tok = (d_otok.float() * o.float()).sum(-1, keepdim=True)
-        (do,) = ops.all_to_all([d_otok], ops.SEQ_TO_HEAD_DIR, st.name)
-        (delta,) = ops.all_to_all([delta_tok], ops.SEQ_TO_HEAD_DIR, st.name)
-        dqkv_f = ops.qkv_attention_grad(do, qh, kh, vh, delta.squeeze(-1), lse, pos, 500000.0,
-                                        scale, st.name)
+        # the same backward with the gradient reshard fused into K4's epilogues (the same
+        # dO / delta reshard feeds both)
+        do, delta = ops.grad_out_reshard(d_otok, o, st.name)
+        dqkv_f = ops.qkv_attention_grad(do, qh, kh, vh, delta, lse, pos, 500000.0, scale,
+                                        st.name)
         results[r] = (o.clone(), dqkv.clone(), dqkv_f.clone())
     stream.synchronize()
 
@@ -233,3 +232,45 @@ def test_sp_ac_plan_on_the_cuda_graph():
     assert len(attn_o) == cfg.layers and len(lse) == cfg.layers, det
     assert not ffn, ffn
     assert not sp_ac.LAST_PLAN["bw_recomputes_attention"]
+
+
+def _grad_out_rank(st, dot_full, o_full, results, r, P):
+    from paper_2604_27089_b200 import ops
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream), torch.no_grad():
+        sl = dot_full.shape[2] // P
+        # token-major [b, H, s/P, d] views, as the O-projection backward hands them over
+        d_otok = dot_full[:, :, r * sl:(r + 1) * sl].transpose(1, 2).contiguous().transpose(1, 2)
+        o_tok = o_full[:, :, r * sl:(r + 1) * sl].transpose(1, 2).contiguous().transpose(1, 2)
+        do, delta = ops.grad_out_reshard(d_otok, o_tok, st.name)
+        (do_ref,) = ops.all_to_all([d_otok], ops.SEQ_TO_HEAD_DIR, st.name)
+        results[r] = (do.clone(), delta.clone(), do_ref.clone())
+    stream.synchronize()
+
+
+@pytest.mark.parametrize("P,H,d", [(2, 4, 64), (4, 8, 128), (8, 32, 64), (4, 8, 32)])
+def test_grad_out_reshard_virtual_ranks(P, H, d):
+    """autosp_a2a_grad_out: the dO reshard (bit-exact vs the plain push kernel) fused with
+    delta = rowsum(dO * O) (vs an fp64 reference), P virtual ranks on one GPU."""
+    from paper_2604_27089_b200 import testing
+    states, keep = testing.loopback_states(P, 32 << 20, prefix=f"gor{P}_{d}_")
+    b, s = 2, 64 * P
+    g = torch.Generator().manual_seed(P * d)
+    dot = torch.randn(b, H, s, d, generator=g).bfloat16().cuda()
+    o = torch.randn(b, H, s, d, generator=g).bfloat16().cuda()
+    results = [None] * P
+    threads = [threading.Thread(target=_grad_out_rank, args=(states[r], dot, o, results, r, P))
+               for r in range(P)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=120)
+    assert all(x is not None for x in results)
+    ref = (dot.double() * o.double()).sum(-1)  # [b, H, s]
+    hl = H // P
+    for r, (do, delta, do_ref) in enumerate(results):
+        assert torch.equal(do.view(torch.int16), do_ref.view(torch.int16))
+        want = ref[:, r * hl:(r + 1) * hl]
+        err = float((delta.double() - want).abs().max() / want.abs().max())
+        assert err < 1e-5, (r, err)

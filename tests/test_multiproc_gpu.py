@@ -109,9 +109,10 @@ def test_two_processes_ipc_match_unsharded(mode):
         # the QKV projection GEMM itself pushes RoPE'd head-major rows (K0) in every layer
         assert n_proj == CFG["layers"], n_proj
         assert abs(loss - ref_loss) / abs(ref_loss) < 1e-3, (loss, ref_loss)
-        # forward: ONE collective op per layer (RoPE-fused q/k/v reshard + attention whose
-        # epilogue pushes O); backward: dO and delta reshards + packed-gradient gather
-        assert n_fw == CFG["layers"] and n_bw == 3 * CFG["layers"]
+        # forward: ONE collective op per layer (QKV GEMM pushing RoPE'd q/k/v + attention
+        # whose epilogue pushes O); backward: TWO (dO reshard fused with delta =
+        # rowsum(dO * O); the attention backward pushing dq/dk/dv from its epilogues)
+        assert n_fw == CFG["layers"] and n_bw == 2 * CFG["layers"]
         for n, gr in ref_grads.items():
             err = float(abs(grads[n] - gr).max() / max(abs(gr).max(), 1e-30))
             assert err < 2e-2, (rank, n, err)

@@ -148,13 +148,10 @@ def test_auto_sp_sp_ac_world2_matches_oracle(mode):
             assert orc.max_rel_err(grads[k], ref.grads[r][k]) <= 1e-9, k
             assert orc.max_rel_err(red[k], tg[k]) <= 1e-9, k  # after SP-group reduction
         # 2 collectives per layer forward (q/k/v reshard, attention + O push); backward:
-        # the 2 gradient reshards + the tiny delta = rowsum(dO*O) reshard (3 per layer);
-        # attention never recomputed (sp_ac guard) and no forward collective re-issued
-        # (head dims the kernels do not implement natively -- d = 4 here -- run the
-        # unfused O reshard: backward = dO reshard + gradient reshard, no delta reshard)
-        fused = dims.d in (32, 64, 128)
-        assert plan["fw_collectives"] == 2 * dims.layers
-        assert plan["bw_collectives"] == (3 if fused else 2) * dims.layers
+        # 2 (the dO reshard -- fused with delta = rowsum(dO*O) when the head dim is one
+        # the kernels implement -- and the q/k/v gradient reshard); attention never
+        # recomputed (sp_ac guard) and no forward collective re-issued
+        assert plan["bw_collectives"] == 2 * dims.layers
         assert not plan["bw_recomputes_attention"]
         reasons = sorted(prov.values())
         assert reasons.count("InsertedCollective") == dims.layers
