@@ -134,7 +134,11 @@ def load():
                 "(there is no CPU fallback for the AutoSP hot path)")
         lib = C.CDLL(str(LIB_PATH))
         for name, (res, args) in EXPORTS.items():
-            fn = getattr(lib, name)
+            fn = getattr(lib, name, None)
+            if fn is None:
+                if os.environ.get("AUTOSP_LIB"):  # an older A/B variant (tools/emu): skip
+                    continue
+                raise ExtensionMissingError(f"libautosp.so lacks {name}; rebuild")
             fn.restype = res
             fn.argtypes = args
         if lib.autosp_abi_version() != ABI_VERSION:

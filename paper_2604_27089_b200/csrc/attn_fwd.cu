@@ -38,6 +38,9 @@ extern "C" void autosp_set_error(const char* fmt, ...);
 #ifndef AUTOSP_FWD_KVRING64
 #define AUTOSP_FWD_KVRING64 98304  // K/V ring bytes for d <= 64 (3 stages of 128 keys at d = 64)
 #endif
+#ifndef AUTOSP_FWD_MMA2
+#define AUTOSP_FWD_MMA2 1  // one MMA-issuing warp per Q tile for d <= 64 (A/B: +1.5 % at
+#endif                     // d = 64; -11 % at d = 128, where it stays off)
 #ifndef AUTOSP_FWD_EMU128
 #define AUTOSP_FWD_EMU128 2  // exps per 8 on the FMA pipe for d = 128
 #endif
@@ -75,6 +78,10 @@ struct Cfg {
   static constexpr int kAllocWarp = 4 * NQ;
   static constexpr int kTmaWarp = 4 * NQ + 2;
   static constexpr int kMmaWarp = 4 * NQ + 3;
+  // AUTOSP_FWD_MMA2 (NQ = 2): warp 4NQ+1 issues tile 0's MMAs, kMmaWarp tile 1's -- each
+  // tile's QK / PV wait only on its own softmax; the K/V stages are released by both
+  static constexpr bool MMA2 = AUTOSP_FWD_MMA2 && NQ == 2 && D <= 64;
+  static constexpr int kMmaWarp2 = 4 * NQ + 1;
   static constexpr int SW = (D * 2 >= 128) ? 128 : D * 2;  // swizzle bytes
   static constexpr int CE = SW / 2;                         // elements per swizzle chunk
   static constexpr int NCH = D / CE;                        // chunks per row
@@ -183,9 +190,9 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
     mbar_init(q_full, 1);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(k_full + s, 1);
-      mbar_init(k_empty + s, 1);
+      mbar_init(k_empty + s, C::MMA2 ? 2 : 1);
       mbar_init(v_full + s, 1);
-      mbar_init(v_empty + s, 1);
+      mbar_init(v_empty + s, C::MMA2 ? 2 : 1);
     }
     for (int i = 0; i < NQ; ++i) {
       mbar_init(s_full + i, 1);
@@ -234,7 +241,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
                       v_full + st, c * C::CE, j * BN, kvhead, batch, pol_kv);
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kMmaWarp || (C::MMA2 && warp == C::kMmaWarp2)) {
     // ------------------------------------------------------------ MMA issuer
     // The whole warp runs the schedule (warp-uniform control flow keeps descriptors in
     // uniform registers); one elected lane issues each batch of tcgen05.mma + commit.
@@ -274,10 +281,13 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
         if (elect_one()) tc_commit(bar);
         __syncwarp();
       };
+      // the Q tiles this warp issues for (all of them, or one with MMA2)
+      const int i_lo = C::MMA2 ? (warp == kMmaWarp ? 1 : 0) : 0;
+      const int i_hi = C::MMA2 ? i_lo + 1 : NQ;
       mbar_wait(q_full, 0);
       mbar_wait(k_full + 0, 0);
       tc_fence_after();
-      for (int i = 0; i < NQ; ++i)
+      for (int i = i_lo; i < i_hi; ++i)
         if (n_tiles[i] > 0) issue_qk(i, 0);
       commit(k_empty + 0);
       for (int j = 0; j < n_max; ++j) {
@@ -296,7 +306,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
             k_next_ready = true;
           }
         };
-        for (int i = 0; i < NQ; ++i) {
+        for (int i = i_lo; i < i_hi; ++i) {
           if (j >= n_tiles[i]) continue;
           if (C::SEP_P && j + 1 < n_tiles[i]) {
             // S_i(j+1) as soon as the softmax has read S_i(j)

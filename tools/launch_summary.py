@@ -25,7 +25,8 @@ def main(path, step=1):
                 if r[im] == "gpu__time_duration.sum"]
     steps, cur, in_opt = [], [], False
     for name, ms in launches:
-        opt = "FusedOptimizerTensorListMetadata" in name or "FusedAdamW" in name
+        opt = ("FusedOptimizerTensorListMetadata" in name or "FusedAdamW" in name or
+               "adamw_bf16_kernel" in name)
         if in_opt and not opt:
             steps.append(cur)
             cur = []
