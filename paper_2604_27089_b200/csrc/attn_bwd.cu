@@ -40,6 +40,9 @@ int autosp_check_attn_tensor(const autosp_attn_tensor& t, const char* name);
 #define AUTOSP_BWD_EMU128 1  // exps per 8 on the FMA pipe for d = 128
 #endif
 
+#ifndef AUTOSP_BWD_ABL
+#define AUTOSP_BWD_ABL 0  // timing ablations (WRONG results, tools only): 1 no dQ staging /
+#endif                    // reduce, 2 no dS smem stores, 3 no exps (P = S), 4 = 1 + 2
 #ifndef AUTOSP_BWD_SPIN
 #define AUTOSP_BWD_SPIN 0  // 1: the MMA warp busy-polls its mbarriers; 2: + softmax warps
 #endif
@@ -518,8 +521,8 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
               } else {
                 float x0, x1;
                 f2_unpack(x2, x0, x1);
-                e0 = fast_exp2(x0);
-                e1 = fast_exp2(x1);
+                e0 = AUTOSP_BWD_ABL == 3 ? x0 : fast_exp2(x0);
+                e1 = AUTOSP_BWD_ABL == 3 ? x1 : fast_exp2(x1);
               }
               if constexpr (decltype(kMasked)::value) {
                 const int col = c4 * 32 + 2 * c;
@@ -581,8 +584,9 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int unit = unit0 + cc * 4 + u;  // 16-byte unit within the 128 B chunk row
-            sts128(ds_row + ((unit ^ (row & 7)) << 4),
-                   make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
+            if (AUTOSP_BWD_ABL != 2 && AUTOSP_BWD_ABL != 4)
+              sts128(ds_row + ((unit ^ (row & 7)) << 4),
+                     make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
           }
         }
       };
@@ -659,6 +663,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
       auto stage = [&](const uint32_t (&v)[32], int c) {
         const int chunk_id = t * NC + c;
         float* slot = reinterpret_cast<float*>(smem + C::DQ_OFF) + (chunk_id & 1) * (128 * 32);
+        if (AUTOSP_BWD_ABL == 1 || AUTOSP_BWD_ABL == 4) return;
         if (leader && c > 0) bulk_wait_read1();  // the reduce that last used this slot has read it
         named_bar_sync(2, 128);
         uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
