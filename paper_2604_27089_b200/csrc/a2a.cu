@@ -28,7 +28,10 @@
 #include "rope.cuh"
 
 namespace autosp {
-constexpr int kTileTokens = 16;
+#ifndef AUTOSP_A2A_TILE
+#define AUTOSP_A2A_TILE 16  // tokens per warp item of the push kernels
+#endif
+constexpr int kTileTokens = AUTOSP_A2A_TILE;
 constexpr int kA2AThreads = 256;
 
 struct A2ATensorDev {

@@ -89,6 +89,10 @@ AUTOSP_DEV void tma_reduce_add_3d(const CUtensorMap* map, const void* smem, int 
       "r"(smem_u32(smem)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+template <int N>
+AUTOSP_DEV void bulk_wait_read_n() {  // at most N bulk groups still reading their smem source
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
 AUTOSP_DEV void bulk_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
@@ -123,8 +127,13 @@ struct Cfg {
   static constexpr int Q_OFF = 2 * TILE;                       // Q[st]
   static constexpr int DO_OFF = Q_OFF + kQStages * TILE;       // dO[st]
   static constexpr int DS_OFF = DO_OFF + kDOStages * TILE;     // dS^T [128 keys x 128 q] bf16
-  static constexpr int DQ_OFF = DS_OFF + 128 * 128 * 2;        // 2 fp32 chunks [128 x 32]
-  static constexpr int LSE_OFF = DQ_OFF + 2 * 128 * 32 * 4;    // lse[kQStages][128], delta[kQStages][128]
+  // dQ staging slots (fp32 [128 x 32] chunks) between the drain and the TMA reduce-add
+#ifndef AUTOSP_BWD_DQSLOTS64
+#define AUTOSP_BWD_DQSLOTS64 2
+#endif
+  static constexpr int DQS = D <= 64 ? AUTOSP_BWD_DQSLOTS64 : 2;
+  static constexpr int DQ_OFF = DS_OFF + 128 * 128 * 2;
+  static constexpr int LSE_OFF = DQ_OFF + DQS * 128 * 32 * 4;  // lse[kQStages][128], delta[kQStages][128]
   static constexpr int BAR_OFF = LSE_OFF + 2 * kQStages * 128 * 4;
   // dynamic smem starts 1024-aligned when the kernel has no static smem (measured:
   // shared address 0x400, tools/microbench/smem_align); d = 128 needs the slack bytes
@@ -655,16 +664,16 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
       const uint32_t dq_addr = tmem + lane_base + dq_col(t);
       // the slot of chunk 0 was last used two chunks ago: wait for that reduce to have
       // read it BEFORE dQ(t) arrives, off the critical path (dP(t+1) waits for the drain)
-      if (leader) bulk_wait_read1();
+      if (leader) bulk_wait_read_n<C::DQS - 1>();
       mbar_wait(dq_full, t & 1);
       if (threadIdx.x == kDrainWarp0 * 32) BWD_TRACE(9, t);
       tc_fence_after();
       // stage one 32-column chunk through a smem slot and TMA-reduce it into dQacc
       auto stage = [&](const uint32_t (&v)[32], int c) {
         const int chunk_id = t * NC + c;
-        float* slot = reinterpret_cast<float*>(smem + C::DQ_OFF) + (chunk_id & 1) * (128 * 32);
+        float* slot = reinterpret_cast<float*>(smem + C::DQ_OFF) + (chunk_id % C::DQS) * (128 * 32);
         if (AUTOSP_BWD_ABL == 1 || AUTOSP_BWD_ABL == 4) return;
-        if (leader && c > 0) bulk_wait_read1();  // the reduce that last used this slot has read it
+        if (leader && c > 0) bulk_wait_read_n<C::DQS - 1>();  // the slot's last reduce has read it
         named_bar_sync(2, 128);
         uint8_t* srow = reinterpret_cast<uint8_t*>(slot) + row * 128;
 #pragma unroll
