@@ -19,6 +19,7 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 CFG = dict(d_model=256, layers=2, hq=4, hkv=2, d_ffn=512, vocab=512)
+CFG4 = dict(d_model=512, layers=2, hq=8, hkv=4, d_ffn=1024, vocab=512)  # heads divisible by 4
 SEQ = 1024
 
 
@@ -30,7 +31,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, mode, q):
+def _worker(rank, world, port, mode, q, cfgd=None):
     import torch.distributed as tdist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK="0", AUTOSP_POOL_BYTES=str(64 << 20))
@@ -40,8 +41,9 @@ def _worker(rank, world, port, mode, q):
         import paper_2604_27089_b200 as autosp
         from paper_2604_27089_b200 import sp_ac
         from paper_2604_27089_b200.workloads import LlamaConfig, LlamaDecoder, lm_loss
-        cfg = LlamaConfig("mp", CFG["d_model"], CFG["layers"], CFG["hq"], CFG["hkv"],
-                          CFG["d_ffn"], CFG["vocab"])
+        c = cfgd or CFG
+        cfg = LlamaConfig("mp", c["d_model"], c["layers"], c["hq"], c["hkv"], c["d_ffn"],
+                          c["vocab"])
         autosp.reg_passes(["auto_sp", "sp_ac"], ac_mode=mode)
         st = autosp.dist.init(world)
         torch.manual_seed(0)
@@ -82,11 +84,12 @@ def _worker(rank, world, port, mode, q):
             tdist.destroy_process_group()
 
 
-def _run(world, mode):
+def _run(world, mode, cfgd=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q, cfgd))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -113,6 +116,21 @@ def test_two_processes_ipc_match_unsharded(mode):
         # whose epilogue pushes O); backward: TWO (dO reshard fused with delta =
         # rowsum(dO * O); the attention backward pushing dq/dk/dv from its epilogues)
         assert n_fw == CFG["layers"] and n_bw == 2 * CFG["layers"]
+        for n, gr in ref_grads.items():
+            err = float(abs(grads[n] - gr).max() / max(abs(gr).max(), 1e-30))
+            assert err < 2e-2, (rank, n, err)
+
+
+def test_four_processes_ipc_match_unsharded():
+    """P = 4 ranks as four processes on one GPU (each rank pushes into three peers'
+    mapped regions), seq-aware sp_ac, K0 / K3 / K4 pushes and the dO + delta reshard."""
+    ref = _run(1, "seq-aware", CFG4)[0]
+    out = _run(4, "seq-aware", CFG4)
+    _, ref_loss, ref_grads, _, _, _ = ref
+    for rank, loss, grads, n_fw, n_bw, n_proj in out:
+        assert n_proj == CFG4["layers"], n_proj
+        assert abs(loss - ref_loss) / abs(ref_loss) < 1e-3, (loss, ref_loss)
+        assert n_fw == CFG4["layers"] and n_bw == 2 * CFG4["layers"]
         for n, gr in ref_grads.items():
             err = float(abs(grads[n] - gr).max() / max(abs(gr).max(), 1e-30))
             assert err < 2e-2, (rank, n, err)
