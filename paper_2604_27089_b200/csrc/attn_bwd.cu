@@ -43,43 +43,24 @@ int autosp_check_attn_tensor(const autosp_attn_tensor& t, const char* name);
 #ifndef AUTOSP_BWD_ABL
 #define AUTOSP_BWD_ABL 0  // timing ablations (WRONG results, tools only): 1 no dQ staging /
 #endif                    // reduce, 2 no dS smem stores, 3 no exps (P = S), 4 = 1 + 2
-#ifndef AUTOSP_BWD_SPIN
-#define AUTOSP_BWD_SPIN 0  // 1: the MMA warp busy-polls its mbarriers; 2: + softmax warps
-#endif
 
 namespace autosp {
 namespace bwd {
-AUTOSP_DEV void wait_mma(uint64_t* bar, uint32_t ph) {
-  if (AUTOSP_BWD_SPIN >= 1) mbar_wait_spin(bar, ph);
-  else mbar_wait(bar, ph);
-}
-AUTOSP_DEV void wait_sm(uint64_t* bar, uint32_t ph) {
-  if (AUTOSP_BWD_SPIN >= 2) mbar_wait_spin(bar, ph);
-  else mbar_wait(bar, ph);
-}
+
 long long* g_bwd_trace = nullptr;  // set by autosp_debug_set_bwd_trace (tools only)
 
 constexpr int BK = 128;  // keys per CTA
 constexpr int BQ = 128;  // queries per step
 constexpr int kSoftWarp0 = 4;   // softmax-grad warpgroups from warp 4 on
 constexpr int kDrainWarp0 = 0;  // warps 0-3 (lowest priority: the drain has a step of slack)
-#ifndef AUTOSP_BWD_NWG64
-#define AUTOSP_BWD_NWG64 2  // softmax-grad warpgroups for d = 64 (2 or 4; A/B: 4 is 2 % slower)
-#endif
+constexpr int kThreads = 512;
 // Warp roles (the issue arbiter favours higher warp ids: the single-thread TMA / MMA
 // producers sit on top, the dQ drain below the instruction-heavy softmax warpgroups).
-// NWG softmax-grad warpgroups split the 128 query columns of a step (thread = key row):
-//   NWG = 2: warps 4-7 / 8-11 own columns [0,64) / [64,128); alloc 12, TMA 14, MMA 15;
-//   NWG = 4 (d = 64): warps 4-19 own 32 columns each -- twice the warps to hide the
-//            TMEM / smem / MUFU latencies of the (latency-bound) softmax-grad passes,
-//            which hold half the registers each; TMA 20, MMA 21 (also allocates TMEM).
-template <int NWG>
-struct Roles {
-  static constexpr int kThreads = NWG == 4 ? 22 * 32 : 16 * 32;
-  static constexpr int kTmaWarp = NWG == 4 ? 20 : 14;
-  static constexpr int kMmaWarp = NWG == 4 ? 21 : 15;
-  static constexpr int kAllocWarp = NWG == 4 ? 21 : 12;
-};
+// (Measured and removed in round 2: 4 softmax-grad warpgroups of 32 query columns -- 2 %
+// slower; busy-polling mbarrier waits -- neutral.  DESIGN.md section 7.)
+constexpr int kAllocWarp = 12;
+constexpr int kTmaWarp = 14;
+constexpr int kMmaWarp = 15;
 
 AUTOSP_DEV void tma_reduce_add_3d(const CUtensorMap* map, const void* smem, int c0, int c1,
                                   int c2) {
@@ -93,17 +74,9 @@ template <int N>
 AUTOSP_DEV void bulk_wait_read_n() {  // at most N bulk groups still reading their smem source
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
-AUTOSP_DEV void bulk_wait_read1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-}
 
 template <int D>
 struct Cfg {
-  static constexpr int NWG = D == 64 ? AUTOSP_BWD_NWG64 : 2;
-  static constexpr int CPW = BQ / NWG;      // query columns per softmax thread
-  static constexpr int NC32 = CPW / 32;     // 32-column TMEM chunks per softmax thread
-  using R = Roles<NWG>;
-  static constexpr int kThreads = R::kThreads;
   static constexpr int SW = (D * 2 >= 128) ? 128 : D * 2;
   static constexpr int CE = SW / 2;
   static constexpr int NCH = D / CE;
@@ -203,12 +176,11 @@ AUTOSP_DEV uint64_t desc_ds(uint32_t saddr, int kk) {
   return make_smem_desc(saddr + kk * 16 * 128, 128 * 128, 1024, 2);
 }
 
-template <int D>
-__global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __grid_constant__ Params p) {
+// PUSH (compile-time): the fused head->seq push of dK/dV (autosp_attn_bwd_push); a separate
+// instantiation keeps the local-output kernel free of the push path's register pressure
+template <int D, bool PUSH>
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
-  constexpr int NWG = C::NWG, CPW = C::CPW, NC32 = C::NC32;
-  constexpr int kTmaWarp = C::R::kTmaWarp, kMmaWarp = C::R::kMmaWarp,
-                kAllocWarp = C::R::kAllocWarp;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -253,8 +225,8 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
     mbar_init(s_full + 0, 1);
     mbar_init(s_full + 1, 1);
     mbar_init(dp_full, 1);
-    mbar_init(p_ready, 4 * NWG);  // one arrival per softmax warp
-    mbar_init(ds_ready, 4 * NWG);
+    mbar_init(p_ready, 8);     // one arrival per softmax warp
+    mbar_init(ds_ready, 8);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 4);
     mbar_init(acc_full, 1);
@@ -287,18 +259,11 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
   auto dq_col = [&](int t) -> uint32_t {
     return C::NSB == 2 ? (uint32_t)((t & 1) * 128 + 32) : C::DP_COL;
   };
-  // bf16 P^T (S buffer) and dS^T (dP columns) go where no fp32 value still to be read
-  // lives.  S buffer: [0, 32) and [96, 128) (dQ(t) occupies [32, 32 + d)); NWG = 2: half h
-  // writes its 64 queries (32 packed columns) into the part it read itself; NWG = 4:
-  // quarter q writes 16 packed columns at [0,16) [16,32) [96,112) [112,128) -- quarters 1
-  // and 2 write into columns quarters 0 and 3 read, so they wait for those loads (a
-  // 64-thread named barrier per TMEM lane group).  K-step kk (16 queries) of the TS-MMA A
-  // operand lives at pk_col(kk) for both layouts.  dP columns (no dQ there): NWG = 4
-  // quarter q writes into the first half of what it read, [32q, 32q + 16) -> dk_col(kk).
+  // bf16 P^T / dS^T of query-column half h (64 queries = 32 packed columns) are written
+  // inside the columns that half itself read: h = 0 -> cols [0, 32), h = 1 -> [96, 128).
+  // (Writing them densely would overwrite fp32 scores the other half may still be
+  // reading.)  K-step kk (16 queries) of the TS-MMA A operand therefore lives at:
   auto pk_col = [](int kk) -> uint32_t { return kk < 4 ? kk * 8 : 96 + (kk - 4) * 8; };
-  auto dk_col = [](int kk) -> uint32_t {
-    return NWG == 4 ? (uint32_t)((kk >> 1) * 32 + (kk & 1) * 8) : (kk < 4 ? kk * 8 : 96 + (kk - 4) * 8);
-  };
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
@@ -347,7 +312,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
       const uint64_t dk_mn = make_smem_desc(s_k, 128 * C::SW, C::SBO, C::LAYOUT);  // K, MN
       const uint64_t dds = make_smem_desc(s_ds, 128 * 128, 1024, 2);           // dS^T tile
       auto wait_q = [&](int t) {
-        wait_mma(q_full + (t % C::kQStages), (t / C::kQStages) & 1);
+        mbar_wait(q_full + (t % C::kQStages), (t / C::kQStages) & 1);
         tc_fence_after();
       };
       auto issue_s = [&](int t) {  // S^T(t) = K Q(t)^T into S buffer t % NSB
@@ -362,7 +327,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
         __syncwarp();
       };
       auto issue_dp = [&](int t) {  // dP^T(t) = V dO(t)^T
-        wait_mma(do_full + (t % C::kDOStages), (t / C::kDOStages) & 1);
+        mbar_wait(do_full + (t % C::kDOStages), (t / C::kDOStages) & 1);
         tc_fence_after();
         const uint64_t ddo = make_smem_desc(s_do + (t % C::kDOStages) * C::TILE, 16, C::SBO, C::LAYOUT);
         if (elect_one()) {
@@ -374,7 +339,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
         }
         __syncwarp();
       };
-      wait_mma(kv_full, 0);
+      mbar_wait(kv_full, 0);
       wait_q(0);
       issue_s(0);
       for (int t = 0; t < T; ++t) {
@@ -390,7 +355,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
           // S buffer (t+1)%2 holds P(t-1) (consumed by dV(t-1)) and dQ(t-1): wait drain
           // (also on the last step: every drain phase is observed before the next one)
           if (t >= 1) {
-            wait_mma(dq_empty, (t - 1) & 1);
+            mbar_wait(dq_empty, (t - 1) & 1);
             if (lane == 0) BWD_TRACE(0, t);
           }
           if (t + 1 < T) {
@@ -402,7 +367,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
         } else {
           // dQ(t-1) lives in the dP columns: dP(t) waits for its drain
           if (t >= 1) {
-            wait_mma(dq_empty, (t - 1) & 1);
+            mbar_wait(dq_empty, (t - 1) & 1);
             if (lane == 0) BWD_TRACE(0, t);
             tc_fence_after();
           }
@@ -410,7 +375,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
           if (lane == 0) BWD_TRACE(1, t);
         }
         // dV += P^T dO once the exps of tile t are done
-        wait_mma(p_ready, t & 1);
+        mbar_wait(p_ready, t & 1);
         if (lane == 0) BWD_TRACE(2, t);
         tc_fence_after();
         const uint32_t s_col = (t % C::NSB) * 128;
@@ -431,13 +396,13 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
           issue_s(t + 1);
         }
         // dK += dS^T Q and dQ(t) = dS K once dS is in TMEM + smem
-        wait_mma(ds_ready, t & 1);
+        mbar_wait(ds_ready, t & 1);
         if (lane == 0) BWD_TRACE(3, t);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk)
-            mma_ts(tmem + C::DK_COL, tmem + C::DP_COL + dk_col(kk),
+            mma_ts(tmem + C::DK_COL, tmem + C::DP_COL + pk_col(kk),
                    dq_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_g, kk > 0 ? 1u : acc0);
           tc_commit(q_empty + st);
 #pragma unroll
@@ -451,27 +416,20 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
       }
       if (elect_one()) tc_commit(acc_full);
       __syncwarp();
-      wait_mma(dq_empty, (T - 1) & 1);  // the last drain (no phase is left unobserved)
+      mbar_wait(dq_empty, (T - 1) & 1);  // the last drain (no phase is left unobserved)
     }
-  } else if (warp >= kSoftWarp0 && warp < kSoftWarp0 + 4 * NWG) {
+  } else if (warp >= kSoftWarp0 && warp < kSoftWarp0 + 8) {
     // ------------------------------------------------------------ softmax-grad warpgroups
-    // Warpgroup g owns query columns [g*CPW, (g+1)*CPW); thread = key row (TMEM lane).
-    // Part 1: P^T = exp2(S^T c - lse log2e) -> bf16 in S columns.
+    // WG1 (warps 4-7) owns query columns [0, 64), WG2 (warps 8-11) [64, 128); thread =
+    // key row (TMEM lane).  Part 1: P^T = exp2(S^T c - lse log2e) -> bf16 in S columns.
     // Part 2: dS^T = P^T (dP^T - delta) -> bf16 in dP columns + 128B-swizzled smem.
-    const int g = (warp - kSoftWarp0) >> 2;
+    const int half = (warp - kSoftWarp0) >> 2;
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;  // key row within the tile
     const int key = k0 + row;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t dp_addr = tmem + lane_base + C::DP_COL;
-    // dS^T smem tile: two 128B-swizzled chunks of 64 queries; this group's CPW columns
-    uint8_t* ds_row = smem + C::DS_OFF + ((g * CPW) / 64) * (128 * 128) + row * 128;
-    const int unit0 = ((g * CPW) % 64) / 8;  // first 16-byte unit of this group in the chunk
-    // where this group's packed P^T goes in the S buffer (see pk_col)
-    const uint32_t pcol = NWG == 4 ? (g < 2 ? g * 16 : 96 + (g - 2) * 16) : g * 96;
-    const uint32_t dcol = NWG == 4 ? g * 32 : g * 96;  // packed dS^T in the dP columns
-    // NWG = 4: quarters 1 / 2 overwrite columns quarters 0 / 3 read (same TMEM lanes)
-    const int pair_bar = 3 + quarter + (g >= 2 ? 4 : 0);
+    uint8_t* ds_row = smem + C::DS_OFF + half * (128 * 128) + row * 128;
     const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
     const bool row_dead = key >= p.S;
     for (int t = 0; t < T; ++t) {
@@ -482,36 +440,32 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
       const float* lse_b = lse_s + st * 128;
       const float* dlt_b = dlt_s + st * 128;
       if (!p.lse_tma) {  // S % 4 != 0: stage lse/delta through registers (slow path)
-        if (t >= C::kQStages) named_bar_sync(1, 128 * NWG);  // everyone done with this slot
-        if (g == 0) {
+        if (t >= C::kQStages) named_bar_sync(1, 256);  // everyone done with this slot
+        if (half == 0) {
           const int q = q0 + row;
           const int64_t idx = ((int64_t)batch * p.Hq + head) * p.S + q;
           lse_s[st * 128 + row] = q < p.S ? p.lse[idx] : 0.f;
           dlt_s[st * 128 + row] = q < p.S ? p.delta[idx] : 0.f;
         }
-        named_bar_sync(1, 128 * NWG);
+        named_bar_sync(1, 256);
       }
       // tiles that need element masks: the diagonal (causal) and the sequence tail
       const bool masked = (p.causal && (q0 < k0 + BK)) || (k0 + BK > p.S) || (q0 + BQ > p.S);
       const int col_lo = p.causal ? key - q0 : -1;  // col < col_lo -> masked (q < key)
       const int col_hi = min(p.S - q0, BQ);          // col >= col_hi -> masked (q >= S)
       if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(12, t);
-      wait_sm(s_full + (t % C::NSB), (t / C::NSB) & 1);
+      mbar_wait(s_full + (t % C::NSB), (t / C::NSB) & 1);
       if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(5, t);
       tc_fence_after();
-      uint32_t pkeep[CPW / 2];  // this thread's P^T values (bf16 pairs), reused by part 2
+      uint32_t pkeep[32];  // this thread's 64 P^T values (bf16 pairs), reused by part 2
       auto part1 = [&](auto kMasked) {
-        uint32_t sr2[NC32][32];  // all chunks in flight: one TMEM round trip
-#pragma unroll
-        for (int cc = 0; cc < NC32; ++cc) tmem_ld32(s_addr + (g * NC32 + cc) * 32, sr2[cc]);
+        uint32_t sr2[2][32];  // both 32-column chunks in flight: one TMEM round trip
+        tmem_ld32(s_addr + (half * 2) * 32, sr2[0]);
+        tmem_ld32(s_addr + (half * 2 + 1) * 32, sr2[1]);
         tmem_wait_ld();
-        if (NWG == 4) {  // the columns quarters 1 / 2 overwrite have been read (0 / 3)
-          if (g == 0 || g == 3) named_bar_arrive(pair_bar, 64);
-          else named_bar_sync(pair_bar, 64);
-        }
 #pragma unroll
-        for (int cc = 0; cc < NC32; ++cc) {
-          const int c4 = g * NC32 + cc;  // 32-column chunk
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c4 = half * 2 + cc;  // 32-column chunk
           const uint32_t* sr = sr2[cc];
           const float4* l4 = reinterpret_cast<const float4*>(lse_b + c4 * 32);
 #pragma unroll
@@ -541,7 +495,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
               pkeep[cc * 16 + c] = pack_bf16(e0, e1);
             }
           }
-          tmem_st16(s_addr + pcol + cc * 16,
+          tmem_st16(s_addr + half * 96 + cc * 16,
                     *reinterpret_cast<uint32_t(*)[16]>(&pkeep[cc * 16]));
         }
       };
@@ -552,17 +506,17 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
       mbar_arrive_warp(p_ready);
       if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(6, t);
       // (dp_full(t) also implies dQ(t-1) finished reading the smem dS tile)
-      wait_sm(dp_full, t & 1);
+      mbar_wait(dp_full, t & 1);
       if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(7, t);
       tc_fence_after();
       auto part2 = [&](auto kMasked) {
-        uint32_t dr2[NC32][32];
-#pragma unroll
-        for (int cc = 0; cc < NC32; ++cc) tmem_ld32(dp_addr + (g * NC32 + cc) * 32, dr2[cc]);
+        uint32_t dr2[2][32];
+        tmem_ld32(dp_addr + (half * 2) * 32, dr2[0]);
+        tmem_ld32(dp_addr + (half * 2 + 1) * 32, dr2[1]);
         tmem_wait_ld();
 #pragma unroll
-        for (int cc = 0; cc < NC32; ++cc) {
-          const int c4 = g * NC32 + cc;
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c4 = half * 2 + cc;
           const uint32_t* dr = dr2[cc];
           uint32_t dk[16];
           const float4* d4 = reinterpret_cast<const float4*>(dlt_b + c4 * 32);
@@ -589,10 +543,10 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
               dk[c] = bf16x2_mul(pkeep[cc * 16 + c], pack_bf16(a, b));
             }
           }
-          tmem_st16(dp_addr + dcol + cc * 16, dk);
+          tmem_st16(dp_addr + half * 96 + cc * 16, dk);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int unit = unit0 + cc * 4 + u;  // 16-byte unit within the 128 B chunk row
+            const int unit = cc * 4 + u;  // 16-byte unit within this half's 128 B row
             if (AUTOSP_BWD_ABL != 2 && AUTOSP_BWD_ABL != 4)
               sts128(ds_row + ((unit ^ (row & 7)) << 4),
                      make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
@@ -607,18 +561,14 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
       mbar_arrive_warp(ds_ready);
       if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(8, t);
     }
-    // ---- epilogue: dV (first half of the warpgroups) / dK scaled (second half) straight
-    // from TMEM; with NWG = 4 each warpgroup writes half of the D columns
+    // ---- epilogue: dV (WG1) / dK scaled (WG2) straight from TMEM
     if (T > 0) {
       mbar_wait(acc_full, 0);
       tc_fence_after();
-      const int half = g / (NWG / 2);
-      constexpr int DW = D / (NWG / 2);                 // columns per warpgroup
-      const int cbase = (g % (NWG / 2)) * DW;
-      const uint32_t src = tmem + lane_base + (half ? C::DK_COL : C::DV_COL) + cbase;
+      const uint32_t src = tmem + lane_base + (half ? C::DK_COL : C::DV_COL);
       const float sc = half ? p.scale : 1.f;
       __nv_bfloat16* dst;
-      if (p.push) {  // fused K2: the row goes to the owner of token `key`
+      if constexpr (PUSH) {  // fused K2: the row goes to the owner of token `key`
         const int j = min(key, p.S - 1) / p.s_loc;
         const int gh = p.Hq * p.P + (half ? 0 : p.Hkv * p.P) + p.rank * p.Hkv + kvh;
         dst = reinterpret_cast<__nv_bfloat16*>(p.peer_base[j] + p.dst_off) +
@@ -629,7 +579,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
                    : p.dv + (int64_t)batch * p.dv_sb + (int64_t)kvh * p.dv_sh + (int64_t)key * p.dv_ss;
       }
 #pragma unroll
-      for (int c = 0; c < DW; c += 32) {
+      for (int c = 0; c < D; c += 32) {
         uint32_t a[32];
         tmem_ld32(src + c, a);
         tmem_wait_ld();
@@ -641,7 +591,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
             va.y = pack_bf16(__uint_as_float(a[8 * t4 + 2]) * sc, __uint_as_float(a[8 * t4 + 3]) * sc);
             va.z = pack_bf16(__uint_as_float(a[8 * t4 + 4]) * sc, __uint_as_float(a[8 * t4 + 5]) * sc);
             va.w = pack_bf16(__uint_as_float(a[8 * t4 + 6]) * sc, __uint_as_float(a[8 * t4 + 7]) * sc);
-            reinterpret_cast<uint4*>(dst + cbase + c)[t4] = va;
+            reinterpret_cast<uint4*>(dst + c)[t4] = va;
           }
         }
       }
@@ -731,7 +681,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_bwd_kernel(const __g
   if (warp == kAllocWarp) tmem_dealloc<512>(tmem);
   // pushed dK/dV rows: visible system-wide before bwd_post publishes the arrival (the
   // CTA barrier above orders every thread's stores before this cumulative fence)
-  if (p.push && threadIdx.x == 0) __threadfence_system();
+  if (PUSH && threadIdx.x == 0) __threadfence_system();
 }
 
 
@@ -950,10 +900,16 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(attn_bwd_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM);
+    cudaFuncSetAttribute(attn_bwd_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM);
     attr_set = true;
   }
-  attn_bwd_kernel<D><<<dim3(p.n_ktiles, Hkv, B), C::kThreads, C::SMEM, stream>>>(p);
+  if (push)
+    attn_bwd_kernel<D, true><<<dim3(p.n_ktiles, Hkv, B), kThreads, C::SMEM, stream>>>(p);
+  else
+    attn_bwd_kernel<D, false><<<dim3(p.n_ktiles, Hkv, B), kThreads, C::SMEM, stream>>>(p);
   {
     const int64_t threads = a.rows * (D / 8);
     bwd_post_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(a);
@@ -1098,9 +1054,12 @@ extern "C" AUTOSP_API int autosp_debug_set_bwd_trace(long long* dev_buf) {
 
 int autosp_preload_bwd() {
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<32>);
-  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<64>);
-  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<128>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<32, false>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<32, true>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<64, false>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<64, true>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<128, false>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<128, true>);
   cudaFuncGetAttributes(&a, autosp::bwd::bwd_pre_kernel);
   cudaFuncGetAttributes(&a, autosp::bwd::bwd_post_kernel);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;

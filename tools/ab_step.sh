@@ -1,7 +1,4 @@
-# Same-box in-step A/B of library variants: bench.py (no CPU leg) per variant, interleaved.
-# usage: bash tools/ab_step.sh "base bE1 ..." [rounds] [extra bench args]
-VARS=$1; R=${2:-2}; shift 2
-for i in $(seq $R); do for v in $VARS; do
-  AUTOSP_LIB=tools/emu/libautosp_$v.so timeout 600 python bench.py --no-cpu-baseline "$@" > gpurun_out/ab_${v}_$i.log 2>&1
-  echo "$v $i $(tail -1 gpurun_out/ab_${v}_$i.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); k=d["kernels"]; print(round(d["value"]), d["clocks"]["sm_mhz"], round(k["attn_fwd"]["tflops"]), round(k["attn_bwd"]["tflops"]))')" >> gpurun_out/ab_summary.txt
+# same-box A/B of the whole bench step: bash tools/ab_step.sh "v1 v2 ..."  (gpurun_out/abs.txt)
+for i in 1 2; do for v in $1; do
+  echo "$v $(AUTOSP_LIB=tools/emu/libautosp_$v.so timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-sp-ac-block 2>&1 | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"]), round(d["kernels"]["attn_bwd"]["tflops"]), round(d["kernels"]["attn_fwd"]["tflops"]), d["clocks"]["sm_mhz"])')" >> gpurun_out/abs.txt
 done; done
