@@ -301,8 +301,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sp-ac-block", action="store_true",
                     help="skip the extra seq-aware-vs-save-all comparison steps")
-    ap.add_argument("--no-zero1", action="store_true",
-                    help="N > 1: all-reduce gradients + replicated AdamW instead of ZeRO-1")
+    ap.add_argument("--zero1", default="auto", choices=["auto", "on", "off"],
+                    help="N > 1: ZeRO-1 (AdamW state sharded over the SP group, updated "
+                         "parameters all-gathered) -- auto: only when the replicated bf16 "
+                         "AdamW state would exceed 10 %% of device memory (the in-graph "
+                         "gradient all-reduce already overlaps the backward; ZeRO-1 adds an "
+                         "exposed all-gather, so it is a memory, not a speed, option)")
+    ap.add_argument("--no-zero1", action="store_true", help="same as --zero1 off")
     ap.add_argument("--layers", type=int, default=None, help="override (debug only; invalid bench)")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -342,7 +347,11 @@ def main():
 
     torch.manual_seed(0)
     model = LlamaDecoder(cfg, dtype=torch.bfloat16, device=dev)
-    zero1 = P > 1 and not args.no_zero1
+    if args.no_zero1:
+        args.zero1 = "off"
+    opt_state = 2 * 2 * cfg.n_params()  # bf16 first + second moments
+    zero1 = P > 1 and (args.zero1 == "on" or (
+        args.zero1 == "auto" and opt_state > 0.10 * torch.cuda.get_device_properties(dev).total_memory))
     if zero1:  # ZeRO-1 over the SP group: reduce-scatter + sharded AdamW + all-gather
         from paper_2604_27089_b200.zero import ShardedAdamW
         opt = ShardedAdamW(model.parameters(), st, lr=1e-4)
