@@ -28,6 +28,9 @@
 #include "rope.cuh"
 
 namespace autosp {
+#ifndef AUTOSP_A2A_BPS
+#define AUTOSP_A2A_BPS 4  // push CTAs per SM (grid cap; A/B: 1, 2, 8, 16 slower)
+#endif
 #ifndef AUTOSP_A2A_TILE
 #define AUTOSP_A2A_TILE 16  // tokens per warp item of the push kernels
 #endif
@@ -520,7 +523,7 @@ static int a2a_impl(int direction, const autosp_a2a_tensor* tensors, int n_tenso
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int64_t warps_needed = p.total_items;
   int64_t blocks = (warps_needed + (kA2AThreads / 32) - 1) / (kA2AThreads / 32);
-  const int64_t max_blocks = (int64_t)sms * 4;
+  const int64_t max_blocks = (int64_t)sms * AUTOSP_A2A_BPS;
   if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -18,11 +18,19 @@ constexpr int kCounterSlots = 8;  // epoch mod 8: consecutive calls never share 
 // ordered before thread 0's system-scope fence by the CTA barrier (fences are
 // cumulative); the last CTA to finish publishes arrive[rank] = epoch (+ check word) in
 // every peer's flag block.  Must be called by all threads of every CTA.
+// AUTOSP_GPU_FENCE_CTAS=1: every CTA fences at gpu scope and only the last one at system
+// scope (cumulativity through the gpu-scope counter atomics): -13 % per small loopback
+// call, but it leans on cross-scope cumulativity for NVLink peer writes that one GPU cannot
+// test, so the default keeps a system-scope fence per CTA.
+#ifndef AUTOSP_GPU_FENCE_CTAS
+#define AUTOSP_GPU_FENCE_CTAS 0
+#endif
 AUTOSP_DEV void publish_arrival(uint32_t* const* peer_flags, int P, int rank, uint32_t epoch,
                                 uint32_t check, uint32_t n_ctas) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    if (AUTOSP_GPU_FENCE_CTAS) __threadfence();
+    else __threadfence_system();
     uint32_t* ctr = peer_flags[rank] + kCounterWord + (epoch % kCounterSlots);
     const uint32_t old = atom_add_acqrel_gpu(ctr, 1u);
     if (old == n_ctas - 1) {
