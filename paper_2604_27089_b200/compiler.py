@@ -18,7 +18,7 @@ import torch
 import torch.distributed as tdist
 
 from . import dist as sp_dist
-from . import grad_sync
+from . import grad_sync, opt_in_bw
 from .auto_sp import auto_sp
 from .errors import ValidationError
 from .sp_ac import AcMode, is_autosp_collective, make_partition_fn
@@ -45,7 +45,7 @@ def registered_passes() -> list[str]:
     return list(_PASSES)
 
 
-def backend(passes: list[str] | None = None, ac_mode: AcMode | None = None):
+def backend(passes: list[str] | None = None, ac_mode: AcMode | None = None, optimizer=None):
     """A torch.compile backend applying the registered passes."""
     from functorch.compile import make_boxed_func
     from torch._dynamo.backends.common import aot_autograd
@@ -54,11 +54,13 @@ def backend(passes: list[str] | None = None, ac_mode: AcMode | None = None):
     passes = list(_PASSES if passes is None else passes)
     mode = _AC_MODE if ac_mode is None else AcMode(ac_mode)
 
-    def _compiler(gm, example_inputs, sync=None):
+    def _compiler(gm, example_inputs, sync=None, opt=None):
         if _COMPILER_OVERRIDE is not None:
             return _COMPILER_OVERRIDE(gm, example_inputs)
         if sync is not None:  # backward graph: bucketed SP/DP gradient all-reduce
             grad_sync.insert(gm, *sync)
+        if opt is not None:  # backward graph: parameters updated as their gradients appear
+            opt_in_bw.insert(gm, *opt)
         fn = make_boxed_func(gm.forward)
         st = sp_dist.state()
         if st.world > 1 and st.group is not None and \
@@ -83,8 +85,19 @@ def backend(passes: list[str] | None = None, ac_mode: AcMode | None = None):
         if "auto_sp" in passes:
             gm, info = auto_sp(gm, example_inputs, st)
             LAST_INFO["auto_sp"] = info
-        part = make_partition_fn(mode) if "sp_ac" in passes else default_partition
+        base_part = make_partition_fn(mode) if "sp_ac" in passes else default_partition
+        aliases: dict = {}
+
+        def part(joint_module, joint_inputs, **kw):
+            if optimizer is not None:  # which joint nodes are views of which parameter
+                aliases.update(opt_in_bw.alias_names(joint_module))
+            return base_part(joint_module, joint_inputs, **kw)
+
         bw = _compiler
+        if optimizer is not None:
+            pidx = [i for i, x in enumerate(example_inputs) if isinstance(x, torch.nn.Parameter)]
+            bw = functools.partial(_compiler, opt=(pidx, [example_inputs[i] for i in pidx],
+                                                   len(example_inputs), aliases, optimizer))
         if grad_sync.enabled(st):
             # the forward inputs that are parameters: their (partial) gradients are
             # all-reduced inside the backward graph, overlapped with it (grad_sync.py)
@@ -92,6 +105,9 @@ def backend(passes: list[str] | None = None, ac_mode: AcMode | None = None):
             dp = tdist.get_world_size() // max(st.world, 1)
             sync = (pidx, [example_inputs[i] for i in pidx], len(example_inputs), dp)
             bw = functools.partial(_compiler, sync=sync)
+            if optimizer is not None:
+                raise ValidationError("optimizer in the backward needs a single rank (the "
+                                      "SP-partial gradients are reduced at the graph's end)")
         return aot_autograd(fw_compiler=_compiler, bw_compiler=bw,
                             partition_fn=part)(gm, example_inputs)
 
@@ -105,7 +121,7 @@ def _frames():
 
 
 def compile(model: torch.nn.Module, passes: list[str] | None = None,
-            ac_mode: AcMode | None = None) -> torch.nn.Module:
+            ac_mode: AcMode | None = None, optimizer=None) -> torch.nn.Module:
     """``model.compile()`` with the AutoSP backend (static shapes).
 
     Graph breaks are allowed (``fullgraph=False``): auto_sp rewrites every Dynamo
@@ -113,12 +129,21 @@ def compile(model: torch.nn.Module, passes: list[str] | None = None,
     graph break inside a loop: "skipping the frame and falling back to eager") would run
     its attention eagerly over the LOCAL shard only -- silently wrong at P > 1.  So at
     P > 1 a call that left any frame uncompiled raises ValidationError (set
-    AUTOSP_ALLOW_EAGER_FRAMES=1 if the skipped frames are known to hold no attention)."""
+    AUTOSP_ALLOW_EAGER_FRAMES=1 if the skipped frames are known to hold no attention).
+
+    optimizer (opt-in, single rank): an ``optim.AdamW`` that updates each parameter INSIDE
+    the compiled backward as soon as its gradient exists (opt_in_bw.py): the gradients are
+    never all alive at once; ``optimizer.step()`` then handles only the parameters used
+    outside the compiled graphs."""
     passes_eff = list(_PASSES if passes is None else passes)
     st = sp_dist.state()
     if grad_sync.enabled(st):  # SP-partial gradients summed by the backward itself
         grad_sync.install(model, tdist.get_world_size() // max(st.world, 1))
-    cm = torch.compile(model, backend=backend(passes, ac_mode), dynamic=False, fullgraph=False)
+    if optimizer is not None and not hasattr(optimizer, "step_params"):
+        raise ValidationError("compile(optimizer=...) needs an optimizer with step_params "
+                              "(optim.AdamW)")
+    cm = torch.compile(model, backend=backend(passes, ac_mode, optimizer), dynamic=False,
+                       fullgraph=False)
     if "auto_sp" not in passes_eff:
         return cm
     snap = {}

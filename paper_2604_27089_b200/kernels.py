@@ -131,11 +131,19 @@ def attn_fwd_push(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Te
     return int(lib.autosp_push_check(C.byref(spec), hq))
 
 
+BWD_WORKSPACE_BYTES = 1 << 30  # larger fp32 workspaces: the backward runs per kv-head group
+
+
 def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = None,
              dq=None, dk=None, dv=None, delta: torch.Tensor | None = None):
     """Flash attention backward recomputing P from the saved LSE.
     Returns (dq, dk, dv) in bf16 ([b, h, s, d]).  With `delta` ([b, hq, s] fp32 =
-    rowsum(dO * O)) `o` is not read and may be None (autosp_attn_bwd_delta)."""
+    rowsum(dO * O)) `o` is not read and may be None (autosp_attn_bwd_delta).
+    Long sequences: the fp32 dQ accumulator workspace grows as b*hq*s*d*4 bytes (3.8 GB
+    for 32 heads x 224K tokens at d = 128), so when it would exceed BWD_WORKSPACE_BYTES the
+    kernels run per group of kv heads (their q heads with them) on head slices of the same
+    tensors -- identical results, a fraction of the transient memory at the backward's
+    memory peak."""
     lib = _lib.load()
     b, hq, s, d = q.shape
     hkv = k.shape[1]
@@ -144,6 +152,20 @@ def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = Non
     dq = torch.empty((b, hq, s, d), dtype=torch.bfloat16, device=dev) if dq is None else dq
     dk = torch.empty((b, hkv, s, d), dtype=torch.bfloat16, device=dev) if dk is None else dk
     dv = torch.empty((b, hkv, s, d), dtype=torch.bfloat16, device=dev) if dv is None else dv
+    ws_total = lib.autosp_attn_bwd_workspace_bytes(b, hq, s, d)
+    if ws_total > BWD_WORKSPACE_BYTES and hkv > 1:
+        n = 1
+        while n < hkv and (hkv % (2 * n) == 0) and ws_total // n > BWD_WORKSPACE_BYTES:
+            n *= 2
+        if n > 1:
+            gk, gq = hkv // n, hq // n
+            for i in range(n):
+                kv, qh = slice(i * gk, (i + 1) * gk), slice(i * gq, (i + 1) * gq)
+                attn_bwd(q[:, qh], k[:, kv], v[:, kv], None if o is None else o[:, qh],
+                         do[:, qh], lse[:, qh].contiguous(), causal, scale,
+                         dq[:, qh], dk[:, kv], dv[:, kv],
+                         None if delta is None else delta[:, qh].contiguous())
+            return dq, dk, dv
     ws = torch.empty(lib.autosp_attn_bwd_workspace_bytes(b, hq, s, d), dtype=torch.uint8,
                      device=dev)
     if not lse.is_contiguous() or lse.dtype != torch.float32:

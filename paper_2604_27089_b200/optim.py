@@ -12,6 +12,8 @@ import torch
 
 from . import _lib
 
+UPDATED = "_autosp_updated"  # set by step_params (update done inside the backward)
+
 
 class _Tensor(C.Structure):
     _fields_ = [("p", C.c_void_p), ("g", C.c_void_p), ("m", C.c_void_p), ("v", C.c_void_p),
@@ -30,12 +32,36 @@ class AdamW(torch.optim.Optimizer):
     @torch.no_grad()
     def step(self, closure=None):
         loss = closure() if closure is not None else None
+        for group in self.param_groups:
+            # parameters the compiled backward already updated in this iteration
+            # (autosp.compile(model, optimizer=...)) are skipped once
+            live = []
+            for p in group["params"]:
+                if getattr(p, UPDATED, False):
+                    setattr(p, UPDATED, False)
+                elif p.grad is not None:
+                    live.append(p)
+            self._apply(group, [(p, p.grad) for p in live])
+        return loss
+
+    @torch.no_grad()
+    def step_params(self, pairs) -> None:
+        """AdamW on the given (parameter, gradient) pairs right now -- called from inside
+        a compiled backward graph (optimizer in the backward: the gradient is freed as
+        soon as its parameter is updated); the next ``step()`` skips these parameters."""
+        for group in self.param_groups:
+            mine = [(p, g) for p, g in pairs if any(p is q for q in group["params"])]
+            if mine:
+                self._apply(group, mine)
+                for p, _ in mine:
+                    setattr(p, UPDATED, True)
+
+    def _apply(self, group, pairs) -> None:
         lib = _lib.load()
         stream = torch.cuda.current_stream().cuda_stream
-        for group in self.param_groups:
-            live = [p for p in group["params"] if p.grad is not None]
-            if not live:
-                continue
+        if pairs:
+            live = [p for p, _ in pairs]
+            grads = {id(p): g for p, g in pairs}
             # the bias corrections depend on each parameter's own step count: one launch
             # per distinct step value (normally exactly one)
             by_step: dict[int, list] = {}
@@ -46,7 +72,8 @@ class AdamW(torch.optim.Optimizer):
                     st["exp_avg"] = torch.zeros_like(p)
                     st["exp_avg_sq"] = torch.zeros_like(p)
                 st["step"] += 1
-                g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
+                g = grads[id(p)]
+                g = g if g.is_contiguous() else g.contiguous()
                 if g.dtype != torch.bfloat16:
                     raise ValueError("optim.AdamW: bf16 gradients only")
                 st["_g"] = g  # keep a made-contiguous gradient alive until the launch
@@ -65,4 +92,3 @@ class AdamW(torch.optim.Optimizer):
                 LOG.end("adamw", None, (len(ps) + 63) // 64)
             for p in live:
                 self.state[p].pop("_g", None)
-        return loss

@@ -316,3 +316,26 @@ def test_attn_bwd_with_supplied_delta_equals_o_path(hq, hkv, s, d):
     for a, b in zip(got, ref):
         err = float((a.float() - b.float()).abs().max() / b.float().abs().max())
         assert err < 1e-2, err  # same math; dQ's fp32 reduce order is not deterministic
+
+
+def test_attn_bwd_head_chunked_equals_whole():
+    """Long-sequence backward split by kv-head groups (smaller fp32 dQ workspace at the
+    backward's memory peak): dK / dV bit-exact against one launch, dQ within the
+    order-dependent rounding of its fp32 reduce-add accumulator."""
+    K = _k()
+    g = torch.Generator().manual_seed(11)
+    b, hq, hkv, s, d = 1, 8, 4, 512, 64
+    q, k, v, do = (torch.randn(b, h, s, d, generator=g).bfloat16().cuda()
+                   for h in (hq, hkv, hkv, hq))
+    o, lse = K.attn_fwd(q, k, v)
+    whole = K.attn_bwd(q, k, v, o, do, lse)
+    old = K.BWD_WORKSPACE_BYTES
+    try:
+        K.BWD_WORKSPACE_BYTES = 1 << 16  # force 4 groups of one kv head
+        chunked = K.attn_bwd(q, k, v, o, do, lse)
+    finally:
+        K.BWD_WORKSPACE_BYTES = old
+    torch.cuda.synchronize()
+    assert torch.equal(chunked[1], whole[1]) and torch.equal(chunked[2], whole[2])
+    err = float((chunked[0].float() - whole[0].float()).abs().max() / whole[0].float().abs().max())
+    assert err < 1e-2, err

@@ -19,7 +19,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def probe(model: str, seq: int, sp_ac: bool, layers: int | None) -> dict:
+def probe(model: str, seq: int, sp_ac: bool, layers: int | None, opt: str = "torch") -> dict:
     code = f"""
 import sys, time, json, torch
 sys.path.insert(0, {str(ROOT)!r})
@@ -32,8 +32,13 @@ autosp.reg_passes({['auto_sp', 'sp_ac'] if sp_ac else ['auto_sp']!r})
 autosp.dist.init(1)
 torch.manual_seed(0)
 m = LlamaDecoder(cfg, dtype=torch.bfloat16, device='cuda')
-opt = torch.optim.AdamW(m.parameters(), lr=1e-4, fused=True)
-cm = autosp.compile(m)
+if {opt!r} == "torch":
+    opt = torch.optim.AdamW(m.parameters(), lr=1e-4, fused=True)
+    cm = autosp.compile(m)
+else:  # the bf16 multi-tensor kernel; "in-backward": updates inside the compiled backward
+    from paper_2604_27089_b200.optim import AdamW
+    opt = AdamW(m.parameters(), lr=1e-4)
+    cm = autosp.compile(m, optimizer=opt if {opt!r} == "in-backward" else None)
 ids = torch.randint(0, cfg.vocab, (1, {seq} + 1), device='cuda')
 t0 = None
 from paper_2604_27089_b200 import sp_ac
@@ -72,7 +77,7 @@ print(json.dumps({{"ok": True, "step_s": time.perf_counter() - t0, "marks": mark
     env = dict(os.environ, PYTORCH_CUDA_ALLOC_CONF="expandable_segments:True")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                        timeout=3600, env=env)
-    out = {"seq": seq, "sp_ac": sp_ac, "wall_s": round(time.time() - t0, 1)}
+    out = {"seq": seq, "sp_ac": sp_ac, "opt": opt, "wall_s": round(time.time() - t0, 1)}
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     if lines:
         out.update(json.loads(lines[-1]))
@@ -91,10 +96,13 @@ def main():
     ap.add_argument("--seqs", default="32768,65536,98304,131072")
     ap.add_argument("--no-sp-ac", action="store_true")
     ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--opt", default="torch", choices=["torch", "autosp", "in-backward"],
+                    help="optimizer: torch fused AdamW, the autosp bf16 AdamW kernel, or that "
+                         "kernel applied inside the compiled backward (gradients never all live)")
     a = ap.parse_args()
-    res = [probe(a.model, int(s), not a.no_sp_ac, a.layers) for s in a.seqs.split(",")]
+    res = [probe(a.model, int(s), not a.no_sp_ac, a.layers, a.opt) for s in a.seqs.split(",")]
     ok = [r["seq"] for r in res if r.get("ok")]
-    print(json.dumps({"model": a.model, "sp_ac": not a.no_sp_ac, "n_gpus": 1,
+    print(json.dumps({"model": a.model, "sp_ac": not a.no_sp_ac, "opt": a.opt, "n_gpus": 1,
                       "max_trainable_seq": max(ok) if ok else None, "probes": res}))
 
 
