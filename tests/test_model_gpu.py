@@ -164,15 +164,16 @@ def _qkv_rank(st, qkv_full, pos_full, dout_full, results, r, P, hq, hkv):
     stream.synchronize()
 
 
-@pytest.mark.parametrize("P,hq,hkv,d", [(2, 4, 2, 64), (4, 8, 4, 128), (8, 32, 8, 64)])
-def test_rope_fused_reshard_block_virtual_ranks(P, hq, hkv, d):
+@pytest.mark.parametrize("P,hq,hkv,d,b", [(2, 4, 2, 64, 1), (4, 8, 4, 128, 1), (8, 32, 8, 64, 1),
+                                           (2, 4, 2, 64, 2)])
+def test_rope_fused_reshard_block_virtual_ranks(P, hq, hkv, d, b):
     """RoPE + split + transpose folded into the seq->head reshard (autosp_a2a_rope), the
     attention epilogue pushing O, and the packed-gradient gather in backward: equal to the
     unsharded qkv_rope -> attention reference (forward bit-exact, gradients within bf16
     tolerance)."""
     from paper_2604_27089_b200 import kernels, ops, testing
-    states, keep = testing.loopback_states(P, 64 << 20, prefix=f"qkv{P}_")
-    b, s = 1, 128 * P
+    states, keep = testing.loopback_states(P, 64 << 20, prefix=f"qkv{P}_{b}_")
+    s = 128 * P
     g = torch.Generator().manual_seed(P + d)
     qkv_full = torch.randn(b, s, hq + 2 * hkv, d, generator=g).bfloat16().cuda()
     pos_full = torch.arange(s, dtype=torch.float32).cuda()
