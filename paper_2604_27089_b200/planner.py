@@ -28,7 +28,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .workloads import MLP_CHUNK, LlamaConfig
+from .workloads import MLP_CHUNK, MLP_CHUNK_TOKENS, LlamaConfig
 
 GB = 1e9
 USABLE_FRACTION = 0.97   # of device memory the caching allocator can hand out
@@ -88,9 +88,14 @@ def step_memory(cfg: LlamaConfig, S: int, P: int = 1, zero1: bool = True,
         per_layer = e * sl * d + 4 * S * hq // P + 4 * sl * 2            # x_in, LSE, rstd
     saved = L * per_layer + e * sl * d                                   # + final hidden
     pool = pool_bytes(cfg, S, P, e)                                      # a2a outputs
-    chunk = min(sl, MLP_CHUNK)
+    chunk = sl if sl <= MLP_CHUNK else MLP_CHUNK_TOKENS
     mlp = e * chunk * (2 * F) * 2 + e * chunk * F * 2                    # gate/up (+grad), act (+grad)
-    attn = 4 * S * hq // P * hd + e * S * (hq + 2 * hkv) // P * hd       # dQ acc, dq/dk/dv
+    dq_acc = 4 * S * hq // P * hd                                        # fp32 dQ accumulator,
+    groups = max(hkv // P, 1)                                            # run per kv-head group
+    while groups > 1 and dq_acc > (1 << 30):                             # above 1 GiB
+        dq_acc //= 2                                                     # (kernels.attn_bwd)
+        groups //= 2
+    attn = dq_acc + e * S * (hq + 2 * hkv) // P * hd                     # + dq/dk/dv
     if P == 1:
         attn += e * S * hq * hd                                          # dO (in the heap at P > 1)
     proj = e * sl * ((hq + 2 * hkv) * hd + 3 * d)                        # recomputed qkv, x_mid, grads

@@ -136,7 +136,10 @@ def rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
     return torch.cat((x1 * c - x2 * s_, x2 * c + x1 * s_), dim=-1)
 
 
-MLP_CHUNK = 32768  # tokens per MLP chunk above which the MLP runs chunked (memory only)
+MLP_CHUNK = 32768  # sequences longer than this run the MLP chunked (memory only) ...
+MLP_CHUNK_TOKENS = 16384  # ... in chunks of this many tokens: the backward recomputes one
+                          # chunk's [tokens, 2*d_ffn] gate/up at a time at its memory peak
+                          # (Llama-3-8B at 224K: 0.94 GB instead of 1.88 GB)
 FUSE_RESIDUAL = os.environ.get("AUTOSP_FUSE_RESIDUAL", "1") == "1"  # addmm epilogue adds
 
 
@@ -188,7 +191,7 @@ class LlamaBlock(nn.Module):
             # long contexts: the MLP in sequence chunks, so its [s, 2*d_ffn] intermediate
             # (and, under sp_ac, its recomputation in backward) is live one chunk at a time
             return x + torch.cat([ops.swiglu(hc @ self.w13.t()) @ self.w2.t()
-                                  for hc in h.split(MLP_CHUNK, dim=1)], dim=1)
+                                  for hc in h.split(MLP_CHUNK_TOKENS, dim=1)], dim=1)
         h = rmsnorm(x, self.norm2, cfg.eps)
         g, u = (h @ self.w13.t()).chunk(2, dim=-1)
         return x + (F.silu(g) * u) @ self.w2.t()

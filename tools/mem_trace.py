@@ -30,9 +30,15 @@ class MemInterp(fx.Interpreter):
         try:
             out = super().run_node(n)
         except torch.OutOfMemoryError:
-            live = sorted(((v.untyped_storage().nbytes(), k.name, str(k.target), tuple(v.shape))
-                           for k, v in self.env.items()
-                           if isinstance(v, torch.Tensor) and v.is_cuda), reverse=True)
+            seen, uniq = set(), []
+            for k, v in self.env.items():  # one entry per storage (views share theirs)
+                if isinstance(v, torch.Tensor) and v.is_cuda:
+                    sid = v.untyped_storage().data_ptr()
+                    if sid not in seen:
+                        seen.add(sid)
+                        uniq.append((v.untyped_storage().nbytes(), k.name, str(k.target),
+                                     tuple(v.shape)))
+            live = sorted(uniq, reverse=True)
             tot = sum(b for b, *_ in live)
             print(json.dumps({"oom_in": self.tag, "at": n.name, "target": str(n.target),
                               "allocated_gb": torch.cuda.memory_allocated() / 1e9,
@@ -64,7 +70,12 @@ def main():
     ap.add_argument("--seq", type=int, default=131072)
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--ac-mode", default="seq-aware")
+    ap.add_argument("--reserve-gb", type=float, default=0.0,
+                    help="allocate this much first (e.g. 32 = the bf16 AdamW moments of the 8B "
+                         "shape, present from the second step on)")
     a = ap.parse_args()
+    reserve = torch.empty(int(a.reserve_gb * 1e9), dtype=torch.uint8, device="cuda") \
+        if a.reserve_gb else None  # noqa: F841 (held for the whole step)
     import paper_2604_27089_b200 as autosp
     from paper_2604_27089_b200 import compiler, sp_ac
     from paper_2604_27089_b200.workloads import CONFIGS, LlamaConfig, LlamaDecoder, lm_loss
@@ -101,6 +112,8 @@ def main():
         if "primals" not in d[0] and not d[1].endswith("::t"):
             print("saved", d, flush=True)
     loss = lm_loss(hidden, m.lm_head, ids[:, 1:])
+    print(json.dumps({"after_loss_gb": torch.cuda.memory_allocated() / 1e9,
+                      "peak_so_far_gb": torch.cuda.max_memory_allocated() / 1e9}), flush=True)
     del hidden
     loss.backward()
     torch.cuda.synchronize()
