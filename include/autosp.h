@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define AUTOSP_ABI_VERSION 2
+#define AUTOSP_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define AUTOSP_API __attribute__((visibility("default")))
@@ -191,8 +191,9 @@ AUTOSP_API int autosp_attn_fwd_push(autosp_attn_tensor q, autosp_attn_tensor k,
                     const autosp_push_spec* push, void* stream);
 
 /* fp32 workspace the backward needs: dq accumulator [b, hq, s, d] + delta [b, hq, s]
- * + -lse*log2(e) [b, hq, s] */
-AUTOSP_API size_t autosp_attn_bwd_workspace_bytes(int b, int hq, int s, int d);
+ * + -lse*log2(e) [b, hq, s] (+ dK/dV partials [2, b, hkv, s, d] when the launch splits
+ * each kv head's q-head group over two CTAs to fill the GPU: small grids, GQA) */
+AUTOSP_API size_t autosp_attn_bwd_workspace_bytes(int b, int hq, int hkv, int s, int d);
 AUTOSP_API int autosp_attn_bwd(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
                     autosp_attn_tensor o, autosp_attn_tensor d_o, const float* lse,
                     autosp_attn_tensor dq, autosp_attn_tensor dk, autosp_attn_tensor dv,

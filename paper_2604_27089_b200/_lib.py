@@ -13,7 +13,7 @@ from .errors import (CudaError, ExtensionMissingError, SeqcompError, Unsupported
                      ValidationError)
 
 LIB_PATH = Path(os.environ.get("AUTOSP_LIB") or Path(__file__).resolve().parent / "libautosp.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 IPC_HANDLE_BYTES = 64
 MAX_WORLD = 8
 MAX_A2A_TENSORS = 4
@@ -101,7 +101,7 @@ EXPORTS = {
     "autosp_adamw_bf16": (C.c_int, [C.c_void_p, C.c_int] + [C.c_float] * 5 + [C.c_int, C.c_void_p]),
     "autosp_debug_set_bwd_trace": (C.c_int, [C.c_void_p]),
     "autosp_debug_set_fwd_trace": (C.c_int, [C.c_void_p]),
-    "autosp_attn_bwd_workspace_bytes": (C.c_size_t, [C.c_int] * 4),
+    "autosp_attn_bwd_workspace_bytes": (C.c_size_t, [C.c_int] * 5),
     "autosp_attn_bwd": (C.c_int, [AttnTensor] * 5 + [C.c_void_p] + [AttnTensor] * 3 +
                         [C.c_void_p] + [C.c_int] * 5 + [C.c_float, C.c_int, C.c_void_p]),
     "autosp_attn_bwd_delta": (C.c_int, [AttnTensor] * 3 + [C.c_void_p, AttnTensor, C.c_void_p] +

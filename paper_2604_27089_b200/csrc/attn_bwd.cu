@@ -144,6 +144,12 @@ struct Params {
   int push, P, rank, s_loc;
   int64_t dst_off, d_sb, d_ss, d_sh;  // bytes / elements
   char* peer_base[AUTOSP_MAX_WORLD];
+  // GQA split (small grids, e.g. one kv head per rank at SP = 8): hsplit CTAs share a
+  // (key tile, kv head), each taking group/hsplit of its q heads; their dK/dV partials are
+  // red.add-ed into dkv_acc (fp32 [2][B][Hkv][S][D]: dK, dV) and bwd_post finishes them.
+  // With hsplit = 2 every element gets exactly two addends: deterministic.
+  int hsplit;
+  float* dkv_acc;
 };
 
 constexpr int kTraceSteps = 64;
@@ -178,7 +184,7 @@ AUTOSP_DEV uint64_t desc_ds(uint32_t saddr, int kk) {
 
 // PUSH (compile-time): the fused head->seq push of dK/dV (autosp_attn_bwd_push); a separate
 // instantiation keeps the local-output kernel free of the push path's register pressure
-template <int D, bool PUSH>
+template <int D, bool PUSH, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
@@ -207,14 +213,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   const int warp = warp_id();
   const int lane = lane_id();
   const int ktile = blockIdx.x;  // launch order = heaviest (most query tiles) first
-  const int kvh = blockIdx.y;
+  constexpr int HS = SPLIT ? 2 : 1;                            // (compile-time: registers)
+  const int kvh = blockIdx.y / HS;
   const int batch = blockIdx.z;
   const int group = p.Hq / p.Hkv;
+  const int gsz = group / HS;                                  // q heads of this CTA
   const int k0 = ktile * BK;
   const int n_qtiles = (p.S + BQ - 1) / BQ;
   const int m_first = p.causal ? (k0 / BQ) : 0;
   const int per_head = n_qtiles - m_first;
-  const int T = per_head * group;  // steps of this CTA
+  const int T = per_head * gsz;  // steps of this CTA
 
   if (warp == kTmaWarp && lane == 0) {
     mbar_init(kv_full, 1);
@@ -279,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       for (int t = 0; t < T; ++t) {
         const int st = t % C::kQStages;
         const uint32_t ph = (t / C::kQStages) & 1;
-        const int head = kvh * group + t / per_head;
+        const int head = kvh * group + (SPLIT ? (int)(blockIdx.y % HS) * gsz : 0) + t / per_head;
         const int q0 = (m_first + t % per_head) * BQ;
         mbar_wait(q_empty + st, ph ^ 1);
         mbar_arrive_expect_tx(q_full + st, C::TILE + (p.lse_tma ? 2 * 128 * 4 : 0));
@@ -433,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
     const bool row_dead = key >= p.S;
     for (int t = 0; t < T; ++t) {
-      const int head = kvh * group + t / per_head;
+      const int head = kvh * group + (SPLIT ? (int)(blockIdx.y % HS) * gsz : 0) + t / per_head;
       const int q0 = (m_first + t % per_head) * BQ;
       const uint32_t s_addr = tmem + lane_base + (t % C::NSB) * 128;
       const int st = t % C::kQStages;
@@ -567,6 +575,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       tc_fence_after();
       const uint32_t src = tmem + lane_base + (half ? C::DK_COL : C::DV_COL);
       const float sc = half ? p.scale : 1.f;
+      if constexpr (SPLIT) {  // GQA split: fp32 partials, finished by bwd_post
+        float* acc_row = p.dkv_acc + ((((int64_t)(half ? 0 : 1) * p.B + batch) * p.Hkv + kvh) *
+                                      p.S + key) * D;
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+          uint32_t a[32];
+          tmem_ld32(src + c, a);
+          tmem_wait_ld();
+          if (key < p.S) {
+#pragma unroll
+            for (int t4 = 0; t4 < 8; ++t4)
+              red_add_v4(acc_row + c + 4 * t4, a[4 * t4], a[4 * t4 + 1], a[4 * t4 + 2],
+                         a[4 * t4 + 3]);
+          }
+        }
+      } else {
       __nv_bfloat16* dst;
       if constexpr (PUSH) {  // fused K2: the row goes to the owner of token `key`
         const int j = min(key, p.S - 1) / p.s_loc;
@@ -595,6 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           }
         }
       }
+      }
     }
   } else if (warp >= kDrainWarp0 && warp < kDrainWarp0 + 4) {
     // ------------------------------------------------------------ dQ drain warpgroup
@@ -609,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     const bool leader = (warp == kDrainWarp0 && lane == 0);
     constexpr int NC = D / 32;  // 32-column chunks
     for (int t = 0; t < T; ++t) {
-      const int head = kvh * group + t / per_head;
+      const int head = kvh * group + (SPLIT ? (int)(blockIdx.y % HS) * gsz : 0) + t / per_head;
       const int q0 = (m_first + t % per_head) * BQ;
       const uint32_t dq_addr = tmem + lane_base + dq_col(t);
       // the slot of chunk 0 was last used two chunks ago: wait for that reduce to have
@@ -706,6 +731,12 @@ struct PrePost {
   char* peer_base[AUTOSP_MAX_WORLD];
   uint32_t* peer_flags[AUTOSP_MAX_WORLD];
   uint32_t epoch, check;
+  // GQA split: dK / dV finished here from the fp32 partials (rows after the dQ rows)
+  int Hkv;
+  int64_t rows_kv;  // B * Hkv * S (0 without the split)
+  const float* dkv_acc;
+  __nv_bfloat16 *dk, *dv;
+  int64_t dk_sb, dk_sh, dk_ss, dv_sb, dv_sh, dv_ss;
 };
 
 // delta[row] = sum_d dO*O ; nlse2[row] = -lse[row] * log2(e) ; dqacc[row, :] = 0.
@@ -753,6 +784,34 @@ __global__ void bwd_post_kernel(const __grid_constant__ PrePost a) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t row = gid / lpr;
   const int sub = (int)(gid % lpr);
+  if (row >= a.rows && row < a.rows + 2 * a.rows_kv) {  // GQA-split dK / dV rows
+    const int64_t r2 = row - a.rows;
+    const int which = (int)(r2 / a.rows_kv);               // 0 dK (scaled), 1 dV
+    const int64_t rr = r2 - which * a.rows_kv;
+    const int key = (int)(rr % a.S);
+    const int64_t bh = rr / a.S;
+    const int kvh = (int)(bh % a.Hkv);
+    const int64_t bi = bh / a.Hkv;
+    const float sc = which == 0 ? a.scale : 1.f;
+    const float4* src = reinterpret_cast<const float4*>(a.dkv_acc + r2 * a.D + sub * 8);
+    const float4 x = src[0], y = src[1];
+    uint4 v;
+    v.x = pack_bf16(x.x * sc, x.y * sc);
+    v.y = pack_bf16(x.z * sc, x.w * sc);
+    v.z = pack_bf16(y.x * sc, y.y * sc);
+    v.w = pack_bf16(y.z * sc, y.w * sc);
+    __nv_bfloat16* dst;
+    if (a.push) {
+      const int j = key / a.s_loc;
+      const int gh = a.Hq * a.P + (which ? a.Hkv * a.P : 0) + a.rank * a.Hkv + kvh;
+      dst = reinterpret_cast<__nv_bfloat16*>(a.peer_base[j] + a.dst_off) + bi * a.d_sb +
+            (int64_t)(key - j * a.s_loc) * a.d_ss + (int64_t)gh * a.d_sh;
+    } else {
+      dst = which == 0 ? a.dk + bi * a.dk_sb + kvh * a.dk_sh + (int64_t)key * a.dk_ss
+                       : a.dv + bi * a.dv_sb + kvh * a.dv_sh + (int64_t)key * a.dv_ss;
+    }
+    *reinterpret_cast<uint4*>(dst + sub * 8) = v;
+  }
   if (row < a.rows) {
     const int64_t bh = row / a.S;
     const int q = (int)(row % a.S);
@@ -776,6 +835,28 @@ __global__ void bwd_post_kernel(const __grid_constant__ PrePost a) {
     }
   }
   if (a.push) publish_arrival(a.peer_flags, a.P, a.rank, a.epoch, a.check, gridDim.x);
+}
+
+// GQA split of small grids: two CTAs per (key tile, kv head) when the grid would not fill
+// two waves of SMs (e.g. SP = 8 with one kv head per rank: 256 CTAs for 148 SMs, the
+// heaviest causal CTA then bounds the kernel).  AUTOSP_BWD_HSPLIT=1 disables, =2 forces.
+inline int choose_hsplit(int B, int Hq, int Hkv, int S) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("AUTOSP_BWD_HSPLIT");
+    mode = e ? atoi(e) : 0;
+  }
+  const int group = Hq / Hkv;
+  if (group % 2 || mode == 1) return 1;
+  if (mode == 2) return 2;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t ctas = (int64_t)((S + BK - 1) / BK) * Hkv * B;
+  return ctas < 2LL * sms ? 2 : 1;
 }
 
 inline bool make_map_f32_3d(CUtensorMap* map, void* ptr, int BH, int S, int D) {
@@ -816,6 +897,8 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   float* dqacc = static_cast<float*>(ws);
   float* delta = delta_in ? const_cast<float*>(delta_in) : dqacc + (size_t)B * Hq * S * D;
   float* nlse2 = dqacc + (size_t)B * Hq * S * D + (size_t)B * Hq * S;
+  const int hsplit = choose_hsplit(B, Hq, Hkv, S);
+  float* dkv_acc = hsplit > 1 ? nlse2 + (size_t)B * Hq * S : nullptr;
   PrePost a{};
   a.o = static_cast<const __nv_bfloat16*>(o.ptr);
   a.d_o = static_cast<const __nv_bfloat16*>(d_o.ptr);
@@ -833,6 +916,15 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   a.D = D;
   a.rows = (int64_t)B * Hq * S;
   a.scale = scale;
+  a.Hkv = Hkv;
+  a.rows_kv = hsplit > 1 ? (int64_t)B * Hkv * S : 0;
+  a.dkv_acc = dkv_acc;
+  a.dk = static_cast<__nv_bfloat16*>(const_cast<void*>(dk.ptr));
+  a.dv = static_cast<__nv_bfloat16*>(const_cast<void*>(dv.ptr));
+  a.dk_sb = dk.stride_b; a.dk_sh = dk.stride_h; a.dk_ss = dk.stride_s;
+  a.dv_sb = dv.stride_b; a.dv_sh = dv.stride_h; a.dv_ss = dv.stride_s;
+  if (hsplit > 1)
+    cudaMemsetAsync(dkv_acc, 0, (size_t)2 * B * Hkv * S * D * sizeof(float), stream);
   if (push) {
     a.push = 1;
     a.P = push->world;
@@ -887,6 +979,8 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   p.scale_log2 = scale * 1.4426950408889634f;
   p.causal = causal;
   p.n_ktiles = (S + BK - 1) / BK;
+  p.hsplit = hsplit;
+  p.dkv_acc = dkv_acc;
   if (push) {
     p.push = 1;
     p.P = a.P;
@@ -900,18 +994,23 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(attn_bwd_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::SMEM);
-    cudaFuncSetAttribute(attn_bwd_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::SMEM);
+    cudaFuncSetAttribute(attn_bwd_kernel<D, false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(attn_bwd_kernel<D, true, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(attn_bwd_kernel<D, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(attn_bwd_kernel<D, true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr_set = true;
   }
-  if (push)
-    attn_bwd_kernel<D, true><<<dim3(p.n_ktiles, Hkv, B), kThreads, C::SMEM, stream>>>(p);
-  else
-    attn_bwd_kernel<D, false><<<dim3(p.n_ktiles, Hkv, B), kThreads, C::SMEM, stream>>>(p);
+  const dim3 grid(p.n_ktiles, Hkv * hsplit, B);
+  if (push && hsplit > 1) attn_bwd_kernel<D, true, true><<<grid, kThreads, C::SMEM, stream>>>(p);
+  else if (push) attn_bwd_kernel<D, true, false><<<grid, kThreads, C::SMEM, stream>>>(p);
+  else if (hsplit > 1) attn_bwd_kernel<D, false, true><<<grid, kThreads, C::SMEM, stream>>>(p);
+  else attn_bwd_kernel<D, false, false><<<grid, kThreads, C::SMEM, stream>>>(p);
   {
-    const int64_t threads = a.rows * (D / 8);
+    const int64_t threads = (a.rows + 2 * a.rows_kv) * (D / 8);
     bwd_post_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(a);
   }
   cudaError_t e = cudaGetLastError();
@@ -925,8 +1024,12 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
 }  // namespace bwd
 }  // namespace autosp
 
-extern "C" size_t autosp_attn_bwd_workspace_bytes(int b, int hq, int s, int d) {
-  return (size_t)b * hq * s * (d + 2) * sizeof(float);  // dQ acc + delta + -lse*log2(e)
+extern "C" size_t autosp_attn_bwd_workspace_bytes(int b, int hq, int hkv, int s, int d) {
+  if (b < 1 || hq < 1 || hkv < 1 || s < 1 || d < 1 || hq % hkv) return 0;
+  size_t f = (size_t)b * hq * s * (d + 2);  // dQ acc + delta + -lse*log2(e)
+  if (autosp::bwd::choose_hsplit(b, hq, hkv, s) > 1)
+    f += (size_t)2 * b * hkv * s * d;  // GQA-split dK / dV partials
+  return f * sizeof(float);
 }
 
 static int attn_bwd_impl(autosp_attn_tensor q, autosp_attn_tensor k, autosp_attn_tensor v,
@@ -1054,12 +1157,18 @@ extern "C" AUTOSP_API int autosp_debug_set_bwd_trace(long long* dev_buf) {
 
 int autosp_preload_bwd() {
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<32, false>);
-  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<32, true>);
-  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<64, false>);
-  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<64, true>);
-  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<128, false>);
-  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<128, true>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<32, false, false>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<32, true, false>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<32, false, true>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<32, true, true>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<64, false, false>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<64, true, false>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<64, false, true>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<64, true, true>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<128, false, false>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<128, true, false>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<128, false, true>);
+  cudaFuncGetAttributes(&a, autosp::bwd::attn_bwd_kernel<128, true, true>);
   cudaFuncGetAttributes(&a, autosp::bwd::bwd_pre_kernel);
   cudaFuncGetAttributes(&a, autosp::bwd::bwd_post_kernel);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;

@@ -152,7 +152,7 @@ def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = Non
     dq = torch.empty((b, hq, s, d), dtype=torch.bfloat16, device=dev) if dq is None else dq
     dk = torch.empty((b, hkv, s, d), dtype=torch.bfloat16, device=dev) if dk is None else dk
     dv = torch.empty((b, hkv, s, d), dtype=torch.bfloat16, device=dev) if dv is None else dv
-    ws_total = lib.autosp_attn_bwd_workspace_bytes(b, hq, s, d)
+    ws_total = lib.autosp_attn_bwd_workspace_bytes(b, hq, hkv, s, d)
     if ws_total > BWD_WORKSPACE_BYTES and hkv > 1:
         n = 1
         while n < hkv and (hkv % (2 * n) == 0) and ws_total // n > BWD_WORKSPACE_BYTES:
@@ -166,7 +166,7 @@ def attn_bwd(q, k, v, o, do, lse, causal: bool = True, scale: float | None = Non
                          dq[:, qh], dk[:, kv], dv[:, kv],
                          None if delta is None else delta[:, qh].contiguous())
             return dq, dk, dv
-    ws = torch.empty(lib.autosp_attn_bwd_workspace_bytes(b, hq, s, d), dtype=torch.uint8,
+    ws = torch.empty(lib.autosp_attn_bwd_workspace_bytes(b, hq, hkv, s, d), dtype=torch.uint8,
                      device=dev)
     if not lse.is_contiguous() or lse.dtype != torch.float32:
         raise ValidationError("attn_bwd: lse must be contiguous fp32 [b, hq, s]")
@@ -205,7 +205,7 @@ def attn_bwd_push(q, k, v, do, lse, delta, scale: float, causal: bool, world: in
             delta.dtype != torch.float32 or not delta.is_contiguous() or \
             tuple(delta.shape) != (b, hq, s):
         raise ValidationError("attn_bwd_push: lse / delta must be contiguous fp32 [b, hq, s]")
-    ws = torch.empty(lib.autosp_attn_bwd_workspace_bytes(b, hq, s, d), dtype=torch.uint8,
+    ws = torch.empty(lib.autosp_attn_bwd_workspace_bytes(b, hq, hkv, s, d), dtype=torch.uint8,
                      device=q.device)
     pb = (C.c_void_p * world)(*peer_base)
     pf = (C.c_void_p * world)(*peer_flags)

@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_abi_version_and_sm100a_cubin(lib):
     from paper_2604_27089_b200 import _lib
-    assert lib.autosp_abi_version() == 2
+    assert lib.autosp_abi_version() == 3
     out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
