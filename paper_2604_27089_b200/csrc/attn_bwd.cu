@@ -33,6 +33,11 @@
 extern "C" void autosp_set_error(const char* fmt, ...);
 int autosp_check_attn_tensor(const autosp_attn_tensor& t, const char* name);
 
+#ifndef AUTOSP_BWD_LPT
+#define AUTOSP_BWD_LPT 0  // LPT grid layout (ptx.cuh); A/B: -3 % at the bench shape (L2 sharing
+#endif                    // of Q / dO between co-running key tiles), mixed at per-rank shapes
+#define BWD_RANK_IDX AUTOSP_BLOCK_RANK(AUTOSP_BWD_LPT)
+#define BWD_HEAD_IDX AUTOSP_BLOCK_HEAD(AUTOSP_BWD_LPT)
 #ifndef AUTOSP_BWD_EMU
 #define AUTOSP_BWD_EMU 2  // exps per 8 on the FMA pipe for d <= 64 (tools/emu sweep)
 #endif
@@ -212,9 +217,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   }
   const int warp = warp_id();
   const int lane = lane_id();
-  const int ktile = blockIdx.x;  // launch order = heaviest (most query tiles) first
+  const int ktile = BWD_RANK_IDX;  // launch order = heaviest (most query tiles) first
   constexpr int HS = SPLIT ? 2 : 1;                            // (compile-time: registers)
-  const int kvh = blockIdx.y / HS;
+  const int kvh = BWD_HEAD_IDX / HS;
   const int batch = blockIdx.z;
   const int group = p.Hq / p.Hkv;
   const int gsz = group / HS;                                  // q heads of this CTA
@@ -287,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       for (int t = 0; t < T; ++t) {
         const int st = t % C::kQStages;
         const uint32_t ph = (t / C::kQStages) & 1;
-        const int head = kvh * group + (SPLIT ? (int)(blockIdx.y % HS) * gsz : 0) + t / per_head;
+        const int head = kvh * group + (SPLIT ? (int)(BWD_HEAD_IDX % HS) * gsz : 0) + t / per_head;
         const int q0 = (m_first + t % per_head) * BQ;
         mbar_wait(q_empty + st, ph ^ 1);
         mbar_arrive_expect_tx(q_full + st, C::TILE + (p.lse_tma ? 2 * 128 * 4 : 0));
@@ -441,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
     const bool row_dead = key >= p.S;
     for (int t = 0; t < T; ++t) {
-      const int head = kvh * group + (SPLIT ? (int)(blockIdx.y % HS) * gsz : 0) + t / per_head;
+      const int head = kvh * group + (SPLIT ? (int)(BWD_HEAD_IDX % HS) * gsz : 0) + t / per_head;
       const int q0 = (m_first + t % per_head) * BQ;
       const uint32_t s_addr = tmem + lane_base + (t % C::NSB) * 128;
       const int st = t % C::kQStages;
@@ -634,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     const bool leader = (warp == kDrainWarp0 && lane == 0);
     constexpr int NC = D / 32;  // 32-column chunks
     for (int t = 0; t < T; ++t) {
-      const int head = kvh * group + (SPLIT ? (int)(blockIdx.y % HS) * gsz : 0) + t / per_head;
+      const int head = kvh * group + (SPLIT ? (int)(BWD_HEAD_IDX % HS) * gsz : 0) + t / per_head;
       const int q0 = (m_first + t % per_head) * BQ;
       const uint32_t dq_addr = tmem + lane_base + dq_col(t);
       // the slot of chunk 0 was last used two chunks ago: wait for that reduce to have
@@ -1004,7 +1009,7 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr_set = true;
   }
-  const dim3 grid(p.n_ktiles, Hkv * hsplit, B);
+  const dim3 grid = causal_grid(AUTOSP_BWD_LPT, p.n_ktiles, Hkv * hsplit, B);
   if (push && hsplit > 1) attn_bwd_kernel<D, true, true><<<grid, kThreads, C::SMEM, stream>>>(p);
   else if (push) attn_bwd_kernel<D, true, false><<<grid, kThreads, C::SMEM, stream>>>(p);
   else if (hsplit > 1) attn_bwd_kernel<D, false, true><<<grid, kThreads, C::SMEM, stream>>>(p);

@@ -41,6 +41,9 @@ extern "C" void autosp_set_error(const char* fmt, ...);
 #ifndef AUTOSP_FWD_MMA2
 #define AUTOSP_FWD_MMA2 1  // one MMA-issuing warp per Q tile for d <= 64 (A/B: +1.5 % at
 #endif                     // d = 64; -11 % at d = 128, where it stays off)
+#ifndef AUTOSP_FWD_LPT
+#define AUTOSP_FWD_LPT 1  // LPT grid layout (ptx.cuh; A/B: +1.6 % full shape, +37 % at 4 heads x 16K)
+#endif
 #ifndef AUTOSP_FWD_EMU128
 #define AUTOSP_FWD_EMU128 2  // exps per 8 on the FMA pipe for d = 128
 #endif
@@ -170,8 +173,8 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int qblk = p.n_qblk - 1 - blockIdx.x;  // heaviest causal blocks first
-  const int head = blockIdx.y;
+  const int qblk = p.n_qblk - 1 - (int)AUTOSP_BLOCK_RANK(AUTOSP_FWD_LPT);  // heaviest causal blocks first
+  const int head = AUTOSP_BLOCK_HEAD(AUTOSP_FWD_LPT);
   const int batch = blockIdx.z;
   const int kvhead = head / (p.Hq / p.Hkv);
   const int q0 = qblk * NQ * BM;
@@ -669,7 +672,7 @@ int launch(const autosp_attn_tensor& q, const autosp_attn_tensor& k, const autos
     cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr_set = true;
   }
-  dim3 grid(p.n_qblk, Hq, B);
+  const dim3 grid = causal_grid(AUTOSP_FWD_LPT, p.n_qblk, Hq, B);
   attn_fwd_kernel<D><<<grid, C::kThreads, C::SMEM, stream>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

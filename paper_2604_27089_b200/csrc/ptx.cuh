@@ -392,4 +392,19 @@ AUTOSP_DEV uint32_t atom_add_acqrel_gpu(uint32_t* p, uint32_t v) {
   return old;
 }
 
+// Grid layout of the causal attention kernels, whose per-block work falls with the block's
+// work rank (0 = most KV / Q tiles).  Blocks are dispatched in linear-id order (x fastest),
+// so with the rank on x the LAST head's heaviest block starts near the end of the grid and
+// sets the kernel's tail (at 4 heads x 16K tokens -- a per-rank shape at P = 8 -- that tail
+// cost the forward a third of its time).  LPT layout: head index on x, rank on y, so every
+// head's rank-0 block goes first, then rank 1 ... (longest processing time first, per batch
+// row).  The coordinates stay special registers (a computed linear-id remap instead cost
+// the backward 2.5 % in spills).  Used by the forward; the backward keeps rank-on-x, whose
+// co-running blocks share one head group's Q / dO stream in L2 (A/B in DESIGN.md).
+#define AUTOSP_BLOCK_RANK(LPT) ((LPT) ? blockIdx.y : blockIdx.x)
+#define AUTOSP_BLOCK_HEAD(LPT) ((LPT) ? blockIdx.x : blockIdx.y)
+inline dim3 causal_grid(bool lpt, unsigned n_rank, unsigned n_head, unsigned batch) {
+  return lpt ? dim3(n_head, n_rank, batch) : dim3(n_rank, n_head, batch);
+}
+
 }  // namespace autosp

@@ -1,13 +1,24 @@
 """Optimizer step inside the compiled backward on the Llama block (optim.AdamW, the bf16
-multi-tensor kernel), one GPU: two training steps give BIT-IDENTICAL parameters to the
-normal loop (backward, then optimizer.step()), every compiled parameter is updated inside
-the graph (only the eager LM head by step()), and when the backward returns the compiled
-parameters' gradients are already gone (the memory the normal loop holds until step())."""
+multi-tensor kernel), one GPU.
+
+* Bit-exact given the same gradients: every gradient the compiled backward hands to the
+  optimizer (and the eager LM head's, updated by step()) is recorded, and replaying them
+  through the normal loop (p.grad = g; optimizer.step()) from the same initial weights
+  gives BIT-IDENTICAL parameters after two steps.  (Comparing two independent training
+  runs bit for bit is not possible: the attention backward accumulates dQ over key tiles
+  with fp32 atomics, whose order -- and so the last bit -- varies run to run, as in
+  FlashAttention; tools/bwd_determinism.py measures it.)
+* Against an independent normal run the parameters agree up to that noise.
+* Every compiled parameter is updated inside the graph (only the eager LM head by
+  step()), and when the backward returns the compiled parameters' gradients are already
+  gone (the memory the normal loop holds until step())."""
 
 import pytest
 import torch
 
 pytestmark = pytest.mark.gpu
+
+_LR = 1e-3
 
 
 def _run(in_backward: bool, mode: str):
@@ -21,11 +32,23 @@ def _run(in_backward: bool, mode: str):
     autosp.dist.init(1)
     torch.manual_seed(0)
     model = LlamaDecoder(cfg, dtype=torch.bfloat16, device="cuda")
-    opt = AdamW(model.parameters(), lr=1e-3)
+    init = [p.detach().clone() for p in model.parameters()]
+    index = {id(p): i for i, p in enumerate(model.parameters())}
+    opt = AdamW(model.parameters(), lr=_LR)
+    recorded = []  # per step: {param index: gradient}
+    inner = opt.step_params
+
+    def recording_step_params(pairs):
+        for p, g in pairs:
+            recorded[-1][index[id(p)]] = g.detach().clone()
+        inner(pairs)
+
+    opt.step_params = recording_step_params
     cm = autosp.compile(model, optimizer=opt if in_backward else None)
     g = torch.Generator().manual_seed(3)
     peaks, after_bwd = [], []
     for _ in range(2):
+        recorded.append({})
         ids = torch.randint(0, cfg.vocab, (1, 4097), generator=g).cuda()
         torch.cuda.synchronize()
         torch.cuda.reset_peak_memory_stats()
@@ -35,6 +58,9 @@ def _run(in_backward: bool, mode: str):
         peaks.append(torch.cuda.max_memory_allocated())
         after_bwd.append(torch.cuda.memory_allocated())
         n_grads = sum(p.grad is not None for p in model.parameters())
+        for p in model.parameters():  # what step() will apply
+            if p.grad is not None:
+                recorded[-1][index[id(p)]] = p.grad.detach().clone()
         opt.step()
         opt.zero_grad(set_to_none=True)
     torch.cuda.synchronize()
@@ -42,15 +68,35 @@ def _run(in_backward: bool, mode: str):
     torch._dynamo.reset()
     grad_bytes = sum(p.numel() * p.element_size() for p in model.parameters()
                      if p is not model.lm_head)
-    return params, (peaks, after_bwd, grad_bytes), n_grads, dict(opt_in_bw.LAST)
+    return (params, init, recorded), (peaks, after_bwd, grad_bytes), n_grads, \
+        dict(opt_in_bw.LAST)
+
+
+def _replay(init, recorded):
+    """The normal loop (gradients in .grad, then optimizer.step()) fed the recorded
+    gradients, from the same initial weights."""
+    from paper_2604_27089_b200.optim import AdamW
+    params = [torch.nn.Parameter(t.clone()) for t in init]
+    opt = AdamW(params, lr=_LR)
+    for grads in recorded:
+        assert len(grads) == len(params)
+        for i, p in enumerate(params):
+            p.grad = grads[i]
+        opt.step()
+        opt.zero_grad(set_to_none=True)
+    torch.cuda.synchronize()
+    return [p.detach() for p in params]
 
 
 @pytest.mark.parametrize("mode", ["seq-aware", "auto"])
 def test_optimizer_in_backward_bit_exact_and_frees_gradients(mode):
-    ref, ref_peaks, ref_grads, _ = _run(False, mode)
-    got, peaks, n_grads, info = _run(True, mode)
-    for a, b in zip(got, ref):
+    (ref, _, _), ref_peaks, ref_grads, _ = _run(False, mode)
+    (got, init, recorded), peaks, n_grads, info = _run(True, mode)
+    for a, b in zip(got, _replay(init, recorded)):  # same gradients -> same bits
         assert torch.equal(a, b)
+    for a, b, a0 in zip(got, ref, init):  # independent normal run: equal up to the dQ
+        upd = (a.float() - a0.float()).norm()  # atomics (last-bit flips of the updates)
+        assert (a.float() - b.float()).norm() <= 0.1 * upd, ((a != b).float().mean(), upd)
     assert info["updated_in_graph"] == 2 * 6 + 2  # 6 weights per block + embedding + norm
     assert n_grads == 1 and ref_grads == 2 * 6 + 3  # only the eager LM head keeps a .grad
     (pk_ref, ab_ref, gbytes), (pk, ab, _) = ref_peaks, peaks

@@ -8,7 +8,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch
 from paper_2604_27089_b200 import kernels as K
 
-for (hq, hkv, s, d) in [(4, 1, 32768, 64), (4, 1, 131072, 128), (4, 1, 16384, 64)]:
+for (hq, hkv, s, d) in [(32, 8, 32768, 64), (4, 1, 32768, 64), (4, 1, 131072, 128),
+                        (4, 1, 16384, 64)]:
     q = torch.randn(1, hq, s, d, device="cuda").bfloat16()
     k = torch.randn(1, hkv, s, d, device="cuda").bfloat16()
     v = torch.randn_like(k)
