@@ -41,7 +41,8 @@ from .errors import ValidationError
 BUCKET_BYTES = 64 << 20
 COVERED = "_autosp_grad_sync"   # set on every parameter of a model compiled with grad sync
 IN_GRAPH = "_autosp_in_graph"   # set on parameters reduced inside a compiled backward
-_PENDING: list = []             # async reductions issued by the eager hooks
+_ACCUMULATED = "_autosp_grad_accumulated"  # this backward's contribution reduced apart
+_PENDING: list = []             # (work, param, contribution) issued by the eager hooks
 LAST: dict = {}                 # stats of the last rewritten backward graph (tests/tools)
 
 
@@ -161,30 +162,61 @@ def insert(bw: torch.fx.GraphModule, param_index: list[int], params: list, n_inp
 
 
 def _join_pending():
-    works, _PENDING[:] = list(_PENDING), []
-    for w in works:
-        w.wait()
+    """End of a backward that issued eager reductions: wait for them; an accumulated
+    contribution (see install) is added to its parameter's .grad here."""
+    items, _PENDING[:] = list(_PENDING), []
+    for work, p, contrib in items:
+        work.wait()
+        if p is not None:
+            p.grad.add_(contrib)
+
+
+def _enqueue(work, p=None, contrib=None):
+    if not _PENDING:  # first eager reduction of this backward: join them at its end
+        torch.autograd.Variable._execution_engine.queue_callback(_join_pending)
+    _PENDING.append((work, p, contrib))
 
 
 def install(model: torch.nn.Module, dp_size: int) -> None:
     """Mark every parameter of `model` as reduced by the compiled backward, and hook the
-    ones that end up used outside it (see module doc).  Idempotent per parameter."""
+    ones that end up used outside it (see module doc).  Idempotent per parameter.
+
+    Eager parameters: the usual case (no .grad yet) reduces the accumulated .grad in
+    place after accumulation (post-accumulate hook, async, joined at the end of the
+    backward).  Gradient accumulation (.grad already holds earlier micro-batches' reduced
+    gradients) must reduce only THIS backward's contribution: the tensor hook takes it,
+    starts its reduction on a copy and hands autograd zeros instead; the reduced copy is
+    added to .grad when the backward ends."""
     scale = 1.0 / dp_size
 
-    def hook(p):
-        if getattr(p, IN_GRAPH, False) or p.grad is None:
-            return
-        g = p.grad
-        if scale != 1.0:
-            g.mul_(scale)
-        if not _PENDING:  # first eager reduction of this backward: join them at its end
-            torch.autograd.Variable._execution_engine.queue_callback(_join_pending)
-        _PENDING.append(tdist.all_reduce(g, async_op=True))
+    def make_hooks(p):
+        def contribution(g):  # before accumulation
+            if getattr(p, IN_GRAPH, False) or p.grad is None:
+                return None
+            red = g * scale if scale != 1.0 else g.clone()
+            _enqueue(tdist.all_reduce(red, async_op=True), p, red)
+            setattr(p, _ACCUMULATED, True)
+            return torch.zeros_like(g)
+
+        def accumulated(p):  # after accumulation
+            if getattr(p, IN_GRAPH, False) or p.grad is None:
+                return
+            if getattr(p, _ACCUMULATED, False):  # reduced separately (contribution)
+                setattr(p, _ACCUMULATED, False)
+                return
+            g = p.grad
+            if scale != 1.0:
+                g.mul_(scale)
+            _enqueue(tdist.all_reduce(g, async_op=True))
+
+        return contribution, accumulated
 
     for p in model.parameters():
         if p.requires_grad and not getattr(p, COVERED, False):
             setattr(p, COVERED, True)
-            p.register_post_accumulate_grad_hook(hook)
+            contribution, accumulated = make_hooks(p)
+            p.register_hook(contribution)
+            p.register_post_accumulate_grad_hook(accumulated)
 
 
 def consume(params) -> list:

@@ -57,7 +57,7 @@ def _graph_break_decoder(dims, dtype, in_loop=False):
 
 
 def _worker(rank, world, port, dims_t, seed, passes, mode, q, graph_breaks=False, sp=None,
-            grad_sync=False):
+            grad_sync=False, accum=1):
     import torch.distributed as tdist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), AUTOSP_GRAD_BUCKET_BYTES=str(8 << 10))
@@ -80,12 +80,15 @@ def _worker(rank, world, port, dims_t, seed, passes, mode, q, graph_breaks=False
         model = (_graph_break_decoder(dims, torch.float64, graph_breaks == "loop")
                  if graph_breaks else SeqcompDecoder(dims, dtype=torch.float64))
         model.load_reference(params)
+        if grad_sync:  # a parameter used OUTSIDE the compiled graph (eager hook path)
+            model.loss_scale = torch.nn.Parameter(torch.ones((), dtype=torch.float64))
         cm = autosp.compile(model)
         sl = dims.s // sp
         r_sp = rank % sp
         ids_r = torch.from_numpy(ids[:, r_sp * sl:(r_sp + 1) * sl].copy())
-        hidden, loss = cm(ids_r)
-        loss.backward()
+        for _ in range(accum):  # gradient accumulation: micro-batches before the step
+            hidden, loss = cm(ids_r)
+            (loss * model.loss_scale if grad_sync else loss).backward()
         grads = {k: p.grad.detach().clone() for k, p in model.named_reference_params().items()}
         local_loss = float(loss)
         autosp.dist.reduce_gradients(list(model.named_reference_params().values()), st)
@@ -99,6 +102,7 @@ def _worker(rank, world, port, dims_t, seed, passes, mode, q, graph_breaks=False
             red = dict(red, **{"after_adamw/" + k: p.detach().numpy().copy()
                                for k, p in model.named_reference_params().items()})
         plan = dict(sp_ac.LAST_PLAN, grad_sync=dict(gsync.LAST),
+                    eager_grad=float(model.loss_scale.grad) if grad_sync else None,
                     in_graph=sum(bool(getattr(p, gsync.IN_GRAPH, False))
                                  for p in model.parameters()))
         q.put((rank, hidden.detach().numpy(), local_loss, red,
@@ -113,12 +117,12 @@ def _worker(rank, world, port, dims_t, seed, passes, mode, q, graph_breaks=False
 
 
 def _run(world, dims_t, seed, passes=("auto_sp", "sp_ac"), mode="seq-aware", graph_breaks=False,
-         sp=None, grad_sync=False):
+         sp=None, grad_sync=False, accum=1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, dims_t, seed, list(passes), mode, q,
-                                               graph_breaks, sp, grad_sync))
+                                               graph_breaks, sp, grad_sync, accum))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -212,17 +216,20 @@ def test_c1_size_world2_matches_reference_fixture(golden_dir):
         assert o[5]["mode_applied"] == "seq-aware" and o[5]["recomputed_fw_nodes"]
 
 
-@pytest.mark.parametrize("world,sp", [(2, 2), (4, 2)])
-def test_in_graph_grad_sync_listing1_loop(world, sp):
+@pytest.mark.parametrize("world,sp,accum", [(2, 2, 1), (4, 2, 1), (2, 2, 2)])
+def test_in_graph_grad_sync_listing1_loop(world, sp, accum):
     """Listing 1's unchanged loop: loss.backward() alone leaves every
     rank with the FULL gradient -- summed over the SP group inside the compiled backward
     (grad_sync.py), averaged over data-parallel replicas -- no reduce_gradients call.
     world 4 = SP 2 x DP 2 (paper's ZeRO-1 runs use SP x DP): each DP
     replica trains on its own batch; expected = mean over replicas of the oracle's
-    summed SP gradients."""
+    summed SP gradients.  accum 2: two backward passes before the step (gradient
+    accumulation) -- each contribution reduced once.  A scalar parameter used outside the
+    compiled graph (loss * loss_scale) checks the eager-hook path: its gradient is the
+    sum of the SP ranks' losses."""
     dims_t = (1, 16, 4, 4, 8, 2, 64)
     seed = 11
-    out = _run(world, dims_t, seed=seed, sp=sp, grad_sync=True)
+    out = _run(world, dims_t, seed=seed, sp=sp, grad_sync=True, accum=accum)
     dims = orc.Dims(*dims_t)
     _, params = orc.random_leaves(dims, seed)
     refs = []
@@ -230,7 +237,9 @@ def test_in_graph_grad_sync_listing1_loop(world, sp):
         ids = orc.random_leaves(dims, seed + 1 + dp)[0] if world > sp else \
             orc.random_leaves(dims, seed)[0]
         refs.append(orc.sp_forward_backward(dims, ids, params, sp))
-    want = {k: sum(r.total_grads()[k] for r in refs) / len(refs) for k in refs[0].total_grads()}
+    want = {k: accum * sum(r.total_grads()[k] for r in refs) / len(refs)
+            for k in refs[0].total_grads()}
+    want_eager = accum * sum(sum(r.loss) for r in refs) / len(refs)
     for r, (_, hidden, loss, red, grads, plan, prov) in enumerate(out):
         ref = refs[r // sp]
         assert orc.max_rel_err(hidden, ref.hidden[r % sp]) <= 1e-10
@@ -241,6 +250,7 @@ def test_in_graph_grad_sync_listing1_loop(world, sp):
         # reduced INSIDE the backward graph: every parameter, in >1 bucket (8 KB buckets
         # here), the first issued well before the graph's end (overlap with the backward)
         gs = plan["grad_sync"]
+        assert abs(plan["eager_grad"] - want_eager) <= 1e-10 * abs(want_eager), r
         assert plan["in_graph"] == len(want) == gs["params"]
         assert gs["buckets"] > 1 and gs["start_positions"][0] < 0.8 * gs["nodes"]
         # ZeRO-1 step on the already-reduced gradients == AdamW on the expected gradients
