@@ -41,6 +41,9 @@ extern "C" void autosp_set_error(const char* fmt, ...);
 #ifndef AUTOSP_FWD_MMA2
 #define AUTOSP_FWD_MMA2 1  // one MMA-issuing warp per Q tile for d <= 64 (A/B: +1.5 % at
 #endif                     // d = 64; -11 % at d = 128, where it stays off)
+#ifndef AUTOSP_FWD_EARLY_K
+#define AUTOSP_FWD_EARLY_K 1  // wait for K_{j+1} before s_free (off the hand-off path)
+#endif
 #ifndef AUTOSP_FWD_LPT
 #define AUTOSP_FWD_LPT 1  // LPT grid layout (ptx.cuh; A/B: +1.6 % full shape, +37 % at 4 heads x 16K)
 #endif
@@ -233,11 +236,13 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
         const int st = j % C::kStages;
         const uint32_t ph = (j / C::kStages) & 1;
         mbar_wait(k_empty + st, ph ^ 1);
+        FWD_TRACE(8, j);
         mbar_arrive_expect_tx(k_full + st, C::KTILE);
         for (int c = 0; c < C::NCH; ++c)
           tma_load_4d(smem + C::K_OFF + st * C::KTILE + c * BN * C::SW, &p.tm_k,
                       k_full + st, c * C::CE, j * BN, kvhead, batch, pol_kv);
         mbar_wait(v_empty + st, ph ^ 1);
+        FWD_TRACE(9, j);
         mbar_arrive_expect_tx(v_full + st, C::KTILE);
         for (int c = 0; c < C::NCH; ++c)
           tma_load_4d(smem + C::V_OFF + st * C::KTILE + c * BN * C::SW, &p.tm_v,
@@ -300,15 +305,22 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
         const int st1 = (j + 1) % C::kStages;
         const uint32_t ph1 = ((j + 1) / C::kStages) & 1;
         mbar_wait(v_full + st, ph);
-        if (lane == 0) FWD_TRACE(14, j);
+        if (lane == 0 && i_lo == 0) FWD_TRACE(14, j);
         bool k_next_ready = false;
         auto need_k_next = [&]() {
           if (!k_next_ready) {
+            if (lane == 0 && i_lo == 0) FWD_TRACE(11, j);
             mbar_wait(k_full + st1, ph1);
+            if (lane == 0 && i_lo == 0) FWD_TRACE(10, j);
             tc_fence_after();
             k_next_ready = true;
           }
         };
+        // K_{j+1} (loaded long ago: the ring runs stages ahead) is checked here, not
+        // between s_free / PV(j) and the QK_i(j+1) it feeds: an mbarrier check costs this
+        // warp ~100-300 cycles even when the phase is complete, and there it would sit on
+        // the softmax's critical path (tools/fwd_trace.py: -170 cycles per KV tile, +4.5 %)
+        if (AUTOSP_FWD_EARLY_K && next) need_k_next();
         for (int i = i_lo; i < i_hi; ++i) {
           if (j >= n_tiles[i]) continue;
           if (C::SEP_P && j + 1 < n_tiles[i]) {
@@ -460,7 +472,6 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
           tc_fence_before();
           mbar_arrive_warp(p_full + i);
           if (lane == 0 && (warp & 3) == 0) FWD_TRACE(6 + i, j);
-          if (lane == 0 && i == 0) FWD_TRACE(8 + (warp & 3), j);
           continue;
         }
       }
@@ -553,7 +564,6 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
       tc_fence_before();
       mbar_arrive_warp(p_full + i);
       if (lane == 0 && (warp & 3) == 0) FWD_TRACE(6 + i, j);
-      if (lane == 0 && i == 0) FWD_TRACE(8 + (warp & 3), j);
     }
     // ---- epilogue: O / l -> bf16, LSE
     if (n > 0) {

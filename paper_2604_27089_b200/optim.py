@@ -11,6 +11,7 @@ import ctypes as C
 import torch
 
 from . import _lib
+from .errors import ValidationError
 
 UPDATED = "_autosp_updated"  # set by step_params (update done inside the backward)
 
@@ -39,6 +40,12 @@ class AdamW(torch.optim.Optimizer):
             for p in group["params"]:
                 if getattr(p, UPDATED, False):
                     setattr(p, UPDATED, False)
+                    if p.grad is not None:  # a gradient from outside the compiled graph
+                        raise ValidationError(
+                            "optim.AdamW: a parameter updated inside the compiled backward "
+                            "also has a .grad from code outside it (a weight shared between "
+                            "the compiled model and eager code) -- not supported with "
+                            "compile(optimizer=...)")
                 elif p.grad is not None:
                     live.append(p)
             self._apply(group, [(p, p.grad) for p in live])
@@ -48,9 +55,19 @@ class AdamW(torch.optim.Optimizer):
     def step_params(self, pairs) -> None:
         """AdamW on the given (parameter, gradient) pairs right now -- called from inside
         a compiled backward graph (optimizer in the backward: the gradient is freed as
-        soon as its parameter is updated); the next ``step()`` skips these parameters."""
+        soon as its parameter is updated); the next ``step()`` skips these parameters.
+        ``step()`` must run once per iteration (Listing 1's loop): a second in-backward
+        update of a parameter before it means two compiled graphs both own the parameter
+        (a weight shared across a graph break), each with a partial gradient -- refused."""
         for group in self.param_groups:
             mine = [(p, g) for p, g in pairs if any(p is q for q in group["params"])]
+            for p, _ in mine:
+                if getattr(p, UPDATED, False):
+                    raise ValidationError(
+                        "optim.AdamW: parameter updated twice inside the backward before "
+                        "step(): either step() was not called after the last iteration, or "
+                        "the parameter is used by two compiled graphs (shared across a graph "
+                        "break) -- not supported with compile(optimizer=...)")
             if mine:
                 self._apply(group, mine)
                 for p, _ in mine:

@@ -103,3 +103,47 @@ def test_optimizer_in_backward_bit_exact_and_frees_gradients(mode):
     print("after backward (normal, in-backward):", ab_ref[-1], ab[-1], "peak:", pk_ref[-1], pk[-1])
     if mode == "auto":  # save-all: nothing recomputed, the gradients are all that is freed
         assert ab[-1] <= ab_ref[-1] - 0.9 * gbytes, (ab, ab_ref, gbytes)
+
+
+class _Tiny(torch.nn.Module):
+    def __init__(self):
+        super().__init__()
+        self.w = torch.nn.Parameter(torch.randn(32, 32, device="cuda").bfloat16())
+
+    def forward(self, x):
+        return (x @ self.w.t()).float().pow(2).sum()
+
+
+def _tiny_compiled():
+    from paper_2604_27089_b200 import compiler
+    from paper_2604_27089_b200.optim import AdamW
+    torch._dynamo.reset()
+    net = _Tiny()
+    opt = AdamW(net.parameters(), lr=1e-3)
+    cm = torch.compile(net, backend=compiler.backend([], optimizer=opt), dynamic=False)
+    return net, opt, cm, torch.randn(8, 32, device="cuda").bfloat16()
+
+
+def test_weight_shared_with_eager_code_is_refused():
+    """A parameter updated inside the backward that ALSO got an eager gradient (a weight
+    shared between the compiled model and eager code) would lose that gradient: step()
+    refuses."""
+    from paper_2604_27089_b200.errors import ValidationError
+    net, opt, cm, x = _tiny_compiled()
+    (cm(x) + net.w.float().sum()).backward()
+    with pytest.raises(ValidationError, match="outside"):
+        opt.step()
+    torch._dynamo.reset()
+
+
+def test_second_update_without_step_is_refused():
+    """step() runs once per iteration (Listing 1); a second in-backward update before it
+    (or a parameter owned by two compiled graphs) is refused, not applied twice."""
+    from paper_2604_27089_b200.errors import ValidationError
+    net, opt, cm, x = _tiny_compiled()
+    cm(x).backward()
+    opt.step()
+    cm(x).backward()  # fine: step() ran in between
+    with pytest.raises(Exception, match="updated twice"):
+        cm(x).backward()
+    torch._dynamo.reset()

@@ -18,12 +18,15 @@ torch.cuda.synchronize()
 lib.autosp_debug_set_fwd_trace(None)
 t = buf.view(16, 64).cpu()
 names = ["mma:p_full0", "mma:p_full1", "mma:o_done0", "mma:o_done1", "sm0:s_full", "sm1:s_full",
-         "sm0:p_arrive", "sm1:p_arrive", "w0:parr", "w1:parr", "w2:parr", "w3:parr",
-         "mma:s_free0", "mma:qk0_issued", "mma:v_full", "w0:s_free_arr"]
+         "sm0:p_arrive", "sm1:p_arrive", "tma:K_issue(j)", "tma:V_issue(j)", "mma0:k_full(j+1)ok", "mma0:k_full(j+1)wait",
+         "mma0:s_free0", "mma0:qk0_issued", "mma0:v_full", "w0:s_free_arr"]
 base = int(t[4, 0])
 for j in range(10, 14):
-    print(f"j={j}:")
-    for i, n in enumerate(names):
-        print(f"    {n:16s} {int(t[i, j]) - base:8d}")
+    b = int(t[4, j])
+    print(f"j={j}: (cycles after sm0:s_full of this tile)")
+    for i in sorted(range(16), key=lambda i: int(t[i, j])):
+        print(f"    {names[i]:18s} {int(t[i, j]) - b:8d}")
+print("K(j+1) issue -> ready (tma:K_issue(j+1) -> mma0 k_full(j+1) passed):",
+      [int(t[10, j] - t[8, j + 1]) for j in range(8, 40)])
 print("per-tile cycles (sm0 s_full deltas):", [int(t[4, i + 1] - t[4, i]) for i in range(8, 40)])
 print("sm0 softmax time per tile:", [int(t[6, i] - t[4, i]) for i in range(8, 24)])
