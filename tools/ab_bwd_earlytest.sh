@@ -1,0 +1,4 @@
+# same-box A/B of AUTOSP_BWD_EARLY_TEST: bash tools/ab_bwd_earlytest.sh
+timeout 900 python -m pytest tests/test_kernels_gpu.py -q -x -p no:cacheprovider -k "bwd or running_max" > gpurun_out/t_et.log 2>&1
+for i in 1 2; do for v in et0 et1; do echo "== $v"; AUTOSP_LIB=tools/emu/libautosp_$v.so timeout 300 python tools/bwd_split_bench.py; done; done > gpurun_out/ab_et.txt 2>&1
+rm -f gpurun_out/abs.txt; bash tools/ab_step.sh "et0 et1"
