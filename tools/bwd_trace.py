@@ -26,3 +26,5 @@ for step in range(8, 16):
     row = "  ".join(f"{n}={int(t[i, step]) - base:8d}" for i, n in enumerate(names) if int(t[i, step]) > 0)
     print(f"t={step}: {row}")
 print("per-step cycles (dP issue deltas):", [int(t[1, i + 1] - t[1, i]) for i in range(8, 40)])
+print("per-step cycles (softmax loop-top deltas):", [int(t[12, i + 1] - t[12, i]) for i in range(8, 40)])
+print("softmax wait for dP (dp_full - p_arrive):", [int(t[7, i] - t[6, i]) for i in range(8, 40)])
