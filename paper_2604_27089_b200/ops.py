@@ -12,7 +12,7 @@ other strides).  ``all_to_all`` is the reference's AllToAll node
 launch; its gradient is the inverse-direction all-to-all (``autodiff.py:252-262``).
 
 The ops have CUDA kernels only.  There is no CPU kernel in the product: calling them on
-CPU tensors raises.  (``testing.enable_cpu_lowering()`` registers a test-only CPU/gloo
+CPU tensors raises.  (``tests/autosp_cpu_lowering.py``: ``enable_cpu_lowering()`` registers a test-only CPU/gloo
 lowering used by the multi-process CPU tests.)
 """
 

@@ -31,8 +31,8 @@ def enable_cpu_lowering() -> None:
     global _ENABLED
     if _ENABLED:
         return
-    from . import dist as sp_dist
-    from . import ops  # noqa: F401  (defines the ops)
+    from paper_2604_27089_b200 import dist as sp_dist
+    from paper_2604_27089_b200 import ops  # noqa: F401  (defines the ops)
 
     @torch.library.register_kernel("autosp::attention", "cpu")
     def _attention_cpu(q, k, v, scale, causal):
@@ -111,7 +111,7 @@ def loopback_states(P: int, nbytes: int, device="cuda", prefix: str = "loop"):
     receive region and flag block is a local allocation and each rank's pool maps all of
     them, so the real push kernels and epoch protocol run unchanged.  Returns the
     SPStates (group names f"{prefix}{r}") and the backing buffers (keep them alive)."""
-    from . import dist as sp_dist
+    from paper_2604_27089_b200 import dist as sp_dist
     flags = torch.zeros((P, 1024), dtype=torch.int32, device=device)
     regions = [torch.empty(nbytes, dtype=torch.uint8, device=device) for _ in range(P)]
     peers = [(flags[j].data_ptr(), regions[j].data_ptr()) for j in range(P)]

@@ -13,6 +13,9 @@ import pytest
 ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
+# test helpers (autosp_cpu_lowering: the test-only CPU/gloo lowering of the custom ops)
+if str(ROOT / "tests") not in sys.path:
+    sys.path.insert(0, str(ROOT / "tests"))
 GOLDEN = ROOT / "tests" / "golden"
 
 

@@ -111,7 +111,8 @@ def test_ulysses_block_virtual_ranks_one_gpu(P, hq, hkv, d):
     """P virtual ranks (threads + streams) run the REAL push kernels, epoch flags and
     pool allocator concurrently on one GPU; forward and backward must equal the
     single-rank attention (the SP-equivalence criterion, test_acceptance.py:57-102)."""
-    from paper_2604_27089_b200 import kernels, testing
+    from paper_2604_27089_b200 import kernels
+    import autosp_cpu_lowering as testing
     states, keep = testing.loopback_states(P, 64 << 20)
     b, s = 1, 128 * P
     g = torch.Generator().manual_seed(P)
@@ -171,7 +172,8 @@ def test_rope_fused_reshard_block_virtual_ranks(P, hq, hkv, d, b):
     attention epilogue pushing O, and the packed-gradient gather in backward: equal to the
     unsharded qkv_rope -> attention reference (forward bit-exact, gradients within bf16
     tolerance)."""
-    from paper_2604_27089_b200 import kernels, ops, testing
+    from paper_2604_27089_b200 import kernels, ops
+    import autosp_cpu_lowering as testing
     states, keep = testing.loopback_states(P, 64 << 20, prefix=f"qkv{P}_{b}_")
     s = 128 * P
     g = torch.Generator().manual_seed(P + d)
@@ -254,7 +256,7 @@ def _grad_out_rank(st, dot_full, o_full, results, r, P):
 def test_grad_out_reshard_virtual_ranks(P, H, d):
     """autosp_a2a_grad_out: the dO reshard (bit-exact vs the plain push kernel) fused with
     delta = rowsum(dO * O) (vs an fp64 reference), P virtual ranks on one GPU."""
-    from paper_2604_27089_b200 import testing
+    import autosp_cpu_lowering as testing
     states, keep = testing.loopback_states(P, 32 << 20, prefix=f"gor{P}_{d}_")
     b, s = 2, 64 * P
     g = torch.Generator().manual_seed(P * d)

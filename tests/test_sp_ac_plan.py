@@ -12,7 +12,8 @@ import torch
 def _plan(layers, s, mode="seq-aware"):
     torch._dynamo.reset()
     import paper_2604_27089_b200 as autosp
-    from paper_2604_27089_b200 import sp_ac, testing
+    from paper_2604_27089_b200 import sp_ac
+    import autosp_cpu_lowering as testing
     from paper_2604_27089_b200.workloads import LlamaConfig, LlamaDecoder
     testing.enable_cpu_lowering()
     cfg = LlamaConfig("t", 256, layers, 4, 2, 512, vocab=128)
@@ -94,7 +95,8 @@ def test_random_ops_are_never_recomputed(mode):
 def _seqcomp_plan(mode, dims_t=(1, 64, 4, 8, 32, 2, 64)):
     torch._dynamo.reset()
     import paper_2604_27089_b200 as autosp
-    from paper_2604_27089_b200 import ops, sp_ac, testing
+    from paper_2604_27089_b200 import ops, sp_ac
+    import autosp_cpu_lowering as testing
     from paper_2604_27089_b200.workloads import SeqcompDecoder, SeqcompDims
     testing.enable_cpu_lowering()
     ops.ATTN_DTYPE = None

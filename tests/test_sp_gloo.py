@@ -65,7 +65,8 @@ def _worker(rank, world, port, dims_t, seed, passes, mode, q, graph_breaks=False
     try:
         tdist.init_process_group("gloo", rank=rank, world_size=world)
         import paper_2604_27089_b200 as autosp
-        from paper_2604_27089_b200 import compiler, ops, sp_ac, testing
+        from paper_2604_27089_b200 import compiler, ops, sp_ac
+        import autosp_cpu_lowering as testing
         from paper_2604_27089_b200.workloads import SeqcompDecoder, SeqcompDims
         testing.enable_cpu_lowering()
         ops.ATTN_DTYPE = None  # keep fp64 end to end on CPU

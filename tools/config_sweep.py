@@ -21,6 +21,10 @@ CONFIGS = [  # name, P, hq, hkv, d, s, layers
 ]
 
 
+_pk = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
+PEAK = json.loads(_pk.read_text()).get("bf16_tflops_sustained", 1400.0) if _pk.exists() else 1400.0
+
+
 def timed(fn, iters):
     fn()
     torch.cuda.synchronize()
@@ -52,6 +56,8 @@ for name, P, hq, hkv, d, s, L in CONFIGS:
         "config": name, "per_rank_heads": [ql, kl], "seq": s, "head_dim": d,
         "attn_fwd_ms_per_layer": tf, "attn_fwd_tflops": fl / tf / 1e9,
         "attn_bwd_ms_per_layer": tb, "attn_bwd_tflops": 2.5 * fl / tb / 1e9,
+        "attn_fwd_frac_of_sustained_peak": fl / tf / 1e9 / PEAK,
+        "attn_bwd_frac_of_sustained_peak": 2.5 * fl / tb / 1e9 / PEAK,
         "attention_ms_per_step": L * (tf + tb),
         "a2a_qkv_loopback_ms_all_ranks": ta, "a2a_bytes_sent_per_rank": per_rank_bytes,
         "a2a_nvlink_model_ms": per_rank_bytes * (P - 1) / P / 770e9 * 1e3}), flush=True)
