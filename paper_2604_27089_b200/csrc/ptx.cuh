@@ -93,15 +93,28 @@ AUTOSP_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+#ifndef AUTOSP_MBAR_HINT
+#define AUTOSP_MBAR_HINT 0  // try_wait suspend-time hint (ns); 0 = none: measured +1-1.5 % K3/K4 vs 1e6
+#endif
 AUTOSP_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
+#if AUTOSP_MBAR_HINT > 0
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, 1000000;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "n"(AUTOSP_MBAR_HINT)
+      : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
       "selp.b32 %0, 1, 0, P;\n\t}\n"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+#endif
   return ok != 0;
 }
 // Wait for the phase with the given parity to complete.  Bounded: after ~4 s the
