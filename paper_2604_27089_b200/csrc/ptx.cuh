@@ -119,7 +119,13 @@ AUTOSP_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 // Wait for the phase with the given parity to complete.  Bounded: after ~4 s the
 // kernel traps instead of hanging the GPU (a protocol bug must not wedge the box).
+#ifndef AUTOSP_MBAR_SPIN
+#define AUTOSP_MBAR_SPIN 0  // 1: every wait busy-polls with test_wait (A/B option)
+#endif
+AUTOSP_DEV bool mbar_test_wait(uint64_t* bar, uint32_t parity);
+AUTOSP_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity);
 AUTOSP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (AUTOSP_MBAR_SPIN) return mbar_wait_spin(bar, parity);
   if (mbar_try_wait(bar, parity)) return;
   uint64_t t0 = globaltimer();
   while (!mbar_try_wait(bar, parity)) {
