@@ -44,6 +44,10 @@ extern "C" void autosp_set_error(const char* fmt, ...);
 #ifndef AUTOSP_FWD_EARLY_K
 #define AUTOSP_FWD_EARLY_K 1  // wait for K_{j+1} before s_free (off the hand-off path)
 #endif
+#ifndef AUTOSP_FWD_LATE_V
+#define AUTOSP_FWD_LATE_V 1  // d = 128: MMA warp checks V_j just before PV(j), not at the top
+                             // of step j (A/B: +1.3 % at d = 128, -0.7 % at d = 64: d > 64 only)
+#endif
 #ifndef AUTOSP_FWD_LPT
 #define AUTOSP_FWD_LPT 1  // LPT grid layout (ptx.cuh; A/B: +1.6 % full shape, +37 % at 4 heads x 16K)
 #endif
@@ -304,8 +308,17 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
         const bool next = j + 1 < n_max;
         const int st1 = (j + 1) % C::kStages;
         const uint32_t ph1 = ((j + 1) / C::kStages) & 1;
-        mbar_wait(v_full + st, ph);
-        if (lane == 0 && i_lo == 0) FWD_TRACE(14, j);
+        // V_j is only needed by PV_i(j): AUTOSP_FWD_LATE_V checks it there, so the warp goes
+        // from PV_i(j-1) straight to the s_free wait that gates QK_i(j+1)
+        bool v_ready = false;
+        auto need_v = [&]() {
+          if (!v_ready) {
+            mbar_wait(v_full + st, ph);
+            if (lane == 0 && i_lo == 0) FWD_TRACE(14, j);
+            v_ready = true;
+          }
+        };
+        if (!(AUTOSP_FWD_LATE_V && D > 64)) need_v();
         bool k_next_ready = false;
         auto need_k_next = [&]() {
           if (!k_next_ready) {
@@ -331,6 +344,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
             issue_qk(i, j + 1);
             if (lane == 0 && i == 0) FWD_TRACE(13, j);
           }
+          need_v();
           mbar_wait(p_full + i, j & 1);
           if (lane == 0) FWD_TRACE(0 + i, j);
           tc_fence_after();
@@ -341,6 +355,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
             issue_qk(i, j + 1);
           }
         }
+        need_v();  // (a warp with no tile left at j still observes the phase it releases)
         commit(v_empty + st);
         if (next) {
           if (!k_next_ready) mbar_wait(k_full + st1, ph1);  // unused K_{j+1}: still release
