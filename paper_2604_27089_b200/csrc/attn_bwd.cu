@@ -98,19 +98,6 @@ struct Cfg {
   static constexpr int kDOStages = D == 128 ? 1 : 2;
   // S^T buffers in TMEM: two (S(t+1) overlaps the softmax of t) when d <= 64
   static constexpr int NSB = D == 128 ? 1 : 2;
-  // d <= 64: the two softmax-grad warpgroups split the WORK, not the query columns --
-  // WG1 computes P^T of step t (all 128 columns) while WG2 computes dS^T of step t-1
-  // (reading P^T back from TMEM), so neither waits on the other's half of the chain
-#ifndef AUTOSP_BWD_PIPE
-#define AUTOSP_BWD_PIPE 0  // measured 4-6 % slower (profiles/ab_bwd_pipe_r02.txt): off
-#endif
-#ifndef AUTOSP_BWD_DKLATE
-#define AUTOSP_BWD_DKLATE 1  // kPipe: dK(t) issued after S^T(t+1) of the next step
-#endif
-#ifndef AUTOSP_BWD_SPIN
-#define AUTOSP_BWD_SPIN 1  // kPipe: busy-poll the waits on the dS -> dQ -> S^T(t+2) chain
-#endif
-  static constexpr bool kPipe = AUTOSP_BWD_PIPE && NSB == 2;
   // exps per 8 done on the FMA pipe (part 1 is MUFU-bound at 16 exp/clk/SM)
   static constexpr int kEmuPer8 = D == 128 ? AUTOSP_BWD_EMU128 : AUTOSP_BWD_EMU;
   static constexpr int K_OFF = 0;
@@ -123,8 +110,7 @@ struct Cfg {
 #define AUTOSP_BWD_DQSLOTS64 2
 #endif
   static constexpr int DQS = D <= 64 ? AUTOSP_BWD_DQSLOTS64 : 2;
-  static constexpr int NDS = kPipe ? 2 : 1;  // dS^T smem tiles (kPipe: dK reads it too)
-  static constexpr int DQ_OFF = DS_OFF + NDS * 128 * 128 * 2;
+  static constexpr int DQ_OFF = DS_OFF + 128 * 128 * 2;
   static constexpr int LSE_OFF = DQ_OFF + DQS * 128 * 32 * 4;  // lse[kQStages][128], delta[kQStages][128]
   static constexpr int BAR_OFF = LSE_OFF + 2 * kQStages * 128 * 4;
   // dynamic smem starts 1024-aligned when the kernel has no static smem (measured:
@@ -222,22 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   uint64_t* acc_full = dq_empty + 1;            // final dK/dV complete
   uint64_t* do_full = acc_full + 1;             // [kDOStages] dO(t) in smem
   uint64_t* do_empty = do_full + C::kDOStages;  // [kDOStages] dP(t), dV(t) done with it
-  uint64_t* p_ready2 = do_empty + C::kDOStages;  // kPipe: P^T of odd steps (even: p_ready)
-  uint64_t* ds_ready2 = p_ready2 + 1;              // kPipe: dS of odd steps (even: ds_ready)
-  uint64_t* dp_free = ds_ready2 + 1;               // kPipe: WG2 holds dP^T(t) in registers
-  uint64_t* ds_free = dp_free + 1;                 // kPipe: [2] dQ(t)/dK(t) done with tile t%2
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ds_free + 2);
-  // P^T(t) written: kPipe alternates two barriers (WG2 may trail WG1 by a step, so one
-  // barrier's phase could run two ahead of a waiter); else one barrier per step
-  auto p_bar = [&](int t) { return (C::kPipe && (t & 1)) ? p_ready2 : p_ready; };
-  auto ds_bar = [&](int t) { return (C::kPipe && (t & 1)) ? ds_ready2 : ds_ready; };
-  auto p_par = [&](int t) -> uint32_t { return C::kPipe ? (t >> 1) & 1 : t & 1; };
-  // kPipe: the step period is the chain dS(t) -> dK/dQ(t) -> drain -> S^T(t+2) -> P^T(t+2)
-  // -> dS(t+2); its waits poll instead of suspending (try_wait wakes up late)
-  auto chain_wait = [&](uint64_t* bar, uint32_t par) {
-    if (C::kPipe && AUTOSP_BWD_SPIN) mbar_wait_spin(bar, par);
-    else mbar_wait(bar, par);
-  };
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(do_empty + C::kDOStages);
   float* lse_s = reinterpret_cast<float*>(smem + C::LSE_OFF);  // [kQStages][128]
   float* dlt_s = lse_s + C::kQStages * 128;                                   // [kQStages][128]
 
@@ -267,13 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     mbar_init(s_full + 0, 1);
     mbar_init(s_full + 1, 1);
     mbar_init(dp_full, 1);
-    mbar_init(p_ready, C::kPipe ? 4 : 8);  // one arrival per softmax warp (kPipe: WG1)
-    mbar_init(p_ready2, 4);
-    mbar_init(ds_ready2, 4);
-    mbar_init(dp_free, 4);
-    mbar_init(ds_free + 0, 1);
-    mbar_init(ds_free + 1, 1);
-    mbar_init(ds_ready, C::kPipe ? 4 : 8);  // (kPipe: WG2)
+    mbar_init(p_ready, 8);     // one arrival per softmax warp
+    mbar_init(ds_ready, 8);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 4);
     mbar_init(acc_full, 1);
@@ -387,93 +353,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         __syncwarp();
       };
       mbar_wait(kv_full, 0);
-      if constexpr (C::kPipe) {
-        // d <= 64 (kPipe): dK(t) reads dS^T from the (double-buffered) smem tile, so dP(t+1)
-        // only waits for WG2 to have LOADED dP(t) (dp_free) and runs under the dS math of
-        // t; S^T(t+1) waits for the drain of dQ(t-1), the other tenant of its TMEM buffer.
-        const uint64_t dsa_k = make_smem_desc(s_ds, 16, 1024, 2);  // dS^T tile, K-major (keys)
-        // dK(t) += dS^T(t) Q(t) (elected lane); releases Q stage t and dS tile t%2
-        auto issue_dk = [&](int t) {
-          const int st = t % C::kQStages;
-          const uint64_t dq_mn = make_smem_desc(s_q + st * C::TILE, 128 * C::SW, C::SBO, C::LAYOUT);
-          const uint64_t ds_off = (uint64_t)(((t & 1) * 128 * 128 * 2) >> 4);
-#pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk)
-            mma_ss(tmem + C::DK_COL, dsa_k + ds_off + kmajor_off<64>(kk),
-                   dq_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_g, kk > 0 || t > 0 ? 1u : 0u);
-          tc_commit(q_empty + st);
-          tc_commit(ds_free + (t & 1));  // dQ(t) and dK(t) are done with dS tile t%2
-        };
-        wait_q(0);
-        issue_s(0);
-        issue_dp(0);
-        if (T > 1) {
-          wait_q(1);
-          issue_s(1);
-        }
-        for (int t = 0; t < T; ++t) {
-          const int st = t % C::kQStages;
-          const uint64_t dq_mn = make_smem_desc(s_q + st * C::TILE, 128 * C::SW, C::SBO, C::LAYOUT);
-          const uint64_t ddo_mn = make_smem_desc(s_do + (t % C::kDOStages) * C::TILE, 128 * C::SW,
-                                                 C::SBO, C::LAYOUT);
-          const uint32_t acc0 = t > 0 ? 1u : 0u;
-          // S^T(t+1) into buffer (t+1)%2 once dQ(t-1) has left it (Q(t+1) checked first: an
-          // mbarrier check costs this warp 100-300 cycles even when already complete)
-          if (t >= 1 && t + 1 < T) {
-            wait_q(t + 1);
-            chain_wait(dq_empty, (t - 1) & 1);
-            if (lane == 0) BWD_TRACE(0, t);
-            tc_fence_after();
-            issue_s(t + 1);
-            if (lane == 0) BWD_TRACE(13, t);
-          }
-          // deferred dK(t-1): off the dQ(t-1) -> drain -> S^T(t+1) chain (it only gates the
-          // reuse of dS tile (t-1)%2 and Q stage t-1)
-          if (AUTOSP_BWD_DKLATE && t >= 1) {
-            if (elect_one()) issue_dk(t - 1);
-            __syncwarp();
-          }
-          // dV += P^T dO once WG1 has written P^T(t)
-          chain_wait(p_bar(t), p_par(t));
-          if (lane == 0) BWD_TRACE(2, t);
-          tc_fence_after();
-          const uint32_t s_col = (t % C::NSB) * 128;
-          if (elect_one()) {
-#pragma unroll
-            for (int kk = 0; kk < BQ / 16; ++kk)
-              mma_ts(tmem + C::DV_COL, tmem + s_col + pk_col(kk),
-                     ddo_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_g, kk > 0 ? 1u : acc0);
-            tc_commit(do_empty + (t % C::kDOStages));  // dP(t) and dV(t) are done with dO(t)
-          }
-          __syncwarp();
-          // dP^T(t+1) as soon as WG2 holds dP^T(t) in registers
-          if (t + 1 < T) {
-            chain_wait(dp_free, t & 1);
-            tc_fence_after();
-            issue_dp(t + 1);
-            if (lane == 0) BWD_TRACE(1, t);
-          }
-          // dQ(t) = dS K and dK += dS^T Q from the smem dS tile t%2 (dQ first: its drain
-          // gates S^T(t+2))
-          chain_wait(ds_bar(t), p_par(t));
-          if (lane == 0) BWD_TRACE(3, t);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint64_t ds_off = (uint64_t)(((t & 1) * 128 * 128 * 2) >> 4);
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk)
-              mma_ss(tmem + dq_col(t), dds + ds_off + (uint64_t)((kk * 16 * 128) >> 4),
-                     dk_mn + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_q, kk > 0);
-            tc_commit(dq_full);
-            if (!AUTOSP_BWD_DKLATE) issue_dk(t);
-          }
-          __syncwarp();
-          if (lane == 0) BWD_TRACE(4, t);
-        }
-        if (AUTOSP_BWD_DKLATE && T > 0 && elect_one()) issue_dk(T - 1);
-        __syncwarp();
-        chain_wait(dp_free, (T - 1) & 1);  // (every phase is observed: sanitizer-clean)
-      } else {
       wait_q(0);
       issue_s(0);
       for (int t = 0; t < T; ++t) {
@@ -548,7 +427,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         __syncwarp();
         if (lane == 0) BWD_TRACE(4, t);
       }
-      }
       if (elect_one()) tc_commit(acc_full);
       __syncwarp();
       mbar_wait(dq_empty, (T - 1) & 1);  // the last drain (no phase is left unobserved)
@@ -567,7 +445,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     uint8_t* ds_row = smem + C::DS_OFF + half * (128 * 128) + row * 128;
     const uint64_t sl2 = f2_pack(p.scale_log2, p.scale_log2);
     const bool row_dead = key >= p.S;
-    if constexpr (!C::kPipe) {
     for (int t = 0; t < T; ++t) {
       const int head = kvh * group + (SPLIT ? (int)(BWD_HEAD_IDX % HS) * gsz : 0) + t / per_head;
       const int q0 = (m_first + t % per_head) * BQ;
@@ -697,152 +574,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       mbar_arrive_warp(ds_ready);
       if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(8, t);
     }
-    } else {
-    // kPipe (d <= 64): WG1 (half 0) turns S^T(t) into P^T(t) for all 128 query columns and
-    // moves on to S^T(t+1) (the other S buffer); WG2 (half 1) reads P^T(t) back from TMEM
-    // with dP^T(t) and writes dS^T(t).  Per column half h the packed bf16 values land in the
-    // columns that half read (pk_col): S / dP cols [0, 64) -> [0, 32), [64, 128) -> [96, 128).
-    const bool wg1 = half == 0;
-    for (int t = 0; t < T; ++t) {
-      const int head = kvh * group + (SPLIT ? (int)(BWD_HEAD_IDX % HS) * gsz : 0) + t / per_head;
-      const int q0 = (m_first + t % per_head) * BQ;
-      const uint32_t s_addr = tmem + lane_base + (t % C::NSB) * 128;
-      const int st = t % C::kQStages;
-      const float* lse_b = lse_s + st * 128;
-      const float* dlt_b = dlt_s + st * 128;
-      if (!p.lse_tma) {  // S % 4 != 0: each warpgroup stages the row it reads (slow path)
-        const uint32_t bar_id = wg1 ? 1 : 3;
-        if (t >= C::kQStages) named_bar_sync(bar_id, 128);  // everyone done with this slot
-        const int q = q0 + row;
-        const int64_t idx = ((int64_t)batch * p.Hq + head) * p.S + q;
-        if (wg1) lse_s[st * 128 + row] = q < p.S ? p.lse[idx] : 0.f;
-        else dlt_s[st * 128 + row] = q < p.S ? p.delta[idx] : 0.f;
-        named_bar_sync(bar_id, 128);
-      }
-      const bool masked = (p.causal && (q0 < k0 + BK)) || (k0 + BK > p.S) || (q0 + BQ > p.S);
-      const int col_lo = p.causal ? key - q0 : -1;  // col < col_lo -> masked (q < key)
-      const int col_hi = min(p.S - q0, BQ);          // col >= col_hi -> masked (q >= S)
-      if (wg1) {
-        if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(12, t);
-        chain_wait(s_full + (t % C::NSB), (t / C::NSB) & 1);
-        if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(5, t);
-        tc_fence_after();
-        auto part1 = [&](auto kMasked) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t sr2[2][32];  // the half's two 32-column chunks: one TMEM round trip
-            tmem_ld32(s_addr + (h * 2) * 32, sr2[0]);
-            tmem_ld32(s_addr + (h * 2 + 1) * 32, sr2[1]);
-            tmem_wait_ld();
-#pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-              const int c4 = h * 2 + cc;
-              const uint32_t* sr = sr2[cc];
-              const float4* l4 = reinterpret_cast<const float4*>(lse_b + c4 * 32);
-              uint32_t pk[16];
-#pragma unroll
-              for (int c8 = 0; c8 < 8; ++c8) {
-                const float4 l = lds128(l4 + c8);  // broadcast LDS.128
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                  const int c = c8 * 2 + hh;
-                  const uint64_t lz = hh ? f2_pack(l.z, l.w) : f2_pack(l.x, l.y);
-                  const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(sr[2 * c]),
-                                                     __uint_as_float(sr[2 * c + 1])),
-                                             sl2, lz);
-                  float e0, e1;
-                  if (!decltype(kMasked)::value && (c & 7) >= 8 - C::kEmuPer8) {
-                    f2_unpack(f2_exp2_poly(x2), e0, e1);
-                  } else {
-                    float x0, x1;
-                    f2_unpack(x2, x0, x1);
-                    e0 = AUTOSP_BWD_ABL == 3 ? x0 : fast_exp2(x0);
-                    e1 = AUTOSP_BWD_ABL == 3 ? x1 : fast_exp2(x1);
-                  }
-                  if constexpr (decltype(kMasked)::value) {
-                    const int col = c4 * 32 + 2 * c;
-                    e0 = (row_dead || col < col_lo || col >= col_hi) ? 0.f : e0;
-                    e1 = (row_dead || col + 1 < col_lo || col + 1 >= col_hi) ? 0.f : e1;
-                  }
-                  pk[c] = pack_bf16(e0, e1);
-                }
-              }
-              tmem_st16(s_addr + h * 96 + cc * 16, pk);
-            }
-          }
-        };
-        if (masked) part1(std::true_type{});
-        else part1(std::false_type{});
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive_warp(p_bar(t));
-        if (threadIdx.x == kSoftWarp0 * 32) BWD_TRACE(6, t);
-      } else {
-        chain_wait(p_bar(t), p_par(t));
-        mbar_wait(dp_full, t & 1);
-        // dS tile t%2 was last read by dQ(t-2) / dK(t-2)
-        if (t >= 2) mbar_wait(ds_free + (t & 1), ((t >> 1) & 1) ^ 1);
-        if (threadIdx.x == (kSoftWarp0 + 4) * 32) BWD_TRACE(7, t);
-        tc_fence_after();
-        auto part2 = [&](auto kMasked) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint8_t* dsr = smem + C::DS_OFF + (t & 1) * (128 * 128 * 2) + h * (128 * 128) + row * 128;
-#pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-              const int c4 = h * 2 + cc;
-              uint32_t pkc[16], dr[32];  // one chunk per TMEM round trip (registers)
-              tmem_ld16(s_addr + h * 96 + cc * 16, pkc);
-              tmem_ld32(dp_addr + c4 * 32, dr);
-              tmem_wait_ld();
-              if (c4 == 3) {  // all of dP^T(t) read: the MMA warp may issue dP^T(t+1)
-                tc_fence_before();
-                mbar_arrive_warp(dp_free);
-              }
-              uint32_t dk[16];
-              const float4* d4 = reinterpret_cast<const float4*>(dlt_b + c4 * 32);
-#pragma unroll
-              for (int c8 = 0; c8 < 8; ++c8) {
-                float4 dl = lds128(d4 + c8);
-                if constexpr (decltype(kMasked)::value) {  // rows past S (slow path garbage)
-                  const int col = c4 * 32 + 4 * c8;
-                  dl.x = col + 0 < col_hi ? dl.x : 0.f;
-                  dl.y = col + 1 < col_hi ? dl.y : 0.f;
-                  dl.z = col + 2 < col_hi ? dl.z : 0.f;
-                  dl.w = col + 3 < col_hi ? dl.w : 0.f;
-                }
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                  const int c = c8 * 2 + hh;
-                  const uint64_t dd = f2_add(f2_pack(__uint_as_float(dr[2 * c]),
-                                                     __uint_as_float(dr[2 * c + 1])),
-                                             hh ? f2_pack(-dl.z, -dl.w) : f2_pack(-dl.x, -dl.y));
-                  float a, b;
-                  f2_unpack(dd, a, b);
-                  dk[c] = bf16x2_mul(pkc[c], pack_bf16(a, b));
-                }
-              }
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int unit = cc * 4 + u;
-                if (AUTOSP_BWD_ABL != 2 && AUTOSP_BWD_ABL != 4)
-                  sts128(dsr + ((unit ^ (row & 7)) << 4),
-                         make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
-              }
-            }
-          }
-        };
-        if (masked) part2(std::true_type{});
-        else part2(std::false_type{});
-        fence_proxy_async_smem();
-        tc_fence_before();
-        mbar_arrive_warp(ds_bar(t));
-        if (threadIdx.x == (kSoftWarp0 + 4) * 32) BWD_TRACE(8, t);
-      }
-    }
-    if (!wg1)  // the last two dS tiles' release (every phase is observed: sanitizer-clean)
-      for (int t = T > 2 ? T - 2 : 0; t < T; ++t) mbar_wait(ds_free + (t & 1), (t >> 1) & 1);
-    }
     // ---- epilogue: dV (WG1) / dK scaled (WG2) straight from TMEM
     if (T > 0) {
       mbar_wait(acc_full, 0);
@@ -914,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       // the slot of chunk 0 was last used two chunks ago: wait for that reduce to have
       // read it BEFORE dQ(t) arrives, off the critical path (dP(t+1) waits for the drain)
       if (leader) bulk_wait_read_n<C::DQS - 1>();
-      chain_wait(dq_full, t & 1);
+      mbar_wait(dq_full, t & 1);
       if (threadIdx.x == kDrainWarp0 * 32) BWD_TRACE(9, t);
       tc_fence_after();
       // stage one 32-column chunk through a smem slot and TMA-reduce it into dQacc
