@@ -144,11 +144,21 @@ struct Params {
   uint32_t epoch, check;
 };
 constexpr int kTraceSteps = 64;
-#define FWD_TRACE(ev, t)                                                                   \
+#define FWD_TRACE_RAW(ev, t)                                                               \
   do {                                                                                     \
     if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (t) < kTraceSteps) \
       p.trace[(ev) * kTraceSteps + (t)] = clock64();                                       \
   } while (0)
+#ifndef AUTOSP_FWD_TRACE_SKEW
+#define AUTOSP_FWD_TRACE_SKEW 0  // tools only (fwd_skew_trace.py): per-warp S release / P arrival
+#endif
+#if AUTOSP_FWD_TRACE_SKEW
+#define FWD_TRACE(ev, t) do { if ((ev) == 4 || (ev) == 5) FWD_TRACE_RAW(ev, t); } while (0)
+#define FWD_TRACE_SKEW(base, t) do { if (lane == 0 && warp < 4) FWD_TRACE_RAW((base) + warp, t); } while (0)
+#else
+#define FWD_TRACE(ev, t) FWD_TRACE_RAW(ev, t)
+#define FWD_TRACE_SKEW(base, t) do { } while (0)
+#endif
 long long* g_fwd_trace = nullptr;
 
 // byte offset >> 4 of K-step kk inside a K-major tile of ROWS rows stored as NCH swizzled
@@ -448,6 +458,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
             tc_fence_before();
             mbar_arrive_warp(s_free + i);
             if (lane == 0 && warp == 0) FWD_TRACE(15, j);
+            FWD_TRACE_SKEW(6, j);  // events 6..9: warps 0..3 release S_0(j)
           }
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
@@ -487,6 +498,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
           tc_fence_before();
           mbar_arrive_warp(p_full + i);
           if (lane == 0 && (warp & 3) == 0) FWD_TRACE(6 + i, j);
+          FWD_TRACE_SKEW(10, j);  // events 10..13: warps 0..3 arrive P_0(j)
           continue;
         }
       }
@@ -536,6 +548,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
             tc_fence_before();
             mbar_arrive_warp(s_free + i);
             if (lane == 0 && warp == 0) FWD_TRACE(15, j);
+            FWD_TRACE_SKEW(6, j);  // events 6..9: warps 0..3 release S_0(j)
           }
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
