@@ -48,6 +48,15 @@ extern "C" void autosp_set_error(const char* fmt, ...);
 #define AUTOSP_FWD_LATE_V 1  // d = 128: MMA warp checks V_j just before PV(j), not at the top
                              // of step j (A/B: +1.3 % at d = 128, -0.7 % at d = 64: d > 64 only)
 #endif
+#ifndef AUTOSP_FWD_MMA4
+#define AUTOSP_FWD_MMA4 1  // d <= 64: one MMA stream per SMSP (see Cfg); A/B: +3.4 % at d = 64
+#endif
+#ifndef AUTOSP_FWD_MMA4_VROLE
+#define AUTOSP_FWD_MMA4_VROLE 2  // MMA4: the QK stream (0 or 2) that issues the V loads (A/B: 2 > 0)
+#endif
+#ifndef AUTOSP_FWD_KVRING64_MMA4
+#define AUTOSP_FWD_KVRING64_MMA4 163840  // MMA4: 5 K/V stages (loads issued one tile later)
+#endif
 #ifndef AUTOSP_FWD_LPT
 #define AUTOSP_FWD_LPT 1  // LPT grid layout (ptx.cuh; A/B: +1.6 % full shape, +37 % at 4 heads x 16K)
 #endif
@@ -86,18 +95,25 @@ struct Cfg {
   // single-thread producers (TMA, MMA) get the top ids and are never starved by the
   // instruction-heavy softmax warpgroups (whole, aligned warpgroups for TMEM lanes).
   static constexpr int kAllocWarp = 4 * NQ;
-  static constexpr int kTmaWarp = 4 * NQ + 2;
+  static constexpr int kTmaWarp = 4 * NQ + ((AUTOSP_FWD_MMA4 && NQ == 2 && D <= 64) ? 0 : 2);
   static constexpr int kMmaWarp = 4 * NQ + 3;
   // AUTOSP_FWD_MMA2 (NQ = 2): warp 4NQ+1 issues tile 0's MMAs, kMmaWarp tile 1's -- each
   // tile's QK / PV wait only on its own softmax; the K/V stages are released by both
-  static constexpr bool MMA2 = AUTOSP_FWD_MMA2 && NQ == 2 && D <= 64;
+  static constexpr bool MMA2 = AUTOSP_FWD_MMA2 && !AUTOSP_FWD_MMA4 && NQ == 2 && D <= 64;
   static constexpr int kMmaWarp2 = 4 * NQ + 1;
+  // AUTOSP_FWD_MMA4 (NQ = 2, d <= 64): the four MMA streams QK_0, PV_0, QK_1, PV_1 issued by
+  // warps 4NQ+0..3 -- one per SMSP, so the issue stalls of tcgen05.mma (it blocks while the
+  // pipe is busy) fall evenly on the softmax warps; warp 4NQ also allocates TMEM and runs
+  // the TMA loads (each load issued once the stage's previous tile is released)
+  static constexpr bool MMA4 = AUTOSP_FWD_MMA4 && NQ == 2 && D <= 64;
   static constexpr int SW = (D * 2 >= 128) ? 128 : D * 2;  // swizzle bytes
   static constexpr int CE = SW / 2;                         // elements per swizzle chunk
   static constexpr int NCH = D / CE;                        // chunks per row
   static constexpr int TILE_BYTES = BM * D * 2;             // Q tile: 128 x D bf16
   static constexpr int KTILE = BN * D * 2;                  // K / V tile: BN x D bf16
-  static constexpr int KV_RING = D == 128 ? 131072 : AUTOSP_FWD_KVRING64;  // bytes of K+V stages
+  static constexpr int KV_RING = D == 128 ? 131072
+                                : ((AUTOSP_FWD_MMA4 && NQ == 2) ? AUTOSP_FWD_KVRING64_MMA4
+                                                                : AUTOSP_FWD_KVRING64);
   static constexpr int kStagesRaw = KV_RING / (2 * KTILE);
   static constexpr int kStages = kStagesRaw < 2 ? 2 : (kStagesRaw > 8 ? 8 : kStagesRaw);
   // exps per 8 computed by the FMA-pipe polynomial instead of MUFU (MUFU is the
@@ -210,9 +226,9 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
     mbar_init(q_full, 1);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(k_full + s, 1);
-      mbar_init(k_empty + s, C::MMA2 ? 2 : 1);
+      mbar_init(k_empty + s, (C::MMA2 || C::MMA4) ? 2 : 1);
       mbar_init(v_full + s, 1);
-      mbar_init(v_empty + s, C::MMA2 ? 2 : 1);
+      mbar_init(v_empty + s, (C::MMA2 || C::MMA4) ? 2 : 1);
     }
     for (int i = 0; i < NQ; ++i) {
       mbar_init(s_full + i, 1);
@@ -234,7 +250,120 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
   const uint32_t sk = smem_u32(smem + C::K_OFF);
   const uint32_t sv = smem_u32(smem + C::V_OFF);
 
-  if (warp == kTmaWarp) {
+  if (C::MMA4 && warp >= 4 * NQ) {
+    // ------------------------------------------------------------ MMA4 producers
+    const int role = warp - 4 * NQ;  // 0: loads + QK_0, 1: PV_0, 2: QK_1, 3: PV_1
+    const int i = role >> 1;
+    const bool is_qk = (role & 1) == 0;
+    if (n_max > 0) {
+      constexpr uint32_t idesc_qk = make_idesc_bf16(BM, BN, 0, 0);
+      constexpr uint32_t idesc_pv = make_idesc_bf16(BM, D, 0, 1);
+      const uint64_t pol_kv = policy_evict_last();
+      auto load_k = [&](int L) {  // lane 0
+        const int st = L % C::kStages;
+        if (L >= C::kStages) mbar_wait(k_empty + st, ((L / C::kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(k_full + st, C::KTILE);
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_4d(smem + C::K_OFF + st * C::KTILE + c * BN * C::SW, &p.tm_k, k_full + st,
+                      c * C::CE, L * BN, kvhead, batch, pol_kv);
+      };
+      auto load_v = [&](int L) {  // lane 0
+        const int st = L % C::kStages;
+        if (L >= C::kStages) mbar_wait(v_empty + st, ((L / C::kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(v_full + st, C::KTILE);
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_4d(smem + C::V_OFF + st * C::KTILE + c * BN * C::SW, &p.tm_v, v_full + st,
+                      c * C::CE, L * BN, kvhead, batch, pol_kv);
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) tc_commit(bar);
+        __syncwarp();
+      };
+      if (role == 0) {
+        if (lane == 0) {
+          const uint64_t pol_q = policy_evict_first();
+          int nq_live = 0;
+          for (int t = 0; t < NQ; ++t) nq_live += (q0 + t * BM < p.S) ? 1 : 0;
+          mbar_arrive_expect_tx(q_full, nq_live * C::TILE_BYTES);
+          for (int t = 0; t < nq_live; ++t)
+            for (int c = 0; c < C::NCH; ++c)
+              tma_load_4d(smem + C::Q_OFF + t * C::TILE_BYTES + c * BM * C::SW, &p.tm_q, q_full,
+                          c * C::CE, q0 + t * BM, head, batch, pol_q);
+          for (int L = 0; L < C::kStages && L < n_max; ++L) {
+            load_k(L);
+            load_v(L);
+          }
+        }
+        __syncwarp();
+      }
+      if (is_qk) {
+        auto issue_qk = [&](int j) {
+          const int st = j % C::kStages;
+          const uint64_t da = make_smem_desc(sq + i * C::TILE_BYTES, 16, C::SBO, C::LAYOUT);
+          const uint64_t db = make_smem_desc(sk + st * C::KTILE, 16, C::SBO, C::LAYOUT);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+              mma_ss(tmem + C::S_COL + i * BN, da + kmajor_off<D, BM>(kk),
+                     db + kmajor_off<D, BN>(kk), idesc_qk, kk > 0);
+            tc_commit(s_full + i);
+          }
+          __syncwarp();
+        };
+        mbar_wait(q_full, 0);
+        mbar_wait(k_full + 0, 0);
+        tc_fence_after();
+        if (n_tiles[i] > 0) issue_qk(0);
+        commit(k_empty + 0);
+        for (int j = 0; j < n_max; ++j) {
+          // K of tile j + kStages - 1 into the stage tile j - 1 used (released by both QK
+          // streams long ago); V follows after this step's QK
+          const int L = j + C::kStages - 1;
+          if (role == 0 && j >= 1 && L < n_max) {
+            if (lane == 0) load_k(L);
+            __syncwarp();
+          }
+          if (j + 1 < n_max) {
+            const int st1 = (j + 1) % C::kStages;
+            mbar_wait(k_full + st1, ((j + 1) / C::kStages) & 1);
+            tc_fence_after();
+            if (j + 1 < n_tiles[i]) {
+              mbar_wait(s_free + i, j & 1);  // S_i(j) read: S_i(j+1) may overwrite it
+              tc_fence_after();
+              issue_qk(j + 1);
+            }
+            commit(k_empty + st1);
+          }
+          if (role == AUTOSP_FWD_MMA4_VROLE && j >= 1 && L < n_max) {
+            if (lane == 0) load_v(L);
+            __syncwarp();
+          }
+        }
+      } else {
+        for (int j = 0; j < n_max; ++j) {
+          const int st = j % C::kStages;
+          mbar_wait(v_full + st, (j / C::kStages) & 1);
+          if (j < n_tiles[i]) {
+            mbar_wait(p_full + i, j & 1);
+            tc_fence_after();
+            const uint64_t dv = make_smem_desc(sv + st * C::KTILE, BN * C::SW, C::SBO, C::LAYOUT);
+            const uint32_t pa = tmem + C::P_COL + i * C::P_STRIDE;
+            const uint32_t oa = tmem + C::O_COL + i * D;
+            const uint32_t acc0 = j > 0 ? 1u : 0u;
+            if (elect_one()) {
+#pragma unroll
+              for (int kk = 0; kk < BN / 16; ++kk)
+                mma_ts(oa, pa + kk * 8, dv + (uint64_t)((kk * 16 * C::SW) >> 4), idesc_pv,
+                       kk > 0 ? 1u : acc0);
+              tc_commit(o_done + i);
+            }
+            __syncwarp();
+          }
+          commit(v_empty + st);
+        }
+      }
+    }
+  } else if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && n_max > 0) {
       const uint64_t pol_q = policy_evict_first();
