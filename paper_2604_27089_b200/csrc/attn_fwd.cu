@@ -51,6 +51,9 @@ extern "C" void autosp_set_error(const char* fmt, ...);
 #ifndef AUTOSP_FWD_MMA4
 #define AUTOSP_FWD_MMA4 1  // d <= 64: one MMA stream per SMSP (see Cfg); A/B: +3.4 % at d = 64
 #endif
+#ifndef AUTOSP_FWD_MMA4_KROLE
+#define AUTOSP_FWD_MMA4_KROLE 0  // MMA4: the QK stream (0 or 2) that issues the K loads
+#endif
 #ifndef AUTOSP_FWD_MMA4_VROLE
 #define AUTOSP_FWD_MMA4_VROLE 2  // MMA4: the QK stream (0 or 2) that issues the V loads (A/B: 2 > 0)
 #endif
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(Cfg<D>::kThreads, 1) attn_fwd_kernel(const __g
           // K of tile j + kStages - 1 into the stage tile j - 1 used (released by both QK
           // streams long ago); V follows after this step's QK
           const int L = j + C::kStages - 1;
-          if (role == 0 && j >= 1 && L < n_max) {
+          if (role == AUTOSP_FWD_MMA4_KROLE && j >= 1 && L < n_max) {
             if (lane == 0) load_k(L);
             __syncwarp();
           }
